@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: parameter-assignment evaluations/s (amplitudes/s) on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one pass of the hot path over one batch: evaluating the config's
+assignment batch (C2 default: all 2^20 output-bitstring assignments, P = 20)
+against the config's synthetic term table (2^17 terms, 4.2e6 subterm rows).
+
+ours (default):
+  * value  -- device-resident: the rank's assignments are evaluated from HBM
+              into HBM buffers (amplitudes + |amp|^2), timed with CUDA events on
+              the launching stream, one event pair per step, L2 flushed between
+              steps (256 MiB memset outside the events), max over ranks.
+  * e2e    -- the public API a user calls (Context.evaluate_batch -> C ABI
+              pzx_evaluate) with HOST buffers: pinned assignment words H2D, the
+              kernel, amplitudes + probabilities D2H, every step, wall clock.
+  * roofline -- ALU (INT issue) bound per BASELINE.md §4: algorithmic work
+              W = N * (8 R + 16 m) int ops per launch over the measured kernel
+              time, against 148 SMs x 64 int32 lanes/clk x sm_max_mhz.
+  * cpu_baseline -- the reference's own CPU evaluator (oracle/_ref, built from
+              /root/reference) on all host threads, bounded sample of the same
+              workload (rank 0, N = 1 only).
+  Multi-GPU (torchrun): one process per GPU, each rank evaluates its own 2^20
+  assignment batch against a replicated table ("weak": per-GPU work fixed), no
+  collective on the data path.
+
+reference: rank 0 times the reference's CPU implementation of the path
+  (oracle/_ref) on the same config, bounded sample per step; other ranks exit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+INT_LANES_PER_SM = 64      # LOP3/IADD3 int32 lanes per clock per SM (sm_100)
+N_SM = 148
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max((float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+# --------------------------------------------------------------------------
+def build_workload(cfg_name: str):
+    from paper_2403_06777_b200 import synth
+    cfg = synth.CONFIGS[cfg_name]
+    t0 = time.time()
+    expr = synth.generate_config(cfg)
+    log(f"[bench] {cfg.name}: {expr.n_terms} terms, {expr.n_subterms} subterms, generated in {time.time() - t0:.1f}s")
+    return cfg, expr
+
+
+def cpu_reference_rate(expr, cfg, seconds: float = 12.0, threads: int | None = None, step_sample=None):
+    """Reference CPU evaluator (oracle/_ref) on all host threads, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+    kind = "reference" if O.have_ref() else "port"
+    threads = threads or os.cpu_count() or 1
+    oe = O.OExpr(expr)
+    from paper_2403_06777_b200 import synth
+    words = synth.assignments(cfg, cfg.n_assign)
+    # calibrate on one assignment per thread, then size the sample to ~seconds
+    t0 = time.perf_counter()
+    O.eval_batch(oe, words[:threads], threads, impl="ref" if kind == "reference" else "port")
+    dt = time.perf_counter() - t0
+    per = dt  # seconds for `threads` assignments in parallel
+    n = step_sample or max(threads, int(threads * max(1, seconds / max(per, 1e-9))))
+    n = min(n, len(words))
+    sel = words[np.linspace(0, len(words) - 1, n).astype(np.int64)]
+    t0 = time.perf_counter()
+    O.eval_batch(oe, sel, threads, impl="ref" if kind == "reference" else "port")
+    el = time.perf_counter() - t0
+    return n / el, kind, threads, n, el
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, expr = build_workload(args.config)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+    from paper_2403_06777_b200 import synth
+    kind = "reference" if O.have_ref() else "port"
+    impl = "ref" if kind == "reference" else "port"
+    threads = os.cpu_count() or 1
+    oe = O.OExpr(expr)
+    words = synth.assignments(cfg, cfg.n_assign)
+    per_step = threads * max(1, args.ref_per_thread)
+    rng = np.random.default_rng(0)
+    times = []
+    for s in range(args.warmup + args.steps):
+        sel = words[rng.choice(len(words), per_step, replace=False)]
+        t0 = time.perf_counter()
+        O.eval_batch(oe, sel, threads, impl=impl)
+        el = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(el)
+    total = sum(times)
+    value = per_step * len(times) / total
+    line = {
+        "impl": "reference", "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
+        "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64 (exact Z[sqrt2,i])", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": expr.n_terms,
+                   "n_rows": int(expr.n_subterms), "n_assign": cfg.n_assign, "sample_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": kind,
+                         "sample": f"{per_step} assignments per step of the {cfg.n_assign}-assignment batch "
+                                   f"(random subset), full {expr.n_terms}-term table"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_06777_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    torch.cuda.set_device(dev)
+    peaks, peaks_kind = load_peaks()
+
+    cfg, expr = build_workload(args.config)
+    ctx = P.Context(dev)
+    t0 = time.time()
+    table = ctx.compile_bit_table(expr)
+    log(f"[bench] rank {rank}: table compiled+uploaded in {time.time() - t0:.1f}s "
+        f"({table.n_rows} rows, max {table.max_term_rows}/term)")
+    N = cfg.n_assign                        # per-rank batch (weak scaling)
+    first = rank * N
+    words_host = None
+    if not cfg.enumerated:
+        from paper_2403_06777_b200 import synth
+        words_host = synth.assignments(cfg, N, seed_offset=rank)
+    R, m = table.n_rows, table.n_terms
+
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    d_amp = torch.empty(2 * N, dtype=torch.float64, device=dev)
+    d_prob = torch.empty(N, dtype=torch.float64, device=dev)
+    d_words = torch.from_numpy(words_host.view(np.int64)).to(dev) if words_host is not None else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
+                            first=first, d_amp=d_amp.data_ptr(), d_prob=d_prob.data_ptr(),
+                            flags=P.PROB_REAL if cfg.prob_real else P.PROB_ABS2, stream=sh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident timed region --------------------------------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush outside the events
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * N * args.steps / (tot_ms / 1e3)
+
+    # ---- end to end through the public API (host buffers) -------------------
+    if words_host is None:
+        words_e2e = np.arange(first, first + N, dtype=np.uint64)
+    else:
+        words_e2e = words_host
+    pinned_w = torch.from_numpy(words_e2e.view(np.int64)).pin_memory()
+    pinned_amp = torch.empty(2 * N, dtype=torch.float64).pin_memory()
+    pinned_prob = torch.empty(N, dtype=torch.float64).pin_memory()
+    import ctypes as C
+    from paper_2403_06777_b200 import _native as NV
+    L = NV.lib()
+    fl = P.PROB_REAL if cfg.prob_real else P.PROB_ABS2
+
+    def e2e_step():
+        st = L.pzx_evaluate(ctx.handle, table.handle,
+                            C.cast(pinned_w.data_ptr(), C.POINTER(C.c_uint64)), N,
+                            C.cast(pinned_amp.data_ptr(), NV.dblp), C.cast(pinned_prob.data_ptr(), NV.dblp), fl)
+        if st:
+            raise RuntimeError(L.pzx_last_error(ctx.handle).decode())
+
+    e2e_step()
+    e2e_times = []
+    if world > 1:
+        dist.barrier()
+    for _ in range(max(1, args.steps)):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_tot = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = world * N * len(e2e_times) / e2e_tot
+    # sanity: e2e results equal the device-resident ones (same kernel, same words)
+    same = np.allclose(pinned_amp.numpy(), d_amp.cpu().numpy(), rtol=0, atol=0)
+
+    # ---- roofline (ALU / INT issue bound) -------------------
+    mean_ms = tot_ms / args.steps
+    w_row = 8 if cfg.n_params <= 32 else 12
+    work = N * (w_row * R + 16 * m)                    # algorithmic int ops per launch
+    f_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_tops = N_SM * INT_LANES_PER_SM * f_mhz * 1e6 / 1e12
+    achieved = work / (mean_ms / 1e3) / 1e12
+    row_evals = N * R / (mean_ms / 1e3)
+    table_bytes = R * 16 + m * 24
+    clocks = clk.summary()
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                v, kind, thr, n, el = cpu_reference_rate(expr, cfg, seconds=args.cpu_seconds)
+                cpu = {"value": v, "unit": "evals/s", "cores": thr, "kind": kind,
+                       "sample": f"{n} assignments (evenly spaced) of the {cfg.n_assign}-assignment batch, full "
+                                 f"{m}-term table, {el:.1f}s on {thr} threads"}
+            except Exception as ex:  # the baseline must not kill the GPU number
+                cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
+                       "sample": f"failed: {ex}"}
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        traffic = None
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(args.config)
+        except Exception:
+            pass
+        line = {
+            "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
+            "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32 exact exponent codes + fp64 term sum", "data": "synthetic",
+            "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": m, "n_rows": R,
+                       "assignments_per_gpu": N, "batch": "enumerated" if cfg.enumerated else "random",
+                       "l2": "flushed between timed steps (256 MiB memset outside the events)",
+                       "parallelism": f"assignment shards x{world}"},
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
+                    "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
+                         "frac": achieved / peak_tops, "traffic": traffic,
+                         "peak_source": f"148 SM x 64 int32 lanes/clk x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
+                                        "MEASURED_PEAKS.json clock; lane rate from the CUDA throughput table)",
+                         "work_per_launch": work, "row_evals_per_s": row_evals,
+                         "hbm_gbs_if_table_streamed_once": table_bytes / (mean_ms / 1e3) / 1e9},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    table.free()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-per-thread", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/*
+ * pzx_gpu.h -- C ABI of the B200 evaluator for the parametric sum-over-Cliffords
+ * scalar of arXiv 2403.06777:
+ *
+ *     S(a) = sum_i C_i * prod_j S_ij(a)            (PAPER Eq. 3)
+ *
+ * evaluated at many boolean parameter assignments a (output bitstrings,
+ * marginals, samples). This is the drop-in boundary for the reference's
+ * evaluate-on-assignments path; the entry points replace:
+ *
+ *   pzx_table_upload_expr  <- ZXDiagram leaf list (scalar_ + pending_ subterms,
+ *                             diagram.hpp:70-77, diagram.cpp:114-120) run
+ *                             through normalize_subterm (subterm.cpp:51-96) and
+ *                             SPEC compile_bit_table
+ *   pzx_table_upload       <- SPEC BitTable upload: already
+ *                             normalised phase-pair rows
+ *   pzx_evaluate           <- SPEC evaluate_batch(BitTable, AssignmentBatch)
+ *                             (S:475-483); per element it equals
+ *                             sum_i instantiate_diagram(leaf_i, a).scalar()
+ *                             (diagram.cpp:149-165) through to_complex
+ *                             (ring.cpp:131-136)
+ *   pzx_evaluate_range     <- the same over the enumerated batch first..first+n-1
+ *                             ("all 2^P amplitudes", strong_amplitude /
+ *                             marginal_summing sweeps)
+ *   pzx_debug_phase_indices<- instantiate_phase (phase.hpp:71-77) per (row, a)
+ *   pzx_debug_term_codes   <- the per-term product of subterm_value factors
+ *                             (diagram.cpp:158-161) in exact exponent form
+ *
+ * Conventions: no exceptions cross the ABI -- every call
+ * returns a pzx_status whose codes map the reference's pzx::Error hierarchy
+ * (common.hpp:13-48); validation happens at upload (k in [0,7], masks within
+ * the declared n_params <= 64 = kMaxParams, common.hpp:11); tables are
+ * immutable after upload; a context is driven by one host thread at a time;
+ * evaluation is a pure function of (table, assignments); output order equals
+ * input order. Assignment words follow ParamAssignment::total (phase.hpp:18-23):
+ * bit i = parameter i, bits >= n_params ignored.
+ *
+ * Plain pointers and sizes only; no CUDA or torch types in the signatures
+ * (streams are passed as void* = cudaStream_t, 0 = the context's stream).
+ */
+#ifndef PZX_GPU_H
+#define PZX_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PZX_OK = 0,
+    PZX_E_PARSE = 1,          /* pzx::ParseError        common.hpp:20-23 */
+    PZX_E_DOMAIN = 2,         /* pzx::DomainError       common.hpp:26-29 */
+    PZX_E_MISSING_PARAM = 3,  /* pzx::MissingParameter  common.hpp:45-48 */
+    PZX_E_OVERFLOW = 4,       /* pzx::OverflowError     common.hpp:39-42 */
+    PZX_E_INVALID = 5,        /* bad handle / argument (no reference analogue) */
+    PZX_E_CAPACITY = 6,       /* table shape outside what this build supports */
+    PZX_E_CUDA = 10,
+    PZX_E_NCCL = 11,
+    PZX_E_OOM = 12
+} pzx_status;
+
+/* SubtermKind, subterm.hpp:19 */
+enum { PZX_NODE = 0, PZX_PHASE_PAIR = 1, PZX_HALF_PI = 2, PZX_PI_PAIR = 3 };
+
+/* pzx_evaluate flags */
+enum {
+    PZX_PROB_ABS2 = 1u << 0,  /* prob[i] = |amp_i|^2 (Born rule)            */
+    PZX_PROB_REAL = 1u << 1,  /* prob[i] = Re(amp_i) (doubled diagram)      */
+    PZX_KERNEL_GENERAL = 1u << 8, /* force the per-assignment POPC kernel          */
+    PZX_KERNEL_GRAY = 1u << 9     /* force the enumerated (low-bit Walsh) kernel   */
+};
+
+typedef struct pzx_ctx pzx_ctx;
+typedef struct pzx_table pzx_table;
+
+/* Leaf-term list, i.e. what parametric reduction leaves behind: for term t the
+ * exact constant C_t (RingQuad a,b,c,d,exp; ring.hpp:17-38, value
+ * (a + b*sqrt2 + i(c + d*sqrt2)) * 2^-exp) times the product of the raw
+ * subterms [term_offset[t], term_offset[t+1]) of any of the four kinds
+ * (subterm.hpp:21-36). term_offset holds ABSOLUTE indices into the subterm
+ * arrays, so a contiguous term range of a bigger list is a valid view (used
+ * for the multi-GPU term split). */
+typedef struct {
+    uint32_t n_params;            /* <= 64 */
+    uint64_t n_terms;
+    const uint64_t* term_offset;  /* [n_terms + 1] */
+    const int64_t* term_scalar;   /* [n_terms * 5]: a, b, c, d, exp */
+    const uint8_t* kind;          /* PZX_NODE .. PZX_PI_PAIR */
+    const uint8_t* psi_k;         /* [0,7] */
+    const uint64_t* psi_mask;
+    const uint8_t* phi_k;         /* [0,7]; ignored for Node / HalfPi */
+    const uint64_t* phi_mask;
+} pzx_expr_view;
+
+/* Already-normalised phase-pair rows (SPEC ScalarExpression after Eq. 4,
+ * S:332-335): row r contributes 1 + w^x + w^y - w^(x+y) with
+ * x = k_alpha[r] + 4*parity(psi_mask[r] & a), y = k_beta[r] + 4*parity(phi_mask[r] & a).
+ * No dummy padding is needed (CSR offsets), unlike the paper's padded
+ * m x n_max matrix. */
+typedef struct {
+    uint32_t n_params;
+    uint64_t n_terms;
+    const uint64_t* term_row_offset;  /* [n_terms + 1], absolute */
+    const int64_t* term_coef;         /* [n_terms * 5] exact C_t */
+    const uint64_t* psi_mask;
+    const uint64_t* phi_mask;
+    const uint8_t* k_alpha;
+    const uint8_t* k_beta;
+} pzx_table_view;
+
+/* Per-term debug record of pzx_debug_term_codes: the exact product of the
+ * term's row values at one assignment is
+ *   C'_t * sqrt2^E_t * mu^nLM_t * w^j * (lambda/mu)^s1 * pi^a * pi'^b   (z == 0)
+ * and 0 when z > 0, with w = e^{i pi/4}, lambda = 1 - w, mu = 1 + w,
+ * pi = 1 + w + w^3, pi' = 1 - w - w^3 (E_t, nLM_t, C'_t from
+ * pzx_table_term_info). DESIGN.md §2 derives this factorisation. */
+typedef struct { uint32_t j, z, s1, a, b; } pzx_term_code;
+
+const char* pzx_status_string(pzx_status s);
+const char* pzx_version(void);
+
+pzx_status pzx_create(int device, pzx_ctx** out);
+void pzx_destroy(pzx_ctx* ctx);
+const char* pzx_last_error(const pzx_ctx* ctx);
+/* Number of kernel launches issued by this context since creation. */
+uint64_t pzx_launch_count(const pzx_ctx* ctx);
+
+pzx_status pzx_table_upload_expr(pzx_ctx* ctx, const pzx_expr_view* expr, pzx_table** out);
+pzx_status pzx_table_upload(pzx_ctx* ctx, const pzx_table_view* view, pzx_table** out);
+void pzx_table_free(pzx_table* t);
+/* Host-only compile (no device, no context): normalisation + classification
+ * exactly as pzx_table_upload_expr, for inspection (shape / term_info) and
+ * CPU tests. Evaluating such a table returns PZX_E_INVALID. */
+pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out);
+/* Host-only: the per-class variant codes [64 classes][4 variants], sqrt2
+ * exponent e[64] and lambda/mu flag lm[64] the kernels use. */
+pzx_status pzx_class_table(uint32_t codes[256], int32_t e[64], int32_t lm[64]);
+/* shape: n_params, n_terms, n_rows (genuine rows), max rows in one term */
+pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_terms,
+                           uint64_t* n_rows, uint32_t* max_term_rows);
+/* Folded exact constant C'_t (a,b,c,d,exp), sqrt2 exponent E_t and the count
+ * nLM_t of lambda/mu rows of term t (see pzx_term_code). */
+pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],
+                               int32_t* e_sqrt2, int32_t* n_lm);
+
+/* Synchronous evaluation from HOST buffers: assignments[n] -> amp[2n]
+ * (re,im interleaved; may be NULL) and prob[n] (may be NULL). */
+pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
+                        uint64_t n, double* amp, double* prob, uint32_t flags);
+/* Enumerated batch first, first+1, ..., first+n-1 (generated on device). */
+pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n,
+                              double* amp, double* prob, uint32_t flags);
+
+/* Asynchronous DEVICE-pointer variants on `stream` (0 = context stream):
+ * d_assignments may be NULL for the enumerated batch starting at `first`.
+ * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)
+ * gives partial amplitudes for the term split; d_amp receives 2n doubles,
+ * d_prob n doubles (either may be NULL). accumulate != 0 adds into d_amp. */
+pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
+                               uint64_t first, uint64_t n, uint64_t term_begin,
+                               uint64_t term_end, double* d_amp, double* d_prob,
+                               uint32_t flags, void* stream);
+/* prob from amplitudes on device (after a cross-GPU sum of partials). */
+pzx_status pzx_amp_to_prob_device(pzx_ctx* ctx, const double* d_amp, uint64_t n,
+                                  double* d_prob, uint32_t flags, void* stream);
+pzx_status pzx_synchronize(pzx_ctx* ctx);
+
+/* E3 debug: phase indices idx_psi*8 + idx_phi per (row, assignment), rows in
+ * the canonical normalised order (term-major, subterm order), row-major
+ * [n_rows][n]. */
+pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t,
+                                   const uint64_t* assignments, uint64_t n, uint8_t* idx_out);
+/* Per (term, assignment) exact product codes, [n_terms][n]. */
+pzx_status pzx_debug_term_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
+                                uint64_t n, pzx_term_code* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PZX_GPU_H */

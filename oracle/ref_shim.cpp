@@ -1,0 +1,210 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE: a C-ABI shim over the UNMODIFIED
+// reference core (/root/reference/proj/core/src/{ring,subterm,diagram}.cpp),
+// compiled from the reference's own source files by oracle/Makefile into
+// oracle/_ref/libpzx_ref.so. Nothing here re-implements reference arithmetic:
+// every value is produced by the reference's functions. It exists so that
+//   (1) the plain-C restatement (pzx_oracle.c) can be pinned against the
+//       reference itself, and golden fixtures generated from it, and
+//   (2) bench.py --impl reference can time the reference's own CPU
+//       evaluation path on the GPU box's host cores.
+//
+// Two evaluation modes, both the reference's own code path:
+//   mode 0 (primitives): SPEC eval_expression_reference composed
+//          from subterm_value (subterm.cpp:29-49), ring_mul (ring.cpp:76-86)
+//          and ring_add (ring.cpp:57-70), constant first as in
+//          instantiate_diagram (diagram.cpp:158-161).  == SURVEY CPU baseline A.
+//   mode 1 (literal API): one leaf ZXDiagram per term (set_scalar +
+//          push_subterm, diagram.cpp:114-120), evaluated per assignment with
+//          instantiate_diagram (diagram.cpp:149-165) and summed with ring_add.
+#include <pzx/diagram.hpp>
+#include <pzx/phase.hpp>
+#include <pzx/ring.hpp>
+#include <pzx/subterm.hpp>
+
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#include "pzx_oracle.h"
+
+namespace {
+
+int status_of(const std::exception& ex) {
+    if (dynamic_cast<const pzx::OverflowError*>(&ex)) return OQ_E_OVERFLOW;
+    if (dynamic_cast<const pzx::MissingParameter*>(&ex)) return OQ_E_MISSING;
+    if (dynamic_cast<const pzx::ParseError*>(&ex)) return OQ_E_PARSE;
+    if (dynamic_cast<const pzx::DomainError*>(&ex)) return OQ_E_DOMAIN;
+    return OQ_E_DOMAIN;
+}
+
+pzx::RingQuad to_ref(const oq_quad& q) {
+    pzx::RingQuad r;
+    r.a = q.a; r.b = q.b; r.c = q.c; r.d = q.d; r.exp = q.exp;
+    return r;
+}
+
+oq_quad from_ref(const pzx::RingQuad& r) {
+    oq_quad q{};
+    q.a = r.a; q.b = r.b; q.c = r.c; q.d = r.d; q.exp = r.exp;
+    return q;
+}
+
+pzx::Subterm to_ref(const oq_subterm& s) {
+    pzx::Subterm t;
+    t.kind = static_cast<pzx::SubtermKind>(s.kind);
+    t.psi = pzx::ParamPhase(s.psi_k, s.psi_mask);
+    t.phi = pzx::ParamPhase(s.phi_k, s.phi_mask);
+    return t;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return OQ_OK;
+    } catch (const std::exception& ex) {
+        return status_of(ex);
+    }
+}
+
+struct Prepared {
+    std::vector<pzx::RingQuad> scalars;
+    std::vector<std::vector<pzx::Subterm>> terms;
+    std::vector<pzx::ZXDiagram> leaves;
+};
+
+Prepared prepare(const oq_expr* e, bool diagrams) {
+    Prepared p;
+    p.scalars.reserve(e->n_terms);
+    p.terms.resize(e->n_terms);
+    for (uint64_t t = 0; t < e->n_terms; ++t) {
+        p.scalars.push_back(to_ref(e->scalars[t]));
+        for (uint64_t j = e->term_offset[t]; j < e->term_offset[t + 1]; ++j)
+            p.terms[t].push_back(to_ref(e->subterms[j]));
+    }
+    if (diagrams) {
+        p.leaves.resize(e->n_terms);
+        for (uint64_t t = 0; t < e->n_terms; ++t) {
+            p.leaves[t].set_scalar(p.scalars[t]);
+            for (const auto& s : p.terms[t]) p.leaves[t].push_subterm(s);
+        }
+    }
+    return p;
+}
+
+pzx::RingQuad eval_primitives(const Prepared& p, const pzx::ParamAssignment& a) {
+    pzx::RingQuad total = pzx::RingQuad::zero();
+    for (size_t t = 0; t < p.terms.size(); ++t) {
+        pzx::RingQuad s = p.scalars[t];
+        for (const auto& sub : p.terms[t]) s = pzx::ring_mul(s, pzx::subterm_value(sub, a));
+        total = pzx::ring_add(total, s);
+    }
+    return total;
+}
+
+pzx::RingQuad eval_literal(const Prepared& p, const pzx::ParamAssignment& a) {
+    pzx::RingQuad total = pzx::RingQuad::zero();
+    for (const auto& leaf : p.leaves)
+        total = pzx::ring_add(total, pzx::instantiate_diagram(leaf, a).scalar());
+    return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_eval_batch(const oq_expr* e, const uint64_t* words, uint64_t n, int n_threads,
+                   int mode, oq_quad* exact, double* amp) {
+    Prepared p;
+    int st = guarded([&] { p = prepare(e, mode == 1); });
+    if (st) return st;
+    if (n_threads < 1) n_threads = 1;
+    if (static_cast<uint64_t>(n_threads) > n) n_threads = n ? static_cast<int>(n) : 1;
+    std::vector<int> status(n_threads, OQ_OK);
+    auto work = [&](int tid) {
+        const uint64_t b = n * tid / n_threads, en = n * (tid + 1) / n_threads;
+        status[tid] = guarded([&] {
+            for (uint64_t i = b; i < en; ++i) {
+                const auto a = pzx::ParamAssignment::total(words[i], e->n_params);
+                const pzx::RingQuad v = mode == 1 ? eval_literal(p, a) : eval_primitives(p, a);
+                if (exact) exact[i] = from_ref(v);
+                if (amp) {
+                    const auto c = pzx::to_complex(v);
+                    amp[2 * i] = c.real();
+                    amp[2 * i + 1] = c.imag();
+                }
+            }
+        });
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < n_threads; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& t : th) t.join();
+    for (int s : status)
+        if (s) return s;
+    return OQ_OK;
+}
+
+int ref_term_value(const oq_expr* e, uint64_t t, uint64_t word, oq_quad* out) {
+    return guarded([&] {
+        pzx::ZXDiagram leaf;
+        leaf.set_scalar(to_ref(e->scalars[t]));
+        for (uint64_t j = e->term_offset[t]; j < e->term_offset[t + 1]; ++j)
+            leaf.push_subterm(to_ref(e->subterms[j]));
+        const auto a = pzx::ParamAssignment::total(word, e->n_params);
+        *out = from_ref(pzx::instantiate_diagram(leaf, a).scalar());
+    });
+}
+
+int ref_normalize(const oq_subterm* s, oq_quad* constant, int* has_pair, oq_subterm* pair) {
+    return guarded([&] {
+        const pzx::NormalizedSubterm ns = pzx::normalize_subterm(to_ref(*s));
+        *constant = from_ref(ns.constant);
+        *has_pair = ns.pair.has_value() ? 1 : 0;
+        *pair = oq_subterm{};
+        if (ns.pair) {
+            pair->kind = static_cast<uint8_t>(ns.pair->kind);
+            pair->psi_k = ns.pair->psi.k;
+            pair->psi_mask = ns.pair->psi.mask;
+            pair->phi_k = ns.pair->phi.k;
+            pair->phi_mask = ns.pair->phi.mask;
+        }
+    });
+}
+
+int ref_subterm_value(const oq_subterm* s, uint64_t word, uint32_t n_params, oq_quad* out) {
+    return guarded([&] {
+        *out = from_ref(pzx::subterm_value(to_ref(*s), pzx::ParamAssignment::total(word, n_params)));
+    });
+}
+
+int ref_pair_value(int ka, int kb, oq_quad* out) {
+    return guarded([&] { *out = from_ref(pzx::phase_pair_value(ka, kb)); });
+}
+
+int ref_instantiate_phase(int k, uint64_t mask, uint64_t word, uint32_t n_params, int* out) {
+    return guarded([&] {
+        *out = pzx::instantiate_phase(pzx::ParamPhase(k, mask),
+                                      pzx::ParamAssignment::total(word, n_params));
+    });
+}
+
+int ref_ring_add(const oq_quad* x, const oq_quad* y, oq_quad* out) {
+    return guarded([&] { *out = from_ref(pzx::ring_add(to_ref(*x), to_ref(*y))); });
+}
+
+int ref_ring_mul(const oq_quad* x, const oq_quad* y, oq_quad* out) {
+    return guarded([&] { *out = from_ref(pzx::ring_mul(to_ref(*x), to_ref(*y))); });
+}
+
+int ref_make(int64_t a, int64_t b, int64_t c, int64_t d, int32_t e, oq_quad* out) {
+    return guarded([&] { *out = from_ref(pzx::RingQuad::make(a, b, c, d, e)); });
+}
+
+void ref_to_complex(const oq_quad* x, double* re, double* im) {
+    const auto c = pzx::to_complex(to_ref(*x));
+    *re = c.real();
+    *im = c.imag();
+}
+
+}  // extern "C"

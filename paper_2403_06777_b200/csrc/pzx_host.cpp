@@ -1,0 +1,696 @@
+// pzx_host.cpp -- host side of the C ABI (include/pzx_gpu.h): table compiler
+// (normalisation, classification, SoA/AoS device layout, LUT construction),
+// device memory, launch policy and the synchronous / asynchronous entry points.
+//
+// The table compiler is the SPEC's compile_bit_table re-designed
+// for a thread-per-assignment kernel: rows are stored per term in CSR order
+// (no dummy padding, P:200-223 is not needed when all lanes walk the same
+// term), every row is reduced to a class byte offset + masks + a 4-parameter
+// Walsh pattern, and each term carries one fp64 constant that already contains
+// every assignment-independent factor.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "pzx_gpu.h"
+#include "pzx_internal.h"
+#include "pzx_math.hpp"
+
+using namespace pzxb;
+
+// ------------------------------------------------------------ class table ----
+namespace {
+
+struct ClassInfo {
+    uint32_t code[4];  // variant (p | q << 1)
+    int e;             // sqrt2 exponent, constant over the class's variants
+    int lm;            // 1 if every nonzero variant carries lambda or mu
+    bool ok;
+};
+
+struct Classes {
+    ClassInfo c[64];
+    bool ok = true;
+    Classes() {
+        for (int ka = 0; ka < 8; ++ka)
+            for (int kb = 0; kb < 8; ++kb) {
+                ClassInfo& ci = c[ka * 8 + kb];
+                ci.e = -1; ci.lm = -1; ci.ok = true;
+                for (int v = 0; v < 4; ++v) {
+                    const int p = v & 1, q = v >> 1;
+                    Factor f;
+                    if (!zw_factor(zw_pair_value(ka + 4 * p, kb + 4 * q), f)) { ci.ok = ok = false; continue; }
+                    uint32_t code = 0;
+                    if (f.kind == K_ZERO) {
+                        code = 1u << kZShift;
+                    } else {
+                        code = uint32_t(f.j) << kJShift;
+                        if (f.kind == K_LAMBDA) code |= 1u << kS1Shift;
+                        if (f.kind == K_PI) code |= 1u << kAShift;
+                        if (f.kind == K_PIP) code |= 1u << kBShift;
+                        const int lm = (f.kind == K_LAMBDA || f.kind == K_MU) ? 1 : 0;
+                        // e and lambda/mu membership are class constants
+                        if (ci.e < 0) ci.e = f.e; else if (ci.e != f.e) ci.ok = ok = false;
+                        if (ci.lm < 0) ci.lm = lm; else if (ci.lm != lm) ci.ok = ok = false;
+                    }
+                    ci.code[v] = code;
+                }
+                if (ci.e < 0) { ci.e = 0; ci.lm = 0; }
+            }
+    }
+};
+
+const Classes& classes() {
+    static const Classes k;
+    return k;
+}
+
+// ---------------------------------------------------------- normalisation ----
+struct PairRow { uint8_t ka, kb; uint64_t psi, phi; };
+
+Quad quad_omega(int k) {
+    Quad q;
+    zw_to_quad(zw_pow_w(k), q);
+    return q;
+}
+
+// normalize_subterm, subterm.cpp:51-96 (Lemmas 3-5); returns a pzx_status.
+int normalize(uint8_t kind, int psik, uint64_t psim, int phik, uint64_t phim, Quad& constant,
+              bool& has_pair, PairRow& row) {
+    has_pair = false;
+    switch (kind) {
+    case PZX_PHASE_PAIR:
+        if (!psim && !phim) {
+            return zw_to_quad(zw_pair_value(psik, phik), constant) ? PZX_OK : PZX_E_OVERFLOW;
+        }
+        constant = Quad{1, 0, 0, 0, 0};
+        row = {uint8_t(psik), uint8_t(phik), psim, phim};
+        has_pair = true;
+        return PZX_OK;
+    case PZX_NODE:
+        if (!psim) return zw_to_quad(zw_add(zw(1, 0, 0, 0), zw_pow_w(psik)), constant) ? PZX_OK : PZX_E_OVERFLOW;
+        constant = Quad{1, 0, -1, 0, 1};                     // (1 - i)/2
+        row = {uint8_t((psik + 2) & 7), 2, psim, 0};         // pair(psi + pi/2, pi/2)
+        has_pair = true;
+        return PZX_OK;
+    case PZX_PI_PAIR:
+        if (phik != 0 && phik != 4) return PZX_E_DOMAIN;     // pauli_image(phi)
+        if (!phim && !psim) {
+            constant = phik == 4 ? quad_omega(psik) : Quad{1, 0, 0, 0, 0};
+            return PZX_OK;
+        }
+        constant = Quad{1, 0, 0, 0, 1};                      // 1/2
+        row = {uint8_t(psik), uint8_t(phik), psim, phim};
+        has_pair = true;
+        return PZX_OK;
+    case PZX_HALF_PI: {
+        if (psik != 2 && psik != 6) return PZX_E_DOMAIN;     // proper_clifford_image
+        const Quad c = quad_omega(psik == 2 ? 1 : 7);
+        if (!psim) { constant = c; return PZX_OK; }
+        // pi_pair(base = (8-k, {}), selector = (0, mask)) -> 1/2 pair(base, selector)
+        if (!quad_mul(c, Quad{1, 0, 0, 0, 1}, constant)) return PZX_E_OVERFLOW;
+        row = {uint8_t((8 - psik) & 7), 0, 0, psim};
+        has_pair = true;
+        return PZX_OK;
+    }
+    }
+    return PZX_E_DOMAIN;
+}
+
+// ---------------------------------------------------------- host table ----
+struct HostTable {
+    uint32_t n_params = 0;
+    std::vector<uint64_t> term_row{0};
+    std::vector<Quad> coef;                 // C'_t (exact, normalisation folded)
+    std::vector<int32_t> e_t, nlm_t;
+    std::vector<double> term_c;             // 2 per term
+    std::vector<uint4> rows;                // P <= 32: {psi, phi, code, pat}; P > 32: masks
+    std::vector<uint2> aux;                 // P > 32: {code, pat}
+    std::vector<uint8_t> swapped;           // row stored with psi/phi exchanged
+    uint32_t max_rows = 0;
+};
+
+uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
+    uint32_t pat = 0;
+    for (int g = 0; g < kGray; ++g) {
+        pat |= uint32_t(__builtin_parityll(psi & uint64_t(g))) << (2 * g);
+        pat |= uint32_t(__builtin_parityll(phi & uint64_t(g))) << (2 * g + 1);
+    }
+    return pat;
+}
+
+void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
+    uint8_t sw = 0;
+    if (pr.psi == 0 && pr.phi != 0) {  // V(x,y) = V(y,x): keep a lone parity in psi
+        std::swap(pr.ka, pr.kb);
+        std::swap(pr.psi, pr.phi);
+        sw = 1;
+    }
+    const int cls = pr.ka * 8 + pr.kb;
+    const ClassInfo& ci = classes().c[cls];
+    e += ci.e;
+    lm += ci.lm;
+    const uint32_t code = uint32_t(cls) * 16u;
+    const uint32_t pat = walsh_pattern(pr.psi, pr.phi);
+    if (h.n_params <= 32) {
+        h.rows.push_back(make_uint4(uint32_t(pr.psi), uint32_t(pr.phi), code, pat));
+    } else {
+        h.rows.push_back(make_uint4(uint32_t(pr.psi), uint32_t(pr.psi >> 32), uint32_t(pr.phi),
+                                    uint32_t(pr.phi >> 32)));
+        h.aux.push_back(make_uint2(code, pat));
+    }
+    h.swapped.push_back(sw);
+}
+
+int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t n_rows_term) {
+    if (n_rows_term > uint64_t(kMaxTermRows)) return PZX_E_CAPACITY;
+    h.max_rows = std::max<uint32_t>(h.max_rows, uint32_t(n_rows_term));
+    h.coef.push_back(c);
+    h.e_t.push_back(e);
+    h.nlm_t.push_back(lm);
+    // C'' = C' * sqrt2^E * mu^nLM, rounded once to double
+    f128 re, im;
+    quad_to_f128(c, re, im);
+    C128 v{re, im};
+    for (int i = 0; i < e; ++i) { v.re *= f128_sqrt2(); v.im *= f128_sqrt2(); }
+    const C128 mu = zw_to_c128(zw(1, 1, 0, 0));
+    for (int i = 0; i < lm; ++i) v = cmul(v, mu);
+    h.term_c.push_back(double(v.re));
+    h.term_c.push_back(double(v.im));
+    h.term_row.push_back(h.rows.size());
+    return PZX_OK;
+}
+
+uint64_t param_mask(uint32_t n) { return n >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n) - 1); }
+
+bool canon_input(const int64_t* q, Quad& out) {
+    if (q[4] < INT32_MIN || q[4] > INT32_MAX) return false;
+    return quad_canon(q[0], q[1], q[2], q[3], q[4], out);
+}
+
+int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
+    if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
+    h.n_params = v->n_params;
+    const uint64_t allowed = param_mask(v->n_params);
+    for (uint64_t t = 0; t < v->n_terms; ++t) {
+        Quad c;
+        if (!canon_input(v->term_scalar + 5 * t, c)) { err = "term scalar out of range"; return PZX_E_OVERFLOW; }
+        int e = 0, lm = 0;
+        const uint64_t row0 = h.rows.size();
+        for (uint64_t j = v->term_offset[t]; j < v->term_offset[t + 1]; ++j) {
+            const uint8_t kind = v->kind[j];
+            const int psik = v->psi_k[j], phik = v->phi_k ? v->phi_k[j] : 0;
+            const uint64_t psim = v->psi_mask[j];
+            uint64_t phim = v->phi_mask ? v->phi_mask[j] : 0;
+            if (kind > PZX_PI_PAIR || psik > 7 || phik > 7) { err = "subterm kind or phase out of range"; return PZX_E_DOMAIN; }
+            if (kind == PZX_NODE || kind == PZX_HALF_PI) phim = 0;  // phi unused (subterm.hpp:25)
+            if ((psim | phim) & ~allowed) { err = "subterm mask uses a parameter >= n_params"; return PZX_E_MISSING_PARAM; }
+            Quad k;
+            bool has = false;
+            PairRow pr{};
+            int st = normalize(kind, psik, psim, phik, phim, k, has, pr);
+            if (st) { err = "normalize_subterm: kind invariant violated"; return st; }
+            Quad nc;
+            if (!quad_mul(c, k, nc)) { err = "term constant overflow"; return PZX_E_OVERFLOW; }
+            c = nc;
+            if (has) push_row(h, pr, e, lm);
+        }
+        int st = finish_term(h, c, e, lm, h.rows.size() - row0);
+        if (st) { err = "term has more rows than supported"; return st; }
+    }
+    return PZX_OK;
+}
+
+int compile_rows(const pzx_table_view* v, HostTable& h, std::string& err) {
+    if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
+    h.n_params = v->n_params;
+    const uint64_t allowed = param_mask(v->n_params);
+    for (uint64_t t = 0; t < v->n_terms; ++t) {
+        Quad c;
+        if (!canon_input(v->term_coef + 5 * t, c)) { err = "term coefficient out of range"; return PZX_E_OVERFLOW; }
+        int e = 0, lm = 0;
+        const uint64_t row0 = h.rows.size();
+        for (uint64_t r = v->term_row_offset[t]; r < v->term_row_offset[t + 1]; ++r) {
+            if (v->k_alpha[r] > 7 || v->k_beta[r] > 7) { err = "phase index out of [0,7]"; return PZX_E_DOMAIN; }
+            if ((v->psi_mask[r] | v->phi_mask[r]) & ~allowed) { err = "row mask uses a parameter >= n_params"; return PZX_E_MISSING_PARAM; }
+            PairRow pr{v->k_alpha[r], v->k_beta[r], v->psi_mask[r], v->phi_mask[r]};
+            if (!pr.psi && !pr.phi) {  // assignment independent: fold (push_subterm, diagram.cpp:114-120)
+                Quad k, nc;
+                if (!zw_to_quad(zw_pair_value(pr.ka, pr.kb), k) || !quad_mul(c, k, nc)) { err = "term constant overflow"; return PZX_E_OVERFLOW; }
+                c = nc;
+                continue;
+            }
+            push_row(h, pr, e, lm);
+        }
+        int st = finish_term(h, c, e, lm, h.rows.size() - row0);
+        if (st) { err = "term has more rows than supported"; return st; }
+    }
+    return PZX_OK;
+}
+
+std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
+    const int M = int(std::max<uint32_t>(max_rows, 1));
+    auto align16 = [](uint32_t x) { return (x + 15u) & ~15u; };
+    L.max_rows = M;
+    L.codes_off = 0;
+    L.om_off = align16(L.codes_off + 64 * 4 * 4);
+    L.u_off = align16(L.om_off + 8 * 16);
+    L.p3_off = align16(L.u_off + 8 * (M + 1));
+    L.pd_off = align16(L.p3_off + 8 * (M / 2 + 1));
+    L.bytes = align16(L.pd_off + 16 * (2 * M + 1));
+    std::vector<unsigned char> blob(L.bytes, 0);
+    uint32_t* codes = reinterpret_cast<uint32_t*>(blob.data() + L.codes_off);
+    for (int c = 0; c < 64; ++c)
+        for (int v = 0; v < 4; ++v) codes[c * 4 + v] = classes().c[c].code[v];
+    double* om = reinterpret_cast<double*>(blob.data() + L.om_off);
+    for (int j = 0; j < 8; ++j) {
+        const C128 w = zw_to_c128(zw_pow_w(j));
+        om[2 * j] = double(w.re);
+        om[2 * j + 1] = double(w.im);
+    }
+    double* u = reinterpret_cast<double*>(blob.data() + L.u_off);
+    f128 x = 1;
+    for (int s = 0; s <= M; ++s) { u[s] = double(x); x *= (f128_sqrt2() - 1); }
+    double* p3 = reinterpret_cast<double*>(blob.data() + L.p3_off);
+    x = 1;
+    for (int m = 0; m <= M / 2; ++m) { p3[m] = double(x); x *= 3; }
+    double* pd = reinterpret_cast<double*>(blob.data() + L.pd_off);
+    const C128 pi = zw_to_c128(zw_generator(K_PI)), pip = zw_to_c128(zw_generator(K_PIP));
+    C128 a{1, 0}, b{1, 0};
+    for (int d = 0; d <= M; ++d) {
+        pd[2 * (M + d)] = double(a.re); pd[2 * (M + d) + 1] = double(a.im);
+        pd[2 * (M - d)] = double(b.re); pd[2 * (M - d) + 1] = double(b.im);
+        a = cmul(a, pi);
+        b = cmul(b, pip);
+    }
+    return blob;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- handles ----
+struct pzx_ctx {
+    int device = 0;
+    int n_sm = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    // scratch (grown on demand, freed with the context)
+    void* d_asg = nullptr; size_t asg_cap = 0;
+    void* d_amp = nullptr; size_t amp_cap = 0;
+    void* d_prob = nullptr; size_t prob_cap = 0;
+    void* d_partial = nullptr; size_t partial_cap = 0;
+    void* d_chunks = nullptr; size_t chunks_cap = 0;
+    void* d_dbg = nullptr; size_t dbg_cap = 0;
+};
+
+struct pzx_table {
+    pzx_ctx* ctx = nullptr;
+    int device = 0;
+    DevTable dev;
+    HostTable host;
+    void* d_rows = nullptr;
+    void* d_aux = nullptr;
+    void* d_term_row = nullptr;
+    void* d_term_c = nullptr;
+    void* d_lut = nullptr;
+};
+
+namespace {
+
+pzx_status set_err(pzx_ctx* ctx, int st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return pzx_status(st);
+}
+
+pzx_status cuda_err(pzx_ctx* ctx, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return PZX_OK;
+    return set_err(ctx, e == cudaErrorMemoryAllocation ? PZX_E_OOM : PZX_E_CUDA,
+                   std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaError_t grow(void** p, size_t* cap, size_t need) {
+    if (need <= *cap) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e == cudaSuccess) *cap = need;
+    return e;
+}
+
+template <class T>
+cudaError_t upload_vec(void** dst, const std::vector<T>& v) {
+    const size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table** out) {
+    HostTable& h = t->host;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    if ((st = cuda_err(ctx, upload_vec(&t->d_rows, h.rows), "upload rows"))) return st;
+    if (h.n_params > 32 && (st = cuda_err(ctx, upload_vec(&t->d_aux, h.aux), "upload aux"))) return st;
+    if ((st = cuda_err(ctx, upload_vec(&t->d_term_row, h.term_row), "upload term offsets"))) return st;
+    if ((st = cuda_err(ctx, upload_vec(&t->d_term_c, h.term_c), "upload term constants"))) return st;
+    LutLayout L;
+    std::vector<unsigned char> blob = build_lut(h.max_rows, L);
+    if ((st = cuda_err(ctx, upload_vec(&t->d_lut, blob), "upload lut"))) return st;
+    DevTable& d = t->dev;
+    d.rows = static_cast<const uint4*>(t->d_rows);
+    d.aux = static_cast<const uint2*>(t->d_aux);
+    d.term_row = static_cast<const uint64_t*>(t->d_term_row);
+    d.term_c = static_cast<const double2*>(t->d_term_c);
+    d.lut = static_cast<const unsigned char*>(t->d_lut);
+    d.lut_layout = L;
+    d.n_terms = h.coef.size();
+    d.n_rows = h.rows.size();
+    d.n_params = h.n_params;
+    d.max_rows = h.max_rows;
+    d.p64 = h.n_params > 32;
+    t->ctx = ctx;
+    t->device = ctx->device;
+    *out = t.release();
+    return PZX_OK;
+}
+
+// term-split chunk boundaries balanced by row count
+void chunk_bounds(const HostTable& h, uint64_t tb, uint64_t te, int chunks, std::vector<uint64_t>& b) {
+    b.assign(size_t(chunks) + 1, te);
+    b[0] = tb;
+    const uint64_t r0 = h.term_row[tb], r1 = h.term_row[te];
+    for (int c = 1; c < chunks; ++c) {
+        const uint64_t target = r0 + (r1 - r0) * uint64_t(c) / uint64_t(chunks);
+        auto it = std::lower_bound(h.term_row.begin() + tb, h.term_row.begin() + te, target);
+        uint64_t k = uint64_t(it - h.term_row.begin());
+        b[c] = std::max(b[c - 1], std::min(k, te));
+    }
+}
+
+pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t flags) {
+    if (!ctx || !t) return PZX_E_INVALID;
+    if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table (pzx_table_compile_host)");
+    if (t->device != ctx->device) return set_err(ctx, PZX_E_INVALID, "table belongs to another device");
+    if (r.term_end > t->dev.n_terms) r.term_end = t->dev.n_terms;
+    if (r.term_begin > r.term_end) return set_err(ctx, PZX_E_INVALID, "bad term range");
+    r.kernel = (flags & PZX_KERNEL_GENERAL) ? KC_GENERAL : (flags & PZX_KERNEL_GRAY) ? KC_GRAY : KC_AUTO;
+    if (r.kernel == KC_GRAY && ((r.d_asg && !r.words_contiguous) || r.first % kGray))
+        return set_err(ctx, PZX_E_INVALID, "enumerated kernel needs a device-generated batch starting at a multiple of 16");
+    const KernelChoice kc = choose_kernel(t->dev, r);
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    // grid policy: enough CTAs for >= ~4 per SM; otherwise split the terms
+    const int ablocks = grid_assign_blocks(t->dev, r, kc);
+    const uint64_t nterms = r.term_end - r.term_begin;
+    int chunks = 1;
+    const int target = 4 * ctx->n_sm;
+    if (ablocks < target && nterms > 1) {
+        chunks = int(std::min<uint64_t>((target + ablocks - 1) / ablocks, nterms));
+        chunks = std::min(chunks, 65535);
+    }
+    r.n_chunks = chunks;
+    if (chunks > 1) {
+        std::vector<uint64_t> b;
+        chunk_bounds(t->host, r.term_begin, r.term_end, chunks, b);
+        if ((st = cuda_err(ctx, grow(&ctx->d_chunks, &ctx->chunks_cap, b.size() * 8), "alloc chunks"))) return st;
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_chunks, b.data(), b.size() * 8, cudaMemcpyHostToDevice, r.stream), "copy chunks"))) return st;
+        if ((st = cuda_err(ctx, grow(&ctx->d_partial, &ctx->partial_cap, size_t(chunks) * r.n * 16), "alloc partials"))) return st;
+        r.d_chunk_terms = static_cast<const uint64_t*>(ctx->d_chunks);
+        r.d_partial = static_cast<double2*>(ctx->d_partial);
+    }
+    if (t->dev.lut_layout.bytes > 200 * 1024) return set_err(ctx, PZX_E_CAPACITY, "LUT exceeds 200 KiB");
+    if ((st = cuda_err(ctx, launch_evaluate(t->dev, r, kc, &ctx->launches), "evaluate kernel"))) return st;
+    return PZX_OK;
+}
+
+int prob_mode_of(uint32_t flags) {
+    return (flags & PZX_PROB_REAL) ? 2 : (flags & PZX_PROB_ABS2) ? 1 : 1;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI ----
+extern "C" {
+
+const char* pzx_status_string(pzx_status s) {
+    switch (s) {
+    case PZX_OK: return "ok";
+    case PZX_E_PARSE: return "parse error";
+    case PZX_E_DOMAIN: return "domain error";
+    case PZX_E_MISSING_PARAM: return "missing parameter";
+    case PZX_E_OVERFLOW: return "overflow";
+    case PZX_E_INVALID: return "invalid argument";
+    case PZX_E_CAPACITY: return "capacity exceeded";
+    case PZX_E_CUDA: return "cuda error";
+    case PZX_E_NCCL: return "nccl error";
+    case PZX_E_OOM: return "out of device memory";
+    }
+    return "unknown";
+}
+
+const char* pzx_version(void) { return "pzx-b200 0.1 (sm_100a)"; }
+
+pzx_status pzx_create(int device, pzx_ctx** out) {
+    if (!out) return PZX_E_INVALID;
+    *out = nullptr;
+    if (!classes().ok) return PZX_E_DOMAIN;
+    std::unique_ptr<pzx_ctx> c(new (std::nothrow) pzx_ctx);
+    if (!c) return PZX_E_OOM;
+    c->device = device;
+    pzx_status st;
+    if ((st = cuda_err(c.get(), cudaSetDevice(device), "cudaSetDevice"))) return st;
+    int nsm = 0;
+    if ((st = cuda_err(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device), "device query"))) return st;
+    c->n_sm = nsm > 0 ? nsm : 148;
+    if ((st = cuda_err(c.get(), cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream"))) return st;
+    *out = c.release();
+    return PZX_OK;
+}
+
+void pzx_destroy(pzx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg})
+        if (p) cudaFree(p);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* pzx_last_error(const pzx_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+uint64_t pzx_launch_count(const pzx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+pzx_status pzx_table_upload_expr(pzx_ctx* ctx, const pzx_expr_view* expr, pzx_table** out) {
+    if (!ctx || !expr || !out || (expr->n_terms && (!expr->term_offset || !expr->term_scalar)))
+        return PZX_E_INVALID;
+    std::unique_ptr<pzx_table> t(new (std::nothrow) pzx_table);
+    if (!t) return PZX_E_OOM;
+    std::string err;
+    int st = compile_expr(expr, t->host, err);
+    if (st) return set_err(ctx, st, err);
+    return finish_upload(ctx, t, out);
+}
+
+pzx_status pzx_table_upload(pzx_ctx* ctx, const pzx_table_view* view, pzx_table** out) {
+    if (!ctx || !view || !out || (view->n_terms && (!view->term_row_offset || !view->term_coef)))
+        return PZX_E_INVALID;
+    std::unique_ptr<pzx_table> t(new (std::nothrow) pzx_table);
+    if (!t) return PZX_E_OOM;
+    std::string err;
+    int st = compile_rows(view, t->host, err);
+    if (st) return set_err(ctx, st, err);
+    return finish_upload(ctx, t, out);
+}
+
+pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out) {
+    if (!expr || !out || (expr->n_terms && (!expr->term_offset || !expr->term_scalar)))
+        return PZX_E_INVALID;
+    std::unique_ptr<pzx_table> t(new (std::nothrow) pzx_table);
+    if (!t) return PZX_E_OOM;
+    std::string err;
+    int st = compile_expr(expr, t->host, err);
+    if (st) return pzx_status(st);
+    t->device = -1;
+    t->dev.n_terms = t->host.coef.size();
+    t->dev.n_rows = t->host.rows.size();
+    t->dev.n_params = t->host.n_params;
+    t->dev.max_rows = t->host.max_rows;
+    *out = t.release();
+    return PZX_OK;
+}
+
+pzx_status pzx_class_table(uint32_t codes[256], int32_t e[64], int32_t lm[64]) {
+    const Classes& k = classes();
+    if (!k.ok) return PZX_E_DOMAIN;
+    for (int c = 0; c < 64; ++c) {
+        for (int v = 0; v < 4; ++v)
+            if (codes) codes[c * 4 + v] = k.c[c].code[v];
+        if (e) e[c] = k.c[c].e;
+        if (lm) lm[c] = k.c[c].lm;
+    }
+    return PZX_OK;
+}
+
+void pzx_table_free(pzx_table* t) {
+    if (!t) return;
+    if (t->device < 0) { delete t; return; }
+    cudaSetDevice(t->device);
+    for (void* p : {t->d_rows, t->d_aux, t->d_term_row, t->d_term_c, t->d_lut})
+        if (p) cudaFree(p);
+    delete t;
+}
+
+pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_terms,
+                           uint64_t* n_rows, uint32_t* max_term_rows) {
+    if (!t) return PZX_E_INVALID;
+    if (n_params) *n_params = t->host.n_params;
+    if (n_terms) *n_terms = t->dev.n_terms;
+    if (n_rows) *n_rows = t->dev.n_rows;
+    if (max_term_rows) *max_term_rows = t->host.max_rows;
+    return PZX_OK;
+}
+
+pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],
+                               int32_t* e_sqrt2, int32_t* n_lm) {
+    if (!t || term >= t->dev.n_terms) return PZX_E_INVALID;
+    const Quad& q = t->host.coef[term];
+    if (coef) { coef[0] = q.a; coef[1] = q.b; coef[2] = q.c; coef[3] = q.d; coef[4] = q.e; }
+    if (e_sqrt2) *e_sqrt2 = t->host.e_t[term];
+    if (n_lm) *n_lm = t->host.nlm_t[term];
+    return PZX_OK;
+}
+
+static pzx_status eval_host(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
+                            uint64_t n, double* amp, double* prob, uint32_t flags) {
+    if (!ctx || !t) return PZX_E_INVALID;
+    if (n == 0) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    LaunchReq r;
+    r.stream = ctx->stream;
+    r.first = first;
+    r.n = n;
+    r.term_begin = 0;
+    r.term_end = t->dev.n_terms;
+    r.prob_mode = prob_mode_of(flags);
+    if (asg) {
+        if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc assignments"))) return st;
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_asg, asg, n * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D assignments"))) return st;
+        r.d_asg = static_cast<const uint64_t*>(ctx->d_asg);
+        // a contiguous, 16-aligned word list (a sweep over output bitstrings)
+        // can use the enumerated kernel; the kernel still reads its base words
+        bool contig = n >= uint64_t(kGray) && asg[0] % kGray == 0;
+        for (uint64_t i = 1; contig && i < n; ++i) contig = asg[i] == asg[0] + i;
+        if (contig) { r.words_contiguous = 1; r.first = asg[0]; }
+    }
+    if (amp) {
+        if ((st = cuda_err(ctx, grow(&ctx->d_amp, &ctx->amp_cap, n * 16), "alloc amplitudes"))) return st;
+        r.d_amp = static_cast<double2*>(ctx->d_amp);
+    }
+    if (prob) {
+        if ((st = cuda_err(ctx, grow(&ctx->d_prob, &ctx->prob_cap, n * 8), "alloc probabilities"))) return st;
+        r.d_prob = static_cast<double*>(ctx->d_prob);
+    }
+    if (!amp && !prob) return PZX_OK;
+    if ((st = run_eval(ctx, t, r, flags))) return st;
+    if (amp && (st = cuda_err(ctx, cudaMemcpyAsync(amp, ctx->d_amp, n * 16, cudaMemcpyDeviceToHost, ctx->stream), "D2H amplitudes"))) return st;
+    if (prob && (st = cuda_err(ctx, cudaMemcpyAsync(prob, ctx->d_prob, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H probabilities"))) return st;
+    return cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "evaluate");
+}
+
+pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
+                        uint64_t n, double* amp, double* prob, uint32_t flags) {
+    if (n && !assignments) return PZX_E_INVALID;
+    return eval_host(ctx, t, assignments, 0, n, amp, prob, flags);
+}
+
+pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n,
+                              double* amp, double* prob, uint32_t flags) {
+    return eval_host(ctx, t, nullptr, first, n, amp, prob, flags);
+}
+
+pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
+                               uint64_t first, uint64_t n, uint64_t term_begin,
+                               uint64_t term_end, double* d_amp, double* d_prob,
+                               uint32_t flags, void* stream) {
+    if (!ctx || !t) return PZX_E_INVALID;
+    if (n == 0) return PZX_OK;
+    LaunchReq r;
+    r.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    r.d_asg = d_assignments;
+    r.first = first;
+    r.n = n;
+    r.term_begin = term_begin;
+    r.term_end = term_end;
+    r.d_amp = reinterpret_cast<double2*>(d_amp);
+    r.d_prob = d_prob;
+    r.prob_mode = prob_mode_of(flags);
+    r.accumulate = 0;
+    if (!d_amp && !d_prob) return PZX_OK;
+    return run_eval(ctx, t, r, flags);
+}
+
+pzx_status pzx_amp_to_prob_device(pzx_ctx* ctx, const double* d_amp, uint64_t n, double* d_prob,
+                                  uint32_t flags, void* stream) {
+    if (!ctx || (n && (!d_amp || !d_prob))) return PZX_E_INVALID;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    return cuda_err(ctx, launch_amp_to_prob(reinterpret_cast<const double2*>(d_amp), n, d_prob,
+                                            prob_mode_of(flags), s, &ctx->launches), "amp_to_prob");
+}
+
+pzx_status pzx_synchronize(pzx_ctx* ctx) {
+    if (!ctx) return PZX_E_INVALID;
+    return cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "synchronize");
+}
+
+pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
+                                   uint64_t n, uint8_t* idx_out) {
+    if (!ctx || !t || (n && (!assignments || !idx_out))) return PZX_E_INVALID;
+    const uint64_t R = t->dev.n_rows;
+    if (!n || !R) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc"))) return st;
+    if ((st = cuda_err(ctx, grow(&ctx->d_dbg, &ctx->dbg_cap, R * n), "alloc"))) return st;
+    cudaMemcpyAsync(ctx->d_asg, assignments, n * 8, cudaMemcpyHostToDevice, ctx->stream);
+    if ((st = cuda_err(ctx, launch_debug_phase(t->dev, static_cast<const uint64_t*>(ctx->d_asg), n,
+                                               static_cast<uint8_t*>(ctx->d_dbg), ctx->stream, &ctx->launches), "debug phase"))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(idx_out, ctx->d_dbg, R * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "debug phase"))) return st;
+    // un-swap rows stored as (phi, psi): idx = psi*8 + phi in the caller's order
+    for (uint64_t r = 0; r < R; ++r) {
+        if (!t->host.swapped[r]) continue;
+        uint8_t* o = idx_out + r * n;
+        for (uint64_t i = 0; i < n; ++i) o[i] = uint8_t(((o[i] & 7) << 3) | (o[i] >> 3));
+    }
+    return PZX_OK;
+}
+
+pzx_status pzx_debug_term_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
+                                uint64_t n, pzx_term_code* out) {
+    if (!ctx || !t || (n && (!assignments || !out))) return PZX_E_INVALID;
+    const uint64_t M = t->dev.n_terms;
+    if (!n || !M) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc"))) return st;
+    if ((st = cuda_err(ctx, grow(&ctx->d_dbg, &ctx->dbg_cap, M * n * 20), "alloc"))) return st;
+    cudaMemcpyAsync(ctx->d_asg, assignments, n * 8, cudaMemcpyHostToDevice, ctx->stream);
+    if ((st = cuda_err(ctx, launch_debug_codes(t->dev, static_cast<const uint64_t*>(ctx->d_asg), n,
+                                               static_cast<uint32_t*>(ctx->d_dbg), ctx->stream, &ctx->launches), "debug codes"))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(out, ctx->d_dbg, M * n * 20, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
+    return cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "debug codes");
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// pzx_internal.h -- layout contract between the host table compiler
+// (pzx_host.cpp) and the sm_100a kernels (pzx_kernels.cu). DESIGN.md §3.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pzxb {
+
+// ---- per-variant code word (one 32-bit SWAR add per row-eval) ------------
+// A row of class (k_alpha, k_beta) evaluates, at parities (p, q), to
+//   V = w^j * sqrt2^e * g,   g in {1, lambda, mu, pi, pi'}   or 0.
+// e and "g in {lambda, mu}" depend on the class only (folded into the term
+// constant at compile time); what varies per assignment is packed here:
+constexpr uint32_t kZShift = 0;   // 7 bits: number of zero factors
+constexpr uint32_t kS1Shift = 7;  // 7 bits: number of lambda factors
+constexpr uint32_t kAShift = 14;  // 7 bits: number of pi factors
+constexpr uint32_t kBShift = 21;  // 7 bits: number of pi' factors
+constexpr uint32_t kJShift = 29;  // 3 bits: sum of j mod 8 (wraps off the top)
+constexpr uint32_t kField = 0x7F;
+constexpr int kSegRows = 127;     // rows one SWAR accumulator can absorb
+constexpr int kMaxTermRows = 4095;
+
+// Rows per thread-owned block of the enumerated (Walsh / "gray") kernel:
+// thread owns assignments base + g, g in [0, 2^kGrayBits).
+constexpr int kGrayBits = 4;
+constexpr int kGray = 1 << kGrayBits;
+
+// LUT blob (global memory, copied to shared memory by every CTA)
+struct LutLayout {
+    uint32_t codes_off;  // uint32 codes[64 classes][4 variants]
+    uint32_t om_off;     // double2 w^j, j = 0..7
+    uint32_t u_off;      // double (sqrt2 - 1)^s, s = 0..max_rows
+    uint32_t p3_off;     // double 3^m, m = 0..max_rows/2
+    uint32_t pd_off;     // double2 pi^d (d > 0) / pi'^-d (d < 0), d = -max_rows..max_rows
+    uint32_t bytes;
+    int32_t max_rows;
+};
+
+// Device table. Row record for n_params <= 32 (rows32):
+//   x = psi mask, y = phi mask, z = class byte offset into codes (cls * 16),
+//   w = Walsh pattern of the low kGrayBits parameters:
+//       bit 2g   = parity(psi & g), bit 2g+1 = parity(phi & g)
+// For n_params > 32 (rows64 + aux): rows64 = {psi_lo, psi_hi, phi_lo, phi_hi},
+// aux = {class offset, pattern}.
+struct DevTable {
+    const uint4* rows = nullptr;
+    const uint2* aux = nullptr;
+    const uint64_t* term_row = nullptr;  // [n_terms + 1], term_row[0] == 0
+    const double2* term_c = nullptr;     // C''_t = C'_t * sqrt2^E_t * mu^nLM_t
+    const unsigned char* lut = nullptr;
+    LutLayout lut_layout{};
+    uint64_t n_terms = 0, n_rows = 0;
+    uint32_t n_params = 0, max_rows = 0;
+    int p64 = 0;
+};
+
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2 };
+
+struct LaunchReq {
+    const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1
+    uint64_t first = 0, n = 0;
+    uint64_t term_begin = 0, term_end = 0;
+    double2* d_amp = nullptr;         // may be nullptr if only prob is wanted
+    double* d_prob = nullptr;
+    int prob_mode = 0;                // 0 none, 1 |amp|^2, 2 Re(amp)
+    int accumulate = 0;               // add into d_amp instead of overwriting
+    KernelChoice kernel = KC_AUTO;
+    int words_contiguous = 0;         // host verified d_asg[i] == first + i, first % kGray == 0
+    cudaStream_t stream = 0;
+    // scratch owned by the context
+    double2* d_partial = nullptr;     // [n_chunks][n] when n_chunks > 1
+    const uint64_t* d_chunk_terms = nullptr;  // [n_chunks + 1] term boundaries
+    int n_chunks = 1;
+};
+
+// Grid policy helpers (host)
+int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
+KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
+
+// Launchers; each returns the CUDA error of the launch and adds the number of
+// kernel launches to *launches.
+cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice kc,
+                            uint64_t* launches);
+cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int mode,
+                               cudaStream_t s, uint64_t* launches);
+cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_t n,
+                               uint8_t* d_out, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_t n,
+                               uint32_t* d_out5, cudaStream_t s, uint64_t* launches);
+
+constexpr int kThreads = 256;
+constexpr int kGeneralK = 4;  // assignments per thread, general kernel
+
+}  // namespace pzxb

@@ -1,0 +1,489 @@
+"""Host-side mirror of the reference's evaluate-on-assignments interface.
+
+Names, argument meanings and error classes follow the reference
+(/root/reference/proj/core/include/pzx/*.hpp and SPEC.md):
+
+=====================  =====================================================
+this module            reference
+=====================  =====================================================
+``Error`` ...          ``pzx::Error`` hierarchy, common.hpp:13-48
+``kMaxParams``         common.hpp:11
+``ParamAssignment``    phase.hpp:14-29 (``total``: bits >= n are dropped)
+``ParamPhase``         phase.hpp:34-52 (k mod 8 + XOR mask)
+``SubtermKind``        subterm.hpp:19
+``Subterm``            subterm.hpp:21-36 (``half_pi``/``pi_pair`` validate
+                       and orient exactly like subterm.cpp:5-21)
+``RingQuad``           ring.hpp:17-38 (exact; canonical form ring.cpp:20-48)
+``ScalarExpression``   SPEC ScalarExpression as a leaf-term list
+                       (scalar_ + pending_ of ZXDiagram, diagram.hpp:70-77)
+``compile_bit_table``  SPEC compile_bit_table + upload
+``Context.evaluate_batch``  SPEC evaluate_batch
+``Context.evaluate``   SPEC evaluate
+=====================  =====================================================
+
+Amplitudes come back as complex128 (the value the reference's ``to_complex``
+produces from its exact RingQuad, ring.cpp:131-136). All evaluation runs in
+the sm_100a kernels of ``libpzx_gpu.so``; nothing here computes amplitudes.
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+kMaxParams = 64
+
+
+# ---------------------------------------------------------------- errors ----
+class Error(RuntimeError):
+    """pzx::Error (common.hpp:14-17)."""
+
+
+class ParseError(Error):
+    """pzx::ParseError (common.hpp:20-23)."""
+
+
+class DomainError(Error):
+    """pzx::DomainError (common.hpp:26-29)."""
+
+
+class Lemma1Violation(DomainError):
+    """pzx::Lemma1Violation (common.hpp:33-36)."""
+
+
+class OverflowError(Error):  # noqa: A001 -- the reference's name (common.hpp:39-42)
+    """pzx::OverflowError: exact arithmetic left its range."""
+
+
+class MissingParameter(DomainError):
+    """pzx::MissingParameter (common.hpp:45-48)."""
+
+
+class CudaError(Error):
+    """Device-side failure (no reference analogue)."""
+
+
+_STATUS = {1: ParseError, 2: DomainError, 3: MissingParameter, 4: OverflowError,
+           5: Error, 6: DomainError, 10: CudaError, 11: CudaError, 12: CudaError}
+
+
+def _check(st: int, ctx=None) -> None:
+    if st == 0:
+        return
+    lib = N.lib()
+    msg = lib.pzx_status_string(st).decode()
+    if ctx is not None:
+        detail = lib.pzx_last_error(ctx).decode()
+        if detail:
+            msg = f"{msg}: {detail}"
+    raise _STATUS.get(st, Error)(msg)
+
+
+# ------------------------------------------------------- phases, subterms ----
+@dataclass(frozen=True)
+class ParamAssignment:
+    """Total assignment (phase.hpp:14-29)."""
+
+    bits: int = 0
+    defined: int = 0
+
+    @staticmethod
+    def total(bits: int, n_params: int) -> "ParamAssignment":
+        if n_params >= 64:
+            return ParamAssignment(bits & (2**64 - 1), 2**64 - 1)
+        m = (1 << n_params) - 1
+        return ParamAssignment(bits & m, m)
+
+    def covers(self, mask: int) -> bool:
+        return (mask & ~self.defined) == 0
+
+
+@dataclass(frozen=True)
+class ParamPhase:
+    """k*pi/4 + pi * XOR(params in mask) (phase.hpp:34-52)."""
+
+    k: int = 0
+    mask: int = 0
+
+    def __post_init__(self):
+        object.__setattr__(self, "k", self.k % 8)
+
+    def parametric(self) -> bool:
+        return self.mask != 0
+
+    def pauli_image(self) -> bool:
+        return self.k in (0, 4)
+
+    def proper_clifford_image(self) -> bool:
+        return self.k in (2, 6)
+
+
+def phase_add(a: ParamPhase, b: ParamPhase) -> ParamPhase:
+    """phase.hpp:55-60."""
+    return ParamPhase((a.k + b.k) & 7, a.mask ^ b.mask)
+
+
+class SubtermKind(enum.IntEnum):
+    Node = 0
+    PhasePair = 1
+    HalfPi = 2
+    PiPair = 3
+
+
+@dataclass(frozen=True)
+class Subterm:
+    kind: SubtermKind
+    psi: ParamPhase
+    phi: ParamPhase = ParamPhase()
+
+    @staticmethod
+    def node(psi: ParamPhase) -> "Subterm":
+        return Subterm(SubtermKind.Node, psi)
+
+    @staticmethod
+    def phase_pair(psi: ParamPhase, phi: ParamPhase) -> "Subterm":
+        return Subterm(SubtermKind.PhasePair, psi, phi)
+
+    @staticmethod
+    def half_pi(psi: ParamPhase) -> "Subterm":
+        if not psi.proper_clifford_image():  # subterm.cpp:5-10
+            raise DomainError("half-pi subterm needs Image(psi) in {pi/2, 3pi/2}")
+        return Subterm(SubtermKind.HalfPi, psi)
+
+    @staticmethod
+    def pi_pair(psi: ParamPhase, phi: ParamPhase) -> "Subterm":
+        if phi.pauli_image():  # subterm.cpp:12-21
+            return Subterm(SubtermKind.PiPair, psi, phi)
+        if psi.pauli_image():
+            return Subterm(SubtermKind.PiPair, phi, psi)
+        raise DomainError("pi-pair subterm needs a phase with image in {0, pi}")
+
+    def param_mask(self) -> int:
+        return self.psi.mask | self.phi.mask
+
+
+# -------------------------------------------------------------- RingQuad ----
+@dataclass(frozen=True)
+class RingQuad:
+    """(a + b*sqrt2 + i(c + d*sqrt2)) / 2^exp, canonical (ring.cpp:20-48)."""
+
+    a: int = 0
+    b: int = 0
+    c: int = 0
+    d: int = 0
+    exp: int = 0
+
+    @staticmethod
+    def make(a: int, b: int, c: int, d: int, exp: int) -> "RingQuad":
+        while exp < 0:
+            a, b, c, d, exp = 2 * a, 2 * b, 2 * c, 2 * d, exp + 1
+        if a == b == c == d == 0:
+            return RingQuad()
+        while exp > 0 and not ((a | b | c | d) & 1):
+            a, b, c, d, exp = a >> 1, b >> 1, c >> 1, d >> 1, exp - 1
+        for v in (a, b, c, d):
+            if not (-(2**63) <= v < 2**63):
+                raise OverflowError("ring coefficient out of 64-bit range")
+        return RingQuad(a, b, c, d, exp)
+
+    @staticmethod
+    def one() -> "RingQuad":
+        return RingQuad(1, 0, 0, 0, 0)
+
+    def __mul__(self, o: "RingQuad") -> "RingQuad":
+        x, y = self, o
+        return RingQuad.make(x.a * y.a + 2 * x.b * y.b - x.c * y.c - 2 * x.d * y.d,
+                             x.a * y.b + x.b * y.a - x.c * y.d - x.d * y.c,
+                             x.a * y.c + 2 * x.b * y.d + x.c * y.a + 2 * x.d * y.b,
+                             x.a * y.d + x.b * y.c + x.c * y.b + x.d * y.a, x.exp + y.exp)
+
+    def __add__(self, o: "RingQuad") -> "RingQuad":
+        e = max(self.exp, o.exp)
+        sx, sy = e - self.exp, e - o.exp
+        return RingQuad.make(self.a * 2**sx + o.a * 2**sy, self.b * 2**sx + o.b * 2**sy,
+                             self.c * 2**sx + o.c * 2**sy, self.d * 2**sx + o.d * 2**sy, e)
+
+    def to_complex(self) -> complex:
+        s2 = 2.0 ** 0.5
+        sc = 2.0 ** -self.exp
+        return complex((float(self.a) + float(self.b) * s2) * sc, (float(self.c) + float(self.d) * s2) * sc)
+
+    def as_tuple(self) -> tuple:
+        return (self.a, self.b, self.c, self.d, self.exp)
+
+
+# ------------------------------------------------------ ScalarExpression ----
+@dataclass
+class ScalarExpression:
+    """Leaf-term list: value(a) = sum_t C_t * prod_j subterm_value(S_tj, a).
+
+    Stored structure-of-arrays (numpy) so that million-term synthetic tables
+    and small hand-written ones share one path to the C ABI.
+    """
+
+    n_params: int
+    term_offset: np.ndarray = field(default_factory=lambda: np.zeros(1, np.uint64))
+    term_scalar: np.ndarray = field(default_factory=lambda: np.zeros((0, 5), np.int64))
+    kind: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    psi_k: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    psi_mask: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    phi_k: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    phi_mask: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+
+    @staticmethod
+    def from_terms(n_params: int, terms: Iterable[tuple[RingQuad, Sequence[Subterm]]]) -> "ScalarExpression":
+        if n_params > kMaxParams:
+            raise DomainError("parameter capacity (64) exceeded")
+        off, sc, kd, pk, pm, fk, fm = [0], [], [], [], [], [], []
+        for c, subs in terms:
+            sc.append(c.as_tuple())
+            for s in subs:
+                kd.append(int(s.kind)); pk.append(s.psi.k); pm.append(s.psi.mask)
+                fk.append(s.phi.k); fm.append(s.phi.mask)
+            off.append(len(kd))
+        return ScalarExpression(
+            n_params, np.asarray(off, np.uint64), np.asarray(sc, np.int64).reshape(-1, 5),
+            np.asarray(kd, np.uint8), np.asarray(pk, np.uint8), np.asarray(pm, np.uint64),
+            np.asarray(fk, np.uint8), np.asarray(fm, np.uint64))
+
+    @property
+    def n_terms(self) -> int:
+        return len(self.term_offset) - 1
+
+    @property
+    def n_subterms(self) -> int:
+        return int(self.term_offset[-1]) if len(self.term_offset) else 0
+
+    def terms(self):
+        """Iterate (RingQuad, [Subterm]) -- for small expressions / tests."""
+        for t in range(self.n_terms):
+            subs = []
+            for j in range(int(self.term_offset[t]), int(self.term_offset[t + 1])):
+                subs.append(Subterm(SubtermKind(int(self.kind[j])),
+                                    ParamPhase(int(self.psi_k[j]), int(self.psi_mask[j])),
+                                    ParamPhase(int(self.phi_k[j]), int(self.phi_mask[j]))))
+            yield RingQuad(*map(int, self.term_scalar[t])), subs
+
+    def slice_terms(self, t0: int, t1: int) -> "ScalarExpression":
+        """Contiguous term range (absolute subterm indices are kept)."""
+        return ScalarExpression(self.n_params, self.term_offset[t0:t1 + 1], self.term_scalar[t0:t1],
+                                self.kind, self.psi_k, self.psi_mask, self.phi_k, self.phi_mask)
+
+    def _arrays(self):
+        a = [np.ascontiguousarray(self.term_offset, np.uint64),
+             np.ascontiguousarray(self.term_scalar, np.int64).reshape(-1),
+             np.ascontiguousarray(self.kind, np.uint8), np.ascontiguousarray(self.psi_k, np.uint8),
+             np.ascontiguousarray(self.psi_mask, np.uint64), np.ascontiguousarray(self.phi_k, np.uint8),
+             np.ascontiguousarray(self.phi_mask, np.uint64)]
+        return [x if x.size else np.zeros(1, x.dtype) for x in a]
+
+    def view(self):
+        arrs = self._arrays()
+        v = N.ExprView(self.n_params, self.n_terms, N.ptr(arrs[0], C.c_uint64), N.ptr(arrs[1], C.c_int64),
+                       N.ptr(arrs[2], C.c_uint8), N.ptr(arrs[3], C.c_uint8), N.ptr(arrs[4], C.c_uint64),
+                       N.ptr(arrs[5], C.c_uint8), N.ptr(arrs[6], C.c_uint64))
+        return v, arrs  # keep arrays alive while the view is used
+
+
+# ---------------------------------------------------------------- device ----
+PROB_ABS2 = 1
+PROB_REAL = 2
+KERNEL_GENERAL = 1 << 8
+KERNEL_GRAY = 1 << 9
+
+
+class DeviceTable:
+    """Device-resident compiled table (immutable; SPEC BitTable S:336-339)."""
+
+    def __init__(self, ctx: "Context", handle: C.c_void_p):
+        self._ctx = ctx
+        self.handle = handle
+        L = N.lib()
+        p, m, r, mx = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _check(L.pzx_table_shape(handle, C.byref(p), C.byref(m), C.byref(r), C.byref(mx)))
+        self.n_params, self.n_terms, self.n_rows, self.max_term_rows = p.value, m.value, r.value, mx.value
+
+    def term_info(self, t: int):
+        coef = np.zeros(5, np.int64)
+        e, lm = C.c_int32(), C.c_int32()
+        _check(N.lib().pzx_table_term_info(self.handle, t, N.ptr(coef, C.c_int64), C.byref(e), C.byref(lm)))
+        return RingQuad(*map(int, coef)), e.value, lm.value
+
+    def free(self) -> None:
+        if self.handle:
+            N.lib().pzx_table_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One device, one stream (pzx_ctx). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        L = N.lib()
+        h = C.c_void_p()
+        _check(L.pzx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib().pzx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def launch_count(self) -> int:
+        return int(N.lib().pzx_launch_count(self.handle))
+
+    # -- compile + upload ---------------------------------------------------
+    def compile_bit_table(self, expr: ScalarExpression) -> DeviceTable:
+        v, keep = expr.view()
+        h = C.c_void_p()
+        _check(N.lib().pzx_table_upload_expr(self.handle, C.byref(v), C.byref(h)), self.handle)
+        del keep
+        return DeviceTable(self, h)
+
+    def upload_rows(self, n_params, term_row_offset, term_coef, psi_mask, phi_mask, k_alpha, k_beta) -> DeviceTable:
+        arrs = [np.ascontiguousarray(term_row_offset, np.uint64), np.ascontiguousarray(term_coef, np.int64).reshape(-1),
+                np.ascontiguousarray(psi_mask, np.uint64), np.ascontiguousarray(phi_mask, np.uint64),
+                np.ascontiguousarray(k_alpha, np.uint8), np.ascontiguousarray(k_beta, np.uint8)]
+        arrs = [x if x.size else np.zeros(1, x.dtype) for x in arrs]
+        v = N.TableView(n_params, len(term_row_offset) - 1, N.ptr(arrs[0], C.c_uint64), N.ptr(arrs[1], C.c_int64),
+                        N.ptr(arrs[2], C.c_uint64), N.ptr(arrs[3], C.c_uint64), N.ptr(arrs[4], C.c_uint8),
+                        N.ptr(arrs[5], C.c_uint8))
+        h = C.c_void_p()
+        _check(N.lib().pzx_table_upload(self.handle, C.byref(v), C.byref(h)), self.handle)
+        return DeviceTable(self, h)
+
+    # -- evaluation -----------------------------------------------------------
+    def evaluate_batch(self, table: DeviceTable, assignments, *, prob: bool = False,
+                       prob_real: bool = False, flags: int = 0):
+        """Amplitudes (complex128) at assignment words, input order kept."""
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        n = a.size
+        amp = np.empty(n, np.complex128)
+        pr = np.empty(n, np.float64) if (prob or prob_real) else None
+        fl = flags | (PROB_REAL if prob_real else PROB_ABS2)
+        if n:
+            _check(N.lib().pzx_evaluate(self.handle, table.handle, N.ptr(a, C.c_uint64), n,
+                                        amp.ctypes.data_as(N.dblp), N.ptr(pr, C.c_double), fl), self.handle)
+        return (amp, pr) if pr is not None else amp
+
+    def evaluate(self, table: DeviceTable, word: int) -> complex:
+        return complex(self.evaluate_batch(table, [word])[0])
+
+    def evaluate_range(self, table: DeviceTable, first: int, n: int, *, prob: bool = False,
+                       prob_real: bool = False, flags: int = 0):
+        amp = np.empty(n, np.complex128)
+        pr = np.empty(n, np.float64) if (prob or prob_real) else None
+        fl = flags | (PROB_REAL if prob_real else PROB_ABS2)
+        if n:
+            _check(N.lib().pzx_evaluate_range(self.handle, table.handle, first, n, amp.ctypes.data_as(N.dblp),
+                                              N.ptr(pr, C.c_double), fl), self.handle)
+        return (amp, pr) if pr is not None else amp
+
+    def evaluate_device(self, table: DeviceTable, n: int, *, d_assignments: int = 0, first: int = 0,
+                        term_begin: int = 0, term_end: int = 2**64 - 1, d_amp: int = 0, d_prob: int = 0,
+                        flags: int = PROB_ABS2, stream: int = 0) -> None:
+        """Async device-pointer form (raw CUDA pointers as ints, e.g. torch data_ptr())."""
+        _check(N.lib().pzx_evaluate_device(self.handle, table.handle, d_assignments or None, first, n,
+                                           term_begin, term_end, d_amp or None, d_prob or None, flags,
+                                           stream or None), self.handle)
+
+    def amp_to_prob_device(self, d_amp: int, n: int, d_prob: int, flags: int = PROB_ABS2, stream: int = 0):
+        _check(N.lib().pzx_amp_to_prob_device(self.handle, d_amp, n, d_prob, flags, stream or None), self.handle)
+
+    def synchronize(self) -> None:
+        _check(N.lib().pzx_synchronize(self.handle), self.handle)
+
+    # -- debug / parity hooks -------------------------------------------------
+    def debug_phase_indices(self, table: DeviceTable, assignments) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        out = np.empty((table.n_rows, a.size), np.uint8)
+        if out.size:
+            _check(N.lib().pzx_debug_phase_indices(self.handle, table.handle, N.ptr(a, C.c_uint64), a.size,
+                                                   N.ptr(out, C.c_uint8)), self.handle)
+        return out
+
+    def debug_term_codes(self, table: DeviceTable, assignments) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        out = np.zeros((table.n_terms, a.size, 5), np.uint32)
+        if out.size:
+            _check(N.lib().pzx_debug_term_codes(self.handle, table.handle, N.ptr(a, C.c_uint64), a.size,
+                                                out.ctypes.data_as(C.POINTER(N.TermCode))), self.handle)
+        return out
+
+
+class HostTable:
+    """Host-only compiled table (pzx_table_compile_host): inspection and CPU tests."""
+
+    def __init__(self, expr: ScalarExpression):
+        v, keep = expr.view()
+        h = C.c_void_p()
+        _check(N.lib().pzx_table_compile_host(C.byref(v), C.byref(h)))
+        del keep
+        self.handle = h
+        L = N.lib()
+        p, m, r, mx = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _check(L.pzx_table_shape(h, C.byref(p), C.byref(m), C.byref(r), C.byref(mx)))
+        self.n_params, self.n_terms, self.n_rows, self.max_term_rows = p.value, m.value, r.value, mx.value
+
+    term_info = DeviceTable.term_info
+    free = DeviceTable.free
+    __del__ = DeviceTable.__del__
+
+
+def class_table():
+    """(codes[64,4] uint32, e[64], lm[64]) -- the kernels' per-class variant codes."""
+    codes = np.zeros(256, np.uint32)
+    e = np.zeros(64, np.int32)
+    lm = np.zeros(64, np.int32)
+    _check(N.lib().pzx_class_table(N.ptr(codes, C.c_uint32), N.ptr(e, C.c_int32), N.ptr(lm, C.c_int32)))
+    return codes.reshape(64, 4), e, lm
+
+
+def compile_bit_table(expr: ScalarExpression, ctx: Context) -> DeviceTable:
+    """SPEC compile_bit_table: normalise, classify, upload."""
+    return ctx.compile_bit_table(expr)
+
+
+def evaluate_batch(ctx: Context, table: DeviceTable, assignments) -> np.ndarray:
+    """SPEC evaluate_batch; output order equals input order."""
+    return ctx.evaluate_batch(table, assignments)
+
+
+def evaluate(ctx: Context, table: DeviceTable, word: int) -> complex:
+    """SPEC evaluate."""
+    return ctx.evaluate(table, word)
+
+
+__all__ = [
+    "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
+    "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
+    "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
+    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY",
+]
+_ = builtins

@@ -1,0 +1,123 @@
+"""Seeded synthetic leaf-term lists for the BASELINE configs.
+
+The reference ships no circuits and no reducer, so the term
+tables are synthetic with the statistics SURVEY §8(d) fixes:
+
+* raw subterm kinds PiPair 0.5 / HalfPi 0.2 / Node 0.2 / PhasePair 0.1;
+* phase constants drawn inside each kind's invariant (subterm.cpp:5-21):
+  HalfPi k in {2, 6}; PiPair phi.k in {0, 4}; "general" mix allows odd k
+  (T-like) everywhere else, "clifford" mix only even k;
+* every mask bit set i.i.d. with rho = 0.25 over the P parameters, a mask is
+  never empty (an all-empty subterm would have been folded by push_subterm,
+  diagram.cpp:114-120);
+* n_t ~ U[n_lo, n_hi] subterms per term;
+* C_t = RingQuad::make(U[-8, 8]^4, exp = n_t), never zero;
+* bit generator MT19937 seeded with 20261018 + config id.
+
+Everything is plain numpy; the same arrays feed the GPU path and both CPU
+baselines, so every arm sees identical inputs.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .pzx import ScalarExpression
+
+
+@dataclass(frozen=True)
+class Config:
+    cid: int
+    name: str
+    n_params: int
+    n_terms: int
+    n_lo: int
+    n_hi: int
+    n_assign: int
+    enumerated: bool
+    prob_real: bool = False
+    mix: str = "general"
+
+
+CONFIGS = {
+    "c1": Config(1, "C1: P=8, all 2^8 amplitudes (8 qubits, T=20)", 8, 1 << 10, 8, 24, 1 << 8, True),
+    "c2": Config(2, "C2: P=20, all 2^20 amplitudes (20 qubits, T=40)", 20, 1 << 17, 16, 48, 1 << 20, True),
+    "c3": Config(3, "C3: P=30, 2^24 sampled probabilities (30 qubits, T=60)", 30, 1 << 18, 24, 56, 1 << 24, False),
+    "c4": Config(4, "C4: P=10 doubled-diagram marginals, 2^10 params (term split)", 10, 1 << 22, 32, 64, 1 << 10,
+                 True, prob_real=True),
+    "c5": Config(5, "C5: P=32, T>=100 term-split table (> L2)", 32, 1 << 24, 32, 64, 1 << 16, False),
+}
+
+KIND_P = (0.2, 0.1, 0.2, 0.5)  # Node, PhasePair, HalfPi, PiPair  (SubtermKind order)
+
+
+def _masks(rng: np.random.Generator, n: int, P: int) -> np.ndarray:
+    full = np.uint64((1 << P) - 1) if P < 64 else np.uint64(2**64 - 1)
+    m = (rng.integers(0, 2**64, n, dtype=np.uint64, endpoint=False)
+         & rng.integers(0, 2**64, n, dtype=np.uint64, endpoint=False)) & full
+    empty = m == 0
+    if empty.any():
+        m[empty] = np.left_shift(np.uint64(1), rng.integers(0, P, int(empty.sum())).astype(np.uint64))
+    return m
+
+
+def _canon_scalars(vals: np.ndarray, exps: np.ndarray) -> np.ndarray:
+    """RingQuad::make canonical form (ring.cpp:20-48) on int64 rows."""
+    v = vals.astype(np.int64).copy()
+    e = exps.astype(np.int64).copy()
+    while True:
+        even = ((v[:, 0] | v[:, 1] | v[:, 2] | v[:, 3]) & 1) == 0
+        sel = even & (e > 0)
+        if not sel.any():
+            break
+        v[sel] //= 2
+        e[sel] -= 1
+    return np.concatenate([v, e[:, None]], axis=1)
+
+
+def generate(n_params: int, n_terms: int, n_lo: int, n_hi: int, seed: int, mix: str = "general",
+             kind_p=KIND_P, exp_cap: int | None = None) -> ScalarExpression:
+    rng = np.random.Generator(np.random.MT19937(seed))
+    P = n_params
+    n = rng.integers(n_lo, n_hi + 1, n_terms)
+    off = np.zeros(n_terms + 1, np.uint64)
+    np.cumsum(n, out=off[1:])
+    S = int(off[-1])
+    kind = rng.choice(4, size=S, p=kind_p).astype(np.uint8)
+    psi_k = rng.integers(0, 8, S).astype(np.uint8)
+    phi_k = rng.integers(0, 8, S).astype(np.uint8)
+    if mix == "clifford":
+        psi_k &= np.uint8(6)
+        phi_k &= np.uint8(6)
+    half = kind == 2
+    psi_k[half] = np.where(rng.integers(0, 2, int(half.sum())) == 0, 2, 6).astype(np.uint8)
+    pip = kind == 3
+    phi_k[pip] = np.where(rng.integers(0, 2, int(pip.sum())) == 0, 0, 4).astype(np.uint8)
+    single = (kind == 0) | half
+    phi_k[single] = 0
+    psi_mask = _masks(rng, S, P)
+    phi_mask = _masks(rng, S, P)
+    phi_mask[single] = 0
+    vals = rng.integers(-8, 9, (n_terms, 4))
+    zero = ~vals.any(axis=1)
+    while zero.any():
+        vals[zero] = rng.integers(-8, 9, (int(zero.sum()), 4))
+        zero = ~vals.any(axis=1)
+    scal = _canon_scalars(vals, n if exp_cap is None else np.minimum(n, exp_cap))
+    return ScalarExpression(P, off, scal, kind, psi_k, psi_mask, phi_k, phi_mask)
+
+
+def generate_config(cfg: Config, n_terms: int | None = None) -> ScalarExpression:
+    return generate(cfg.n_params, cfg.n_terms if n_terms is None else n_terms, cfg.n_lo, cfg.n_hi,
+                    20261018 + cfg.cid, cfg.mix)
+
+
+def assignments(cfg: Config, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
+    """The config's assignment batch: enumerated 0..N-1 or seeded uniform P-bit words."""
+    N = cfg.n_assign if n is None else n
+    if cfg.enumerated:
+        return np.arange(N, dtype=np.uint64)
+    rng = np.random.Generator(np.random.MT19937(20261018 + 100 * cfg.cid + seed_offset))
+    full = (1 << cfg.n_params) - 1 if cfg.n_params < 64 else 2**64 - 1
+    return rng.integers(0, 2**64, N, dtype=np.uint64) & np.uint64(full)

@@ -1,0 +1,202 @@
+"""GPU parity: the sm_100a path against the CPU oracle (pinned to the reference).
+
+Bars (north_star): phase indices bit-exact; per-term products bit-exact (exact
+exponent codes, reconstructed with big integers); amplitudes within
+
+    |amp_gpu - amp_ref| <= 1e-12 * max(|amp_ref|, rms(amp_ref over the batch))
+
+i.e. 1e-12 relative, with the batch RMS as the floor for amplitudes that
+cancel to (near) zero. Every call goes through the C ABI (ctypes).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2403_06777_b200 as P
+from paper_2403_06777_b200 import synth
+from zw_exact import ZQ, term_from_code
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+GOLDENS = sorted(glob.glob(os.path.join(GOLD, "expr_*.npz")))
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def load(path):
+    z = np.load(path)
+    e = P.ScalarExpression(int(z["n_params"]), z["term_offset"], z["term_scalar"], z["kind"], z["psi_k"],
+                           z["psi_mask"], z["phi_k"], z["phi_mask"])
+    return e, z
+
+
+def assert_close(got, want, tol=TOL):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape
+    floor = np.sqrt(np.mean(np.abs(want) ** 2)) if want.size else 0.0
+    scale = np.maximum(np.abs(want), floor)
+    err = np.abs(got - want)
+    bad = err > tol * scale + 1e-300
+    assert not bad.any(), f"max rel err {np.max(err / np.maximum(scale, 1e-300)):.3e} at {np.argmax(bad)}"
+    return float(np.max(err / np.maximum(scale, 1e-300))) if want.size else 0.0
+
+
+@pytest.mark.parametrize("path", GOLDENS)
+def test_phase_indices_bit_exact(ctx, path):
+    e, z = load(path)
+    t = ctx.compile_bit_table(e)
+    words = z["words"][:32]
+    got = ctx.debug_phase_indices(t, words)
+    want = O.phase_indices(e, words)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("path", GOLDENS)
+def test_term_products_bit_exact(ctx, path):
+    e, z = load(path)
+    t = ctx.compile_bit_table(e)
+    words = z["words"][:8]
+    codes = ctx.debug_term_codes(t, words)
+    for term in range(min(t.n_terms, 40)):
+        coef, E, nlm = t.term_info(term)
+        for wi, w in enumerate(words):
+            j, zz, s1, a, b = (int(v) for v in codes[term, wi])
+            got = term_from_code(coef.as_tuple(), E, nlm, j, zz, s1, a, b)
+            assert got == ZQ.from_quad(O.term_value(e, term, int(w))), (term, int(w))
+
+
+@pytest.mark.parametrize("path", GOLDENS)
+@pytest.mark.parametrize("kernel", ["auto", "general"])
+def test_amplitudes_vs_reference_goldens(ctx, path, kernel):
+    e, z = load(path)
+    t = ctx.compile_bit_table(e)
+    flags = P.KERNEL_GENERAL if kernel == "general" else 0
+    amp, prob = ctx.evaluate_batch(t, z["words"], prob=True, flags=flags)
+    assert_close(amp, z["amp"])
+    assert_close(prob, np.abs(z["amp"]) ** 2, 1e-11)
+
+
+@pytest.mark.parametrize("path", [p for p in GOLDENS if "p8" in p])
+def test_enumerated_range_kernels(ctx, path):
+    e, z = load(path)
+    t = ctx.compile_bit_table(e)
+    n = len(z["words"])
+    a_gray = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GRAY)
+    a_gen = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GENERAL)
+    assert_close(a_gray, z["amp"])
+    assert_close(a_gen, z["amp"])
+    # unaligned start (general kernel) and ragged length
+    assert_close(ctx.evaluate_range(t, 3, n - 7), z["amp"][3:n - 4])
+
+
+def test_random_assignments_mid_size(ctx):
+    e = synth.generate(20, 4096, 16, 48, 77)
+    t = ctx.compile_bit_table(e)
+    rng = np.random.default_rng(3)
+    words = rng.integers(0, 2**64, 4096, dtype=np.uint64)
+    amp = ctx.evaluate_batch(t, words)
+    idx = rng.choice(len(words), 48, replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+
+
+def test_p64_and_high_bits(ctx):
+    e = synth.generate(64, 256, 4, 20, 5)
+    t = ctx.compile_bit_table(e)
+    words = np.random.default_rng(9).integers(0, 2**64, 300, dtype=np.uint64)
+    _, want = O.eval_batch(e, words, 8)
+    assert_close(ctx.evaluate_batch(t, words), want)
+    # P < 64: bits >= P are ignored (ParamAssignment::total, phase.hpp:18-23)
+    e2 = synth.generate(12, 128, 4, 20, 6)
+    t2 = ctx.compile_bit_table(e2)
+    lo = words & np.uint64(0xFFF)
+    assert np.array_equal(ctx.evaluate_batch(t2, words), ctx.evaluate_batch(t2, lo))
+
+
+def test_edge_cases(ctx):
+    one = P.RingQuad.one()
+    # empty expression: S = 0
+    t = ctx.compile_bit_table(P.ScalarExpression.from_terms(4, []))
+    assert np.all(ctx.evaluate_range(t, 0, 16) == 0)
+    # a term without assignment-dependent rows is its constant (BSS target S:474)
+    half = P.RingQuad.make(1, 0, 0, 0, 1)
+    node = P.Subterm.node(P.ParamPhase(1, 0))  # (1 + w), parameter-free -> folded
+    t = ctx.compile_bit_table(P.ScalarExpression.from_terms(3, [(P.RingQuad.make(1, 0, 0, 0, 6), [node] * 6)]))
+    v = ctx.evaluate_range(t, 0, 8)
+    assert_close(v, np.full(8, complex(-0.4397208691207961, 0.4397208691207961)))
+    # single row, S:455-456 examples through the whole path
+    pp = P.Subterm.phase_pair(P.ParamPhase(0, 1), P.ParamPhase(0, 1))
+    t = ctx.compile_bit_table(P.ScalarExpression.from_terms(1, [(one, [pp])]))
+    assert_close(ctx.evaluate_batch(t, [0, 1]), np.array([2.0, -2.0]))
+    # Clifford-only table, C = 1/2
+    t = ctx.compile_bit_table(P.ScalarExpression.from_terms(0, [(half, [])]))
+    assert_close(ctx.evaluate_batch(t, [0, 5]), np.array([0.5, 0.5]))
+    # n = 0 and n = 1
+    assert ctx.evaluate_batch(t, []).size == 0
+    # Re(value) output for doubled diagrams
+    _, pr = ctx.evaluate_range(t, 0, 4, prob_real=True)
+    assert np.allclose(pr, 0.5, rtol=0, atol=1e-15)
+    # validation at upload
+    with pytest.raises(P.MissingParameter):
+        ctx.compile_bit_table(P.ScalarExpression.from_terms(2, [(one, [P.Subterm.node(P.ParamPhase(1, 4))])]))
+
+
+def test_long_terms_segment_path(ctx):
+    path = [p for p in GOLDENS if "long" in p][0]
+    e, z = load(path)
+    t = ctx.compile_bit_table(e)
+    assert t.max_term_rows > 127
+    assert_close(ctx.evaluate_batch(t, z["words"]), z["amp"])
+    assert_close(ctx.evaluate_batch(t, z["words"], flags=P.KERNEL_GENERAL), z["amp"])
+
+
+def test_device_pointer_api_and_term_split(ctx):
+    torch = pytest.importorskip("torch")
+    e = synth.generate(10, 3000, 16, 40, 21)
+    t = ctx.compile_bit_table(e)
+    n = 1024
+    full = ctx.evaluate_range(t, 0, n)
+    amp = torch.zeros(2 * n, dtype=torch.float64, device="cuda:0")
+    part = torch.zeros(2 * n, dtype=torch.float64, device="cuda:0")
+    cut = 1234
+    st = torch.cuda.current_stream().cuda_stream
+    ctx.evaluate_device(t, n, first=0, term_begin=0, term_end=cut, d_amp=amp.data_ptr(), stream=st)
+    ctx.evaluate_device(t, n, first=0, term_begin=cut, d_amp=part.data_ptr(), stream=st)
+    torch.cuda.synchronize()
+    s = (amp + part).cpu().numpy().view(np.complex128)
+    assert_close(s, full, 1e-13)
+    prob = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    both = amp + part
+    ctx.amp_to_prob_device(both.data_ptr(), n, prob.data_ptr(), stream=st)
+    torch.cuda.synchronize()
+    assert_close(prob.cpu().numpy(), np.abs(full) ** 2, 1e-12)
+
+
+def test_full_size_c2_properties(ctx):
+    """BASELINE config C2 at full size: enumerated 2^20 assignments, 2^17 terms."""
+    cfg = synth.CONFIGS["c2"]
+    e = synth.generate_config(cfg)
+    t = ctx.compile_bit_table(e)
+    N = cfg.n_assign
+    amp = ctx.evaluate_range(t, 0, N)
+    # shard invariance (what the multi-GPU assignment split relies on)
+    half = ctx.evaluate_range(t, N // 2, N // 2)
+    assert_close(half, amp[N // 2:], 1e-13)
+    # general kernel on a random subset of the same words
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(N, 2048, replace=False)).astype(np.uint64)
+    assert_close(ctx.evaluate_batch(t, idx, flags=P.KERNEL_GENERAL), amp[idx.astype(np.int64)], 1e-13)
+    # oracle spot check (reference implementation where built, else the port)
+    pick = idx[:16]
+    _, want = O.eval_batch(e, pick, os.cpu_count() or 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[pick.astype(np.int64)], want)
