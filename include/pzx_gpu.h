@@ -36,7 +36,9 @@
  * bit i = parameter i, bits >= n_params ignored.
  *
  * Plain pointers and sizes only; no CUDA or torch types in the signatures
- * (streams are passed as void* = cudaStream_t, 0 = the context's stream).
+ * (streams are passed as void* = cudaStream_t and used as given: NULL is the
+ * CUDA legacy default stream; the synchronous host entry points use the
+ * context's own stream).
  */
 #ifndef PZX_GPU_H
 #define PZX_GPU_H
@@ -153,7 +155,7 @@ pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assign
 pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n,
                               double* amp, double* prob, uint32_t flags);
 
-/* Asynchronous DEVICE-pointer variants on `stream` (0 = context stream):
+/* Asynchronous DEVICE-pointer variants on `stream` (used as given, NULL = default stream):
  * d_assignments may be NULL for the enumerated batch starting at `first`.
  * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)
  * gives partial amplitudes for the term split; d_amp receives 2n doubles,

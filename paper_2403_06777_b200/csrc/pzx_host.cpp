@@ -131,9 +131,11 @@ struct HostTable {
     std::vector<Quad> coef;                 // C'_t (exact, normalisation folded)
     std::vector<int32_t> e_t, nlm_t;
     std::vector<double> term_c;             // 2 per term
-    std::vector<uint4> rows;                // P <= 32: {psi, phi, code, pat}; P > 32: masks
-    std::vector<uint2> aux;                 // P > 32: {code, pat}
+    std::vector<uint4> rows;                // P <= 32: {psi, phi, code, pat}; P > 32: 2 records per row
     std::vector<uint8_t> swapped;           // row stored with psi/phi exchanged
+    std::vector<uint8_t> unit;              // placeholder row of a row-less term
+    uint64_t n_dev_rows() const { return unit.size(); }
+    uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
     uint32_t max_rows = 0;
 };
 
@@ -144,6 +146,18 @@ uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
         pat |= uint32_t(__builtin_parityll(phi & uint64_t(g))) << (2 * g + 1);
     }
     return pat;
+}
+
+void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, uint32_t pat, uint8_t sw,
+                     uint8_t unit) {
+    if (h.n_params <= 32) {
+        h.rows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, pat));
+    } else {  // 32-byte record: masks, then {code, pattern}
+        h.rows.push_back(make_uint4(uint32_t(psi), uint32_t(psi >> 32), uint32_t(phi), uint32_t(phi >> 32)));
+        h.rows.push_back(make_uint4(code, pat, 0, 0));
+    }
+    h.swapped.push_back(sw);
+    h.unit.push_back(unit);
 }
 
 void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
@@ -157,20 +171,25 @@ void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
     const ClassInfo& ci = classes().c[cls];
     e += ci.e;
     lm += ci.lm;
-    const uint32_t code = uint32_t(cls) * 16u;
-    const uint32_t pat = walsh_pattern(pr.psi, pr.phi);
-    if (h.n_params <= 32) {
-        h.rows.push_back(make_uint4(uint32_t(pr.psi), uint32_t(pr.phi), code, pat));
-    } else {
-        h.rows.push_back(make_uint4(uint32_t(pr.psi), uint32_t(pr.psi >> 32), uint32_t(pr.phi),
-                                    uint32_t(pr.phi >> 32)));
-        h.aux.push_back(make_uint2(code, pat));
-    }
-    h.swapped.push_back(sw);
+    push_device_row(h, pr.psi, pr.phi, uint32_t(cls) * 16u, walsh_pattern(pr.psi, pr.phi), sw, 0);
 }
 
-int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t n_rows_term) {
+uint32_t& code_word(HostTable& h, uint64_t i) { return h.n_params <= 32 ? h.rows[i].z : h.rows[2 * i + 1].x; }
+
+// Close a term: a term without assignment-dependent rows gets one unit row
+// (class kUnitClass, all-zero codes) so that every term owns >= 1 row of the
+// flat row stream; the last row carries kEndFlag and every kSegRows-th row of
+// a long term kSegFlag (the kernels flush their 7-bit SWAR fields there).
+int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
+    uint64_t n_rows_term = h.n_dev_rows() - row0;
     if (n_rows_term > uint64_t(kMaxTermRows)) return PZX_E_CAPACITY;
+    if (n_rows_term == 0) {
+        push_device_row(h, 0, 0, uint32_t(kUnitClass) * 16u, 0, 0, 1);
+        n_rows_term = 1;
+    }
+    for (uint64_t i = 0; i + 1 < n_rows_term; ++i)
+        if ((i + 1) % kSegRows == 0) code_word(h, row0 + i) |= kSegFlag;
+    code_word(h, row0 + n_rows_term - 1) |= kEndFlag;
     h.max_rows = std::max<uint32_t>(h.max_rows, uint32_t(n_rows_term));
     h.coef.push_back(c);
     h.e_t.push_back(e);
@@ -184,7 +203,7 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t n_rows_term
     for (int i = 0; i < lm; ++i) v = cmul(v, mu);
     h.term_c.push_back(double(v.re));
     h.term_c.push_back(double(v.im));
-    h.term_row.push_back(h.rows.size());
+    h.term_row.push_back(h.n_dev_rows());
     return PZX_OK;
 }
 
@@ -203,7 +222,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
         Quad c;
         if (!canon_input(v->term_scalar + 5 * t, c)) { err = "term scalar out of range"; return PZX_E_OVERFLOW; }
         int e = 0, lm = 0;
-        const uint64_t row0 = h.rows.size();
+        const uint64_t row0 = h.n_dev_rows();
         for (uint64_t j = v->term_offset[t]; j < v->term_offset[t + 1]; ++j) {
             const uint8_t kind = v->kind[j];
             const int psik = v->psi_k[j], phik = v->phi_k ? v->phi_k[j] : 0;
@@ -222,7 +241,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
             c = nc;
             if (has) push_row(h, pr, e, lm);
         }
-        int st = finish_term(h, c, e, lm, h.rows.size() - row0);
+        int st = finish_term(h, c, e, lm, row0);
         if (st) { err = "term has more rows than supported"; return st; }
     }
     return PZX_OK;
@@ -236,7 +255,7 @@ int compile_rows(const pzx_table_view* v, HostTable& h, std::string& err) {
         Quad c;
         if (!canon_input(v->term_coef + 5 * t, c)) { err = "term coefficient out of range"; return PZX_E_OVERFLOW; }
         int e = 0, lm = 0;
-        const uint64_t row0 = h.rows.size();
+        const uint64_t row0 = h.n_dev_rows();
         for (uint64_t r = v->term_row_offset[t]; r < v->term_row_offset[t + 1]; ++r) {
             if (v->k_alpha[r] > 7 || v->k_beta[r] > 7) { err = "phase index out of [0,7]"; return PZX_E_DOMAIN; }
             if ((v->psi_mask[r] | v->phi_mask[r]) & ~allowed) { err = "row mask uses a parameter >= n_params"; return PZX_E_MISSING_PARAM; }
@@ -249,7 +268,7 @@ int compile_rows(const pzx_table_view* v, HostTable& h, std::string& err) {
             }
             push_row(h, pr, e, lm);
         }
-        int st = finish_term(h, c, e, lm, h.rows.size() - row0);
+        int st = finish_term(h, c, e, lm, row0);
         if (st) { err = "term has more rows than supported"; return st; }
     }
     return PZX_OK;
@@ -260,7 +279,7 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
     auto align16 = [](uint32_t x) { return (x + 15u) & ~15u; };
     L.max_rows = M;
     L.codes_off = 0;
-    L.om_off = align16(L.codes_off + 64 * 4 * 4);
+    L.om_off = align16(L.codes_off + kCodeClasses * 4 * 4);
     L.u_off = align16(L.om_off + 8 * 16);
     L.p3_off = align16(L.u_off + 8 * (M + 1));
     L.pd_off = align16(L.p3_off + 8 * (M / 2 + 1));
@@ -269,6 +288,7 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
     uint32_t* codes = reinterpret_cast<uint32_t*>(blob.data() + L.codes_off);
     for (int c = 0; c < 64; ++c)
         for (int v = 0; v < 4; ++v) codes[c * 4 + v] = classes().c[c].code[v];
+    for (int v = 0; v < 4; ++v) codes[kUnitClass * 4 + v] = 0;  // unit row: value 1
     double* om = reinterpret_cast<double*>(blob.data() + L.om_off);
     for (int j = 0; j < 8; ++j) {
         const C128 w = zw_to_c128(zw_pow_w(j));
@@ -317,7 +337,6 @@ struct pzx_table {
     DevTable dev;
     HostTable host;
     void* d_rows = nullptr;
-    void* d_aux = nullptr;
     void* d_term_row = nullptr;
     void* d_term_c = nullptr;
     void* d_lut = nullptr;
@@ -360,7 +379,6 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_rows, h.rows), "upload rows"))) return st;
-    if (h.n_params > 32 && (st = cuda_err(ctx, upload_vec(&t->d_aux, h.aux), "upload aux"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_row, h.term_row), "upload term offsets"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_c, h.term_c), "upload term constants"))) return st;
     LutLayout L;
@@ -368,13 +386,12 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     if ((st = cuda_err(ctx, upload_vec(&t->d_lut, blob), "upload lut"))) return st;
     DevTable& d = t->dev;
     d.rows = static_cast<const uint4*>(t->d_rows);
-    d.aux = static_cast<const uint2*>(t->d_aux);
     d.term_row = static_cast<const uint64_t*>(t->d_term_row);
     d.term_c = static_cast<const double2*>(t->d_term_c);
     d.lut = static_cast<const unsigned char*>(t->d_lut);
     d.lut_layout = L;
     d.n_terms = h.coef.size();
-    d.n_rows = h.rows.size();
+    d.n_rows = h.n_dev_rows();
     d.n_params = h.n_params;
     d.max_rows = h.max_rows;
     d.p64 = h.n_params > 32;
@@ -523,7 +540,7 @@ pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out) {
     if (st) return pzx_status(st);
     t->device = -1;
     t->dev.n_terms = t->host.coef.size();
-    t->dev.n_rows = t->host.rows.size();
+    t->dev.n_rows = t->host.n_dev_rows();
     t->dev.n_params = t->host.n_params;
     t->dev.max_rows = t->host.max_rows;
     *out = t.release();
@@ -546,7 +563,7 @@ void pzx_table_free(pzx_table* t) {
     if (!t) return;
     if (t->device < 0) { delete t; return; }
     cudaSetDevice(t->device);
-    for (void* p : {t->d_rows, t->d_aux, t->d_term_row, t->d_term_c, t->d_lut})
+    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut})
         if (p) cudaFree(p);
     delete t;
 }
@@ -556,7 +573,7 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
     if (!t) return PZX_E_INVALID;
     if (n_params) *n_params = t->host.n_params;
     if (n_terms) *n_terms = t->dev.n_terms;
-    if (n_rows) *n_rows = t->dev.n_rows;
+    if (n_rows) *n_rows = t->host.genuine_rows();
     if (max_term_rows) *max_term_rows = t->host.max_rows;
     return PZX_OK;
 }
@@ -627,7 +644,7 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
     if (!ctx || !t) return PZX_E_INVALID;
     if (n == 0) return PZX_OK;
     LaunchReq r;
-    r.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    r.stream = static_cast<cudaStream_t>(stream);
     r.d_asg = d_assignments;
     r.first = first;
     r.n = n;
@@ -644,7 +661,7 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
 pzx_status pzx_amp_to_prob_device(pzx_ctx* ctx, const double* d_amp, uint64_t n, double* d_prob,
                                   uint32_t flags, void* stream) {
     if (!ctx || (n && (!d_amp || !d_prob))) return PZX_E_INVALID;
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     return cuda_err(ctx, launch_amp_to_prob(reinterpret_cast<const double2*>(d_amp), n, d_prob,
                                             prob_mode_of(flags), s, &ctx->launches), "amp_to_prob");
 }
@@ -657,7 +674,8 @@ pzx_status pzx_synchronize(pzx_ctx* ctx) {
 pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
                                    uint64_t n, uint8_t* idx_out) {
     if (!ctx || !t || (n && (!assignments || !idx_out))) return PZX_E_INVALID;
-    const uint64_t R = t->dev.n_rows;
+    if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table");
+    const uint64_t R = t->dev.n_rows;  // device rows incl. unit placeholders
     if (!n || !R) return PZX_OK;
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
@@ -666,13 +684,21 @@ pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t, const uint6
     cudaMemcpyAsync(ctx->d_asg, assignments, n * 8, cudaMemcpyHostToDevice, ctx->stream);
     if ((st = cuda_err(ctx, launch_debug_phase(t->dev, static_cast<const uint64_t*>(ctx->d_asg), n,
                                                static_cast<uint8_t*>(ctx->d_dbg), ctx->stream, &ctx->launches), "debug phase"))) return st;
-    if ((st = cuda_err(ctx, cudaMemcpyAsync(idx_out, ctx->d_dbg, R * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
+    std::vector<uint8_t> all(R * n);
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(all.data(), ctx->d_dbg, R * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
     if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "debug phase"))) return st;
-    // un-swap rows stored as (phi, psi): idx = psi*8 + phi in the caller's order
+    // drop unit placeholder rows; un-swap rows stored as (phi, psi) so that
+    // idx = idx_psi*8 + idx_phi in the caller's canonical row order
+    uint64_t o = 0;
     for (uint64_t r = 0; r < R; ++r) {
-        if (!t->host.swapped[r]) continue;
-        uint8_t* o = idx_out + r * n;
-        for (uint64_t i = 0; i < n; ++i) o[i] = uint8_t(((o[i] & 7) << 3) | (o[i] >> 3));
+        if (t->host.unit[r]) continue;
+        const uint8_t* src = all.data() + r * n;
+        uint8_t* dst = idx_out + o * n;
+        if (t->host.swapped[r])
+            for (uint64_t i = 0; i < n; ++i) dst[i] = uint8_t(((src[i] & 7) << 3) | (src[i] >> 3));
+        else
+            std::memcpy(dst, src, n);
+        ++o;
     }
     return PZX_OK;
 }
@@ -680,6 +706,7 @@ pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t, const uint6
 pzx_status pzx_debug_term_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
                                 uint64_t n, pzx_term_code* out) {
     if (!ctx || !t || (n && (!assignments || !out))) return PZX_E_INVALID;
+    if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table");
     const uint64_t M = t->dev.n_terms;
     if (!n || !M) return PZX_OK;
     pzx_status st;

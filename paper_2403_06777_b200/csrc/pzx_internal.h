@@ -19,6 +19,12 @@ constexpr uint32_t kBShift = 21;  // 7 bits: number of pi' factors
 constexpr uint32_t kJShift = 29;  // 3 bits: sum of j mod 8 (wraps off the top)
 constexpr uint32_t kField = 0x7F;
 constexpr int kSegRows = 127;     // rows one SWAR accumulator can absorb
+// Flags in the row's code word (bits 0..10 hold the class byte offset cls*16)
+constexpr uint32_t kCodeMask = 0x7FFu;
+constexpr uint32_t kSegFlag = 1u << 30;  // flush the SWAR fields after this row
+constexpr uint32_t kEndFlag = 1u << 31;  // last row of its term
+constexpr int kUnitClass = 64;           // placeholder row of a row-less term (all-zero codes)
+constexpr int kCodeClasses = 65;
 constexpr int kMaxTermRows = 4095;
 
 // Rows per thread-owned block of the enumerated (Walsh / "gray") kernel:
@@ -28,7 +34,7 @@ constexpr int kGray = 1 << kGrayBits;
 
 // LUT blob (global memory, copied to shared memory by every CTA)
 struct LutLayout {
-    uint32_t codes_off;  // uint32 codes[64 classes][4 variants]
+    uint32_t codes_off;  // uint32 codes[kCodeClasses][4 variants]
     uint32_t om_off;     // double2 w^j, j = 0..7
     uint32_t u_off;      // double (sqrt2 - 1)^s, s = 0..max_rows
     uint32_t p3_off;     // double 3^m, m = 0..max_rows/2
@@ -37,15 +43,16 @@ struct LutLayout {
     int32_t max_rows;
 };
 
-// Device table. Row record for n_params <= 32 (rows32):
-//   x = psi mask, y = phi mask, z = class byte offset into codes (cls * 16),
+// Device table: ONE flat row stream in term order (every term owns >= 1 row).
+// Row record for n_params <= 32 (rows32):
+//   x = psi mask, y = phi mask, z = code word: class byte offset into codes
+//   (cls * 16) | kSegFlag | kEndFlag,
 //   w = Walsh pattern of the low kGrayBits parameters:
 //       bit 2g   = parity(psi & g), bit 2g+1 = parity(phi & g)
-// For n_params > 32 (rows64 + aux): rows64 = {psi_lo, psi_hi, phi_lo, phi_hi},
-// aux = {class offset, pattern}.
+// For n_params > 32 a row is TWO uint4: {psi_lo, psi_hi, phi_lo, phi_hi},
+// {code word, pattern, 0, 0}.
 struct DevTable {
     const uint4* rows = nullptr;
-    const uint2* aux = nullptr;
     const uint64_t* term_row = nullptr;  // [n_terms + 1], term_row[0] == 0
     const double2* term_c = nullptr;     // C''_t = C'_t * sqrt2^E_t * mu^nLM_t
     const unsigned char* lut = nullptr;

@@ -3,17 +3,26 @@
 //   p_r(a) = parity(psi_r & a), q_r(a) = parity(phi_r & a)
 // (PAPER §3.3 steps 1-7; SPEC eval_row / evaluate S:448-474).
 //
-// Design: a thread owns assignments, every thread of a CTA
-// walks the SAME rows (broadcast loads, no divergence, no dummy padding), the
-// term product is accumulated exactly in exponent form with one 32-bit SWAR
-// add per row-eval (pzx_internal.h code layout), and each term is converted
-// once per assignment to fp64 through small shared-memory tables.
+// Design:
+//  * a thread owns assignments; all threads of a CTA walk the SAME flat row
+//    stream (no divergence, no dummy padding, no per-row global loads):
+//    tiles of kTileRows rows are staged into shared memory by the TMA bulk
+//    engine (cp.async.bulk + mbarrier, double buffered) and read back as
+//    broadcast LDS.128;
+//  * the term product is accumulated EXACTLY in exponent form: one 32-bit
+//    SWAR add per row-eval of a per-(class, parity) code word
+//    (pzx_internal.h), flags in the row's code word mark term ends and
+//    7-bit-field flushes;
+//  * each term is converted once per assignment to fp64 through small
+//    shared-memory tables and accumulated into the amplitude.
 //
-//   k_eval_general<P64> : any batch; AND + POPC parity per (row, assignment).
-//   k_eval_gray<P64>    : enumerated batches; a thread owns 16 assignments
-//                         that differ only in the low 4 bits, so per row it
-//                         needs 2 POPCs for all 16 (the low-bit parities come
-//                         from the row's precomputed Walsh pattern).
+//   k_eval_general<P64, K, LONG> : any assignment batch; AND + POPC parity per
+//                                  (row, assignment), K assignments per thread.
+//   k_eval_gray<P64, GB, LONG>   : enumerated batches; a thread owns 2^GB
+//                                  assignments differing only in the low GB
+//                                  bits: per row 2 POPCs serve all of them, the
+//                                  low-bit parities come from the row's
+//                                  host-precomputed Walsh pattern.
 #include <cuda_runtime.h>
 
 #include "pzx_internal.h"
@@ -22,26 +31,72 @@ namespace pzxb {
 
 namespace {
 
+constexpr int kTileRows = 256;
+
+// ------------------------------------------------------------- PTX glue ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// ------------------------------------------------------------ LUT + math ----
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 struct SmemLut {
     const uint32_t* codes;
+    uint32_t codes_s;  // shared-window address of codes (16-aligned)
     const double2* om;
     const double* u;
     const double* p3;
     const double2* pd;  // centred: pd[d], d in [-max_rows, max_rows]
 };
 
-__device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* smem) {
+__device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* dst_bytes) {
     const uint4* src = reinterpret_cast<const uint4*>(t.lut);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
+    uint4* dst = reinterpret_cast<uint4*>(dst_bytes);
     const uint32_t n16 = t.lut_layout.bytes / 16;
     for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
-    __syncthreads();
     SmemLut L;
-    L.codes = reinterpret_cast<const uint32_t*>(smem + t.lut_layout.codes_off);
-    L.om = reinterpret_cast<const double2*>(smem + t.lut_layout.om_off);
-    L.u = reinterpret_cast<const double*>(smem + t.lut_layout.u_off);
-    L.p3 = reinterpret_cast<const double*>(smem + t.lut_layout.p3_off);
-    L.pd = reinterpret_cast<const double2*>(smem + t.lut_layout.pd_off) + t.lut_layout.max_rows;
+    L.codes = reinterpret_cast<const uint32_t*>(dst_bytes + t.lut_layout.codes_off);
+    L.codes_s = smem_u32(L.codes);
+    L.om = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.om_off);
+    L.u = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.u_off);
+    L.p3 = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.p3_off);
+    L.pd = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.pd_off) + t.lut_layout.max_rows;
     return L;
 }
 
@@ -61,20 +116,24 @@ __device__ __forceinline__ void term_epilogue(uint32_t jraw, uint32_t z, uint32_
         const double2 pd = L.pd[int(a) - int(b)];
         const double wr = w.x * pd.x - w.y * pd.y;
         const double wi = w.x * pd.y + w.y * pd.x;
-        w.x = wr; w.y = wi;
+        w.x = wr;
+        w.y = wi;
     }
-    w.x *= r; w.y *= r;
+    w.x *= r;
+    w.y *= r;
     amp.x += C.x * w.x - C.y * w.y;
     amp.y += C.x * w.y + C.y * w.x;
 }
 
 __device__ __forceinline__ void epilogue_packed(uint32_t acc, const double2 C, const SmemLut& L,
                                                 double2& amp) {
-    term_epilogue(acc >> kJShift, acc & kField, (acc >> kS1Shift) & kField,
-                  (acc >> kAShift) & kField, (acc >> kBShift) & kField, C, L, amp);
+    term_epilogue(acc >> kJShift, acc & kField, (acc >> kS1Shift) & kField, (acc >> kAShift) & kField,
+                  (acc >> kBShift) & kField, C, L, amp);
 }
 
-struct Wide { uint32_t j, z, s1, a, b; };
+struct Wide {
+    uint32_t j, z, s1, a, b;
+};
 
 __device__ __forceinline__ void widen(Wide& w, uint32_t acc) {
     w.j += acc >> kJShift;
@@ -84,8 +143,103 @@ __device__ __forceinline__ void widen(Wide& w, uint32_t acc) {
     w.b += (acc >> kBShift) & kField;
 }
 
-__device__ __forceinline__ void term_range(const DevTable& t, const LaunchReq& r, uint64_t& tb,
-                                           uint64_t& te) {
+// ------------------------------------------------------------ row stream ----
+template <bool P64>
+struct Row;
+
+template <>
+struct Row<false> {
+    uint32_t psi, phi, code, pat;
+    static constexpr int kWords = 1;  // uint4 per row
+    __device__ __forceinline__ void load(const uint4* p) {
+        const uint4 w = *p;
+        psi = w.x; phi = w.y; code = w.z; pat = w.w;
+    }
+    __device__ __forceinline__ uint32_t p(uint64_t a) const { return __popc(psi & uint32_t(a)) & 1u; }
+    __device__ __forceinline__ uint32_t q(uint64_t a) const { return __popc(phi & uint32_t(a)) & 1u; }
+};
+
+template <>
+struct Row<true> {
+    uint32_t psi_lo, psi_hi, phi_lo, phi_hi, code, pat;
+    static constexpr int kWords = 2;
+    __device__ __forceinline__ void load(const uint4* p) {
+        const uint4 w = p[0];
+        const uint4 x = p[1];
+        psi_lo = w.x; psi_hi = w.y; phi_lo = w.z; phi_hi = w.w; code = x.x; pat = x.y;
+    }
+    __device__ __forceinline__ uint32_t p(uint64_t a) const {
+        return __popc((psi_lo & uint32_t(a)) ^ (psi_hi & uint32_t(a >> 32))) & 1u;
+    }
+    __device__ __forceinline__ uint32_t q(uint64_t a) const {
+        return __popc((phi_lo & uint32_t(a)) ^ (phi_hi & uint32_t(a >> 32))) & 1u;
+    }
+};
+
+template <bool P64>
+__host__ __device__ constexpr uint32_t tile_bytes() {
+    return uint32_t(kTileRows) * Row<P64>::kWords * 16u;
+}
+
+// Shared memory: [tile 0][tile 1][2 mbarriers][LUT]
+template <bool P64>
+__host__ __device__ constexpr uint32_t smem_lut_offset() {
+    return 2 * tile_bytes<P64>() + 16;
+}
+
+// Walk the flat row stream of terms [tb, te) -- staged by TMA bulk copies --
+// calling cons.row(row) per row, cons.end_term(C) at term ends and
+// cons.flush() at 7-bit-field flush points (long terms only).
+template <bool P64, bool LONG, class Cons>
+__device__ __forceinline__ void stream_rows(const DevTable& t, uint64_t tb, uint64_t te, unsigned char* smem,
+                                            Cons& cons) {
+    constexpr int RW = Row<P64>::kWords;
+    uint4* tiles = reinterpret_cast<uint4*>(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * tile_bytes<P64>());
+    const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
+    const uint32_t ntiles = uint32_t((R1 - R0 + kTileRows - 1) / kTileRows);
+    auto issue = [&](uint32_t tile) {
+        const uint64_t r = R0 + uint64_t(tile) * kTileRows;
+        const uint64_t n = (R1 - r) < uint64_t(kTileRows) ? (R1 - r) : uint64_t(kTileRows);
+        const uint32_t bytes = uint32_t(n) * RW * 16u;
+        uint64_t* bar = &bars[tile & 1];
+        mbar_expect_tx(bar, bytes);
+        tma_load_1d(tiles + (tile & 1) * kTileRows * RW, t.rows + r * RW, bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        if (ntiles > 0) issue(0);
+        if (ntiles > 1) issue(1);
+    }
+    uint64_t term = tb;
+    double2 C = __ldg(t.term_c + tb);
+    double2 Cn = (tb + 1 < te) ? __ldg(t.term_c + tb + 1) : make_double2(0.0, 0.0);
+    for (uint32_t i = 0; i < ntiles; ++i) {
+        const uint4* buf = tiles + (i & 1) * kTileRows * RW;
+        mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+        const uint64_t rem = R1 - R0 - uint64_t(i) * kTileRows;
+        const uint32_t n = rem < uint64_t(kTileRows) ? uint32_t(rem) : uint32_t(kTileRows);
+        for (uint32_t k = 0; k < n; ++k) {
+            Row<P64> row;
+            row.load(buf + k * RW);
+            cons.row(row);
+            if (row.code & kEndFlag) {
+                cons.end_term(C);
+                C = Cn;
+                ++term;
+                Cn = (term + 1 < te) ? __ldg(t.term_c + term + 1) : make_double2(0.0, 0.0);
+            } else if (LONG && (row.code & kSegFlag)) {
+                cons.flush();
+            }
+        }
+        __syncthreads();  // every thread is done with buffer (i & 1)
+        if (threadIdx.x == 0 && i + 2 < ntiles) {
+            fence_proxy_async();
+            issue(i + 2);
+        }
+    }
+}
+
+__device__ __forceinline__ void term_range(const LaunchReq& r, uint64_t& tb, uint64_t& te) {
     if (r.n_chunks > 1) {
         tb = r.d_chunk_terms[blockIdx.y];
         te = r.d_chunk_terms[blockIdx.y + 1];
@@ -103,176 +257,146 @@ __device__ __forceinline__ void store_result(const LaunchReq& r, uint64_t idx, d
     }
     if (r.accumulate) {
         const double2 o = r.d_amp[idx];
-        amp.x += o.x; amp.y += o.y;
+        amp.x += o.x;
+        amp.y += o.y;
     }
     if (r.d_amp) r.d_amp[idx] = amp;
     if (r.d_prob) r.d_prob[idx] = r.prob_mode == 2 ? amp.x : amp.x * amp.x + amp.y * amp.y;
 }
 
-// Row access for both mask widths. parity bits are returned as 0/1.
-template <bool P64>
-struct RowView;
-
-template <>
-struct RowView<false> {
-    uint32_t psi, phi, code, pat;
-    __device__ __forceinline__ void load(const DevTable& t, uint64_t row) {
-        const uint4 w = __ldg(t.rows + row);
-        psi = w.x; phi = w.y; code = w.z; pat = w.w;
+__device__ __forceinline__ SmemLut kernel_prologue(const DevTable& t, unsigned char* smem, uint32_t lut_off) {
+    const SmemLut L = stage_lut(t, smem + lut_off);
+    if (threadIdx.x == 0) {
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lut_off - 16);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
     }
-    __device__ __forceinline__ uint32_t p(uint64_t a) const { return __popc(psi & uint32_t(a)) & 1u; }
-    __device__ __forceinline__ uint32_t q(uint64_t a) const { return __popc(phi & uint32_t(a)) & 1u; }
-};
+    __syncthreads();
+    return L;
+}
 
-template <>
-struct RowView<true> {
-    uint32_t psi_lo, psi_hi, phi_lo, phi_hi, code, pat;
-    __device__ __forceinline__ void load(const DevTable& t, uint64_t row) {
-        const uint4 w = __ldg(t.rows + row);
-        const uint2 x = __ldg(t.aux + row);
-        psi_lo = w.x; psi_hi = w.y; phi_lo = w.z; phi_hi = w.w; code = x.x; pat = x.y;
-    }
-    __device__ __forceinline__ uint32_t p(uint64_t a) const {
-        return __popc((psi_lo & uint32_t(a)) ^ (psi_hi & uint32_t(a >> 32))) & 1u;
-    }
-    __device__ __forceinline__ uint32_t q(uint64_t a) const {
-        return __popc((phi_lo & uint32_t(a)) ^ (phi_hi & uint32_t(a >> 32))) & 1u;
-    }
-};
-
-// ---------------------------------------------------------------------------
-// General kernel: K assignments per thread, any assignment words.
-template <bool P64, int K>
-__global__ void __launch_bounds__(kThreads) k_eval_general(const DevTable t, const LaunchReq r) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLut L = stage_lut(t, smem);
-    uint64_t tb, te;
-    term_range(t, r, tb, te);
-
-    const uint64_t idx0 = uint64_t(blockIdx.x) * (kThreads * K) + threadIdx.x;
+// ------------------------------------------------------- general kernel ----
+template <bool P64, int K, bool LONG>
+struct GeneralCons {
+    const SmemLut& L;
     uint64_t a[K];
+    uint32_t acc[K];
+    Wide w[LONG ? K : 1];
     double2 amp[K];
+    __device__ __forceinline__ explicit GeneralCons(const SmemLut& l) : L(l) {}
+    __device__ __forceinline__ void row(const Row<P64>& v) {
+        const uint32_t cb = L.codes_s + (v.code & kCodeMask);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] += lds_u32(cb | (v.p(a[k]) << 2) | (v.q(a[k]) << 3));
+    }
+    __device__ __forceinline__ void flush() {
+        if constexpr (LONG) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) { widen(w[k], acc[k]); acc[k] = 0; }
+        }
+    }
+    __device__ __forceinline__ void end_term(const double2 C) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if constexpr (LONG) {
+                widen(w[k], acc[k]);
+                term_epilogue(w[k].j, w[k].z, w[k].s1, w[k].a, w[k].b, C, L, amp[k]);
+                w[k] = Wide{0, 0, 0, 0, 0};
+            } else {
+                epilogue_packed(acc[k], C, L, amp[k]);
+            }
+            acc[k] = 0;
+        }
+    }
+};
+
+template <bool P64, int K, bool LONG>
+__global__ void __launch_bounds__(kThreads) k_eval_general(const DevTable t, const LaunchReq r) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLut L = kernel_prologue(t, smem, smem_lut_offset<P64>());
+    uint64_t tb, te;
+    term_range(r, tb, te);
+    GeneralCons<P64, K, LONG> c(L);
+    const uint64_t idx0 = uint64_t(blockIdx.x) * (kThreads * K) + threadIdx.x;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const uint64_t idx = idx0 + uint64_t(k) * kThreads;
-        a[k] = idx < r.n ? (r.d_asg ? r.d_asg[idx] : r.first + idx) : 0;
-        amp[k] = make_double2(0.0, 0.0);
+        c.a[k] = idx < r.n ? (r.d_asg ? r.d_asg[idx] : r.first + idx) : 0;
+        c.acc[k] = 0;
+        c.amp[k] = make_double2(0.0, 0.0);
+        if constexpr (LONG) c.w[k] = Wide{0, 0, 0, 0, 0};
     }
+    if (tb < te) stream_rows<P64, LONG>(t, tb, te, smem, c);
+#pragma unroll
+    for (int k = 0; k < K; ++k) store_result(r, idx0 + uint64_t(k) * kThreads, c.amp[k]);
+}
 
-    for (uint64_t term = tb; term < te; ++term) {
-        const uint64_t r0 = t.term_row[term], r1 = t.term_row[term + 1];
-        const double2 C = __ldg(t.term_c + term);
-        if (r1 - r0 <= uint64_t(kSegRows)) {
-            uint32_t acc[K];
+// ---------------------------------------------------------- gray kernel ----
+// parity(m & (base | g)) = parity(m & base) ^ parity(m_low & g); the second
+// term, for all g at once, is the row's Walsh pattern.
+template <bool P64, int GB, bool LONG>
+struct GrayCons {
+    static constexpr int G = 1 << GB;
+    const SmemLut& L;
+    uint64_t base;
+    uint32_t acc[G];
+    Wide w[LONG ? G : 1];
+    double2 amp[G];
+    __device__ __forceinline__ explicit GrayCons(const SmemLut& l) : L(l) {}
+    __device__ __forceinline__ void row(const Row<P64>& v) {
+        const uint32_t xi = v.pat ^ (0x55555555u * v.p(base)) ^ (0xAAAAAAAAu * v.q(base));
+        // shared address of the row's class (16-aligned) OR the variant's byte
+        // offset (idx * 4): one shift + one LOP3 + one LDS + one IADD per row-eval
+        const uint32_t cb = L.codes_s + (v.code & kCodeMask);
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = 0;
-#pragma unroll 2
-            for (uint64_t row = r0; row < r1; ++row) {
-                RowView<P64> v;
-                v.load(t, row);
-                const uint32_t* cl = L.codes + (v.code >> 2);
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] += cl[v.p(a[k]) | (v.q(a[k]) << 1)];
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) epilogue_packed(acc[k], C, L, amp[k]);
-        } else {
-            Wide w[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) w[k] = Wide{0, 0, 0, 0, 0};
-            for (uint64_t s0 = r0; s0 < r1; s0 += kSegRows) {
-                const uint64_t s1 = s0 + kSegRows < r1 ? s0 + kSegRows : r1;
-                uint32_t acc[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] = 0;
-                for (uint64_t row = s0; row < s1; ++row) {
-                    RowView<P64> v;
-                    v.load(t, row);
-                    const uint32_t* cl = L.codes + (v.code >> 2);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) acc[k] += cl[v.p(a[k]) | (v.q(a[k]) << 1)];
-                }
-#pragma unroll
-                for (int k = 0; k < K; ++k) widen(w[k], acc[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-                term_epilogue(w[k].j, w[k].z, w[k].s1, w[k].a, w[k].b, C, L, amp[k]);
+        for (int g = 0; g < G; ++g) {
+            const uint32_t sh = g == 0 ? (xi << 2) : (xi >> (2 * g - 2));
+            acc[g] += lds_u32(cb | (sh & 0xCu));
         }
     }
+    __device__ __forceinline__ void flush() {
+        if constexpr (LONG) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) store_result(r, idx0 + uint64_t(k) * kThreads, amp[k]);
-}
+            for (int g = 0; g < G; ++g) { widen(w[g], acc[g]); acc[g] = 0; }
+        }
+    }
+    __device__ __forceinline__ void end_term(const double2 C) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if constexpr (LONG) {
+                widen(w[g], acc[g]);
+                term_epilogue(w[g].j, w[g].z, w[g].s1, w[g].a, w[g].b, C, L, amp[g]);
+                w[g] = Wide{0, 0, 0, 0, 0};
+            } else {
+                epilogue_packed(acc[g], C, L, amp[g]);
+            }
+            acc[g] = 0;
+        }
+    }
+};
 
-// ---------------------------------------------------------------------------
-// Enumerated kernel: thread owns kGray assignments base + g (base % kGray == 0).
-// parity(m & (base | g)) = parity(m & base) ^ parity(m_low & g); the second
-// term, for all g at once, is the row's Walsh pattern (host-precomputed).
-template <bool P64>
-__device__ __forceinline__ uint32_t flips(const RowView<P64>& v, uint64_t base) {
-    const uint32_t p = v.p(base), q = v.q(base);
-    return (0x55555555u * p) ^ (0xAAAAAAAAu * q);
-}
-
-template <bool P64>
+template <bool P64, int GB, bool LONG>
 __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const LaunchReq r) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLut L = stage_lut(t, smem);
+    constexpr int G = 1 << GB;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLut L = kernel_prologue(t, smem, smem_lut_offset<P64>());
     uint64_t tb, te;
-    term_range(t, r, tb, te);
-
-    const uint64_t off = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) * kGray;
+    term_range(r, tb, te);
+    GrayCons<P64, GB, LONG> c(L);
+    const uint64_t off = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) * G;
     // explicit word lists reach this kernel only when the host verified that
     // they are contiguous and 16-aligned: the thread's first word is its base
-    const uint64_t base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
-    double2 amp[kGray];
+    c.base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
 #pragma unroll
-    for (int g = 0; g < kGray; ++g) amp[g] = make_double2(0.0, 0.0);
-
-    for (uint64_t term = tb; term < te; ++term) {
-        const uint64_t r0 = t.term_row[term], r1 = t.term_row[term + 1];
-        const double2 C = __ldg(t.term_c + term);
-        if (r1 - r0 <= uint64_t(kSegRows)) {
-            uint32_t acc[kGray];
-#pragma unroll
-            for (int g = 0; g < kGray; ++g) acc[g] = 0;
-            for (uint64_t row = r0; row < r1; ++row) {
-                RowView<P64> v;
-                v.load(t, row);
-                const uint32_t xi = v.pat ^ flips(v, base);
-                const uint32_t* cl = L.codes + (v.code >> 2);
-#pragma unroll
-                for (int g = 0; g < kGray; ++g) acc[g] += cl[(xi >> (2 * g)) & 3u];
-            }
-#pragma unroll
-            for (int g = 0; g < kGray; ++g) epilogue_packed(acc[g], C, L, amp[g]);
-        } else {
-            Wide w[kGray];
-#pragma unroll
-            for (int g = 0; g < kGray; ++g) w[g] = Wide{0, 0, 0, 0, 0};
-            for (uint64_t s0 = r0; s0 < r1; s0 += kSegRows) {
-                const uint64_t s1 = s0 + kSegRows < r1 ? s0 + kSegRows : r1;
-                uint32_t acc[kGray];
-#pragma unroll
-                for (int g = 0; g < kGray; ++g) acc[g] = 0;
-                for (uint64_t row = s0; row < s1; ++row) {
-                    RowView<P64> v;
-                    v.load(t, row);
-                    const uint32_t xi = v.pat ^ flips(v, base);
-                    const uint32_t* cl = L.codes + (v.code >> 2);
-#pragma unroll
-                    for (int g = 0; g < kGray; ++g) acc[g] += cl[(xi >> (2 * g)) & 3u];
-                }
-#pragma unroll
-                for (int g = 0; g < kGray; ++g) widen(w[g], acc[g]);
-            }
-#pragma unroll
-            for (int g = 0; g < kGray; ++g)
-                term_epilogue(w[g].j, w[g].z, w[g].s1, w[g].a, w[g].b, C, L, amp[g]);
-        }
+    for (int g = 0; g < G; ++g) {
+        c.acc[g] = 0;
+        c.amp[g] = make_double2(0.0, 0.0);
+        if constexpr (LONG) c.w[g] = Wide{0, 0, 0, 0, 0};
     }
+    if (tb < te) stream_rows<P64, LONG>(t, tb, te, smem, c);
 #pragma unroll
-    for (int g = 0; g < kGray; ++g) store_result(r, off + g, amp[g]);
+    for (int g = 0; g < G; ++g) store_result(r, off + g, c.amp[g]);
 }
 
 // ---------------------------------------------------------------------------
@@ -284,9 +408,13 @@ __global__ void k_reduce_partials(const double2* __restrict__ partial, int n_chu
     double2 s = make_double2(0.0, 0.0);
     for (int c = 0; c < n_chunks; ++c) {
         const double2 v = partial[uint64_t(c) * n + i];
-        s.x += v.x; s.y += v.y;
+        s.x += v.x;
+        s.y += v.y;
     }
-    if (accumulate) { s.x += amp[i].x; s.y += amp[i].y; }
+    if (accumulate) {
+        s.x += amp[i].x;
+        s.y += amp[i].y;
+    }
     if (amp) amp[i] = s;
     if (prob) prob[i] = prob_mode == 2 ? s.x : s.x * s.x + s.y * s.y;
 }
@@ -298,31 +426,37 @@ __global__ void k_amp_to_prob(const double2* __restrict__ amp, uint64_t n, doubl
     prob[i] = mode == 2 ? v.x : v.x * v.x + v.y * v.y;
 }
 
-// E3: phase indices of every (row, assignment), device row order.
-__global__ void k_debug_phase(const DevTable t, const uint64_t* __restrict__ asg, uint64_t n,
-                              uint8_t* out) {
+template <bool P64>
+__device__ __forceinline__ Row<P64> load_row_global(const DevTable& t, uint64_t row) {
+    Row<P64> v;
+    v.load(t.rows + row * Row<P64>::kWords);
+    return v;
+}
+
+// E3: phase indices of every (device row, assignment).
+__global__ void k_debug_phase(const DevTable t, const uint64_t* __restrict__ asg, uint64_t n, uint8_t* out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= t.n_rows * n) return;
     const uint64_t row = i / n, k = i % n;
     const uint64_t a = asg[k];
     uint32_t p, q, code;
     if (t.p64) {
-        RowView<true> v; v.load(t, row);
+        const Row<true> v = load_row_global<true>(t, row);
         p = v.p(a); q = v.q(a); code = v.code;
     } else {
-        RowView<false> v; v.load(t, row);
+        const Row<false> v = load_row_global<false>(t, row);
         p = v.p(a); q = v.q(a); code = v.code;
     }
-    const uint32_t cls = code >> 4, ka = cls >> 3, kb = cls & 7;
+    const uint32_t cls = (code & kCodeMask) >> 4, ka = cls >> 3, kb = cls & 7;
     out[i] = uint8_t((((ka + 4 * p) & 7) << 3) | ((kb + 4 * q) & 7));
 }
 
 // Per (term, assignment) exact product codes, one thread each, wide counters
 // (an independent re-derivation of what the SWAR kernels accumulate).
-__global__ void k_debug_codes(const DevTable t, const uint64_t* __restrict__ asg, uint64_t n,
-                              uint32_t* out5) {
+__global__ void k_debug_codes(const DevTable t, const uint64_t* __restrict__ asg, uint64_t n, uint32_t* out5) {
     extern __shared__ __align__(16) unsigned char smem[];
     const SmemLut L = stage_lut(t, smem);
+    __syncthreads();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= t.n_terms * n) return;
     const uint64_t term = i / n, k = i % n;
@@ -331,23 +465,41 @@ __global__ void k_debug_codes(const DevTable t, const uint64_t* __restrict__ asg
     for (uint64_t row = t.term_row[term]; row < t.term_row[term + 1]; ++row) {
         uint32_t p, q, code;
         if (t.p64) {
-            RowView<true> v; v.load(t, row);
+            const Row<true> v = load_row_global<true>(t, row);
             p = v.p(a); q = v.q(a); code = v.code;
         } else {
-            RowView<false> v; v.load(t, row);
+            const Row<false> v = load_row_global<false>(t, row);
             p = v.p(a); q = v.q(a); code = v.code;
         }
-        widen(w, L.codes[(code >> 2) + (p | (q << 1))]);
+        widen(w, L.codes[((code & kCodeMask) >> 2) + (p | (q << 1))]);
     }
     uint32_t* o = out5 + 5 * i;
     o[0] = w.j & 7u; o[1] = w.z; o[2] = w.s1; o[3] = w.a; o[4] = w.b;
+}
+
+template <class KernelT>
+cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, const DevTable& t,
+                       const LaunchReq& r) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, kThreads, smem, s>>>(t, r);
+    return cudaGetLastError();
+}
+
+template <bool P64, bool LONG>
+cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
+    const size_t sm = smem_lut_offset<P64>() + t.lut_layout.bytes;
+    if (kc == KC_GRAY) return launch_one(k_eval_gray<P64, kGrayBits, LONG>, grid, sm, r.stream, t, r);
+    return launch_one(k_eval_general<P64, kGeneralK, LONG>, grid, sm, r.stream, t, r);
 }
 
 }  // namespace
 
 // ------------------------------------------------------------------ host ----
 
-KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
+KernelChoice choose_kernel(const DevTable&, const LaunchReq& r) {
     if (r.kernel != KC_AUTO) return r.kernel;
     if ((r.d_asg == nullptr || r.words_contiguous) && (r.first % kGray) == 0) return KC_GRAY;
     return KC_GENERAL;
@@ -358,45 +510,32 @@ int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
     return int((r.n + per - 1) / per);
 }
 
-cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice kc,
-                            uint64_t* launches) {
+cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice kc, uint64_t* launches) {
     if (r.n == 0) return cudaSuccess;
     const dim3 grid(grid_assign_blocks(t, r, kc), r.n_chunks);
-    const size_t sm = t.lut_layout.bytes;
-    if (sm > 48 * 1024) {
-        cudaFuncSetAttribute(k_eval_gray<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        cudaFuncSetAttribute(k_eval_gray<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        cudaFuncSetAttribute(k_eval_general<true, kGeneralK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        cudaFuncSetAttribute(k_eval_general<false, kGeneralK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        cudaFuncSetAttribute(k_debug_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    }
-    if (kc == KC_GRAY) {
-        if (t.p64) k_eval_gray<true><<<grid, kThreads, sm, r.stream>>>(t, r);
-        else k_eval_gray<false><<<grid, kThreads, sm, r.stream>>>(t, r);
-    } else {
-        if (t.p64) k_eval_general<true, kGeneralK><<<grid, kThreads, sm, r.stream>>>(t, r);
-        else k_eval_general<false, kGeneralK><<<grid, kThreads, sm, r.stream>>>(t, r);
-    }
+    const bool lng = t.max_rows > uint32_t(kSegRows);
+    cudaError_t e;
+    if (t.p64) e = lng ? launch_typed<true, true>(t, r, kc, grid) : launch_typed<true, false>(t, r, kc, grid);
+    else e = lng ? launch_typed<false, true>(t, r, kc, grid) : launch_typed<false, false>(t, r, kc, grid);
     ++*launches;
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || r.n_chunks <= 1) return e;
     const int tpb = 256;
-    k_reduce_partials<<<int((r.n + tpb - 1) / tpb), tpb, 0, r.stream>>>(
-        r.d_partial, r.n_chunks, r.n, r.d_amp, r.d_prob, r.prob_mode, r.accumulate);
+    k_reduce_partials<<<int((r.n + tpb - 1) / tpb), tpb, 0, r.stream>>>(r.d_partial, r.n_chunks, r.n, r.d_amp,
+                                                                        r.d_prob, r.prob_mode, r.accumulate);
     ++*launches;
     return cudaGetLastError();
 }
 
-cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int mode,
-                               cudaStream_t s, uint64_t* launches) {
+cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int mode, cudaStream_t s,
+                               uint64_t* launches) {
     if (n == 0) return cudaSuccess;
     k_amp_to_prob<<<int((n + 255) / 256), 256, 0, s>>>(amp, n, prob, mode);
     ++*launches;
     return cudaGetLastError();
 }
 
-cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_t n,
-                               uint8_t* d_out, cudaStream_t s, uint64_t* launches) {
+cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_t n, uint8_t* d_out,
+                               cudaStream_t s, uint64_t* launches) {
     const uint64_t total = t.n_rows * n;
     if (total == 0) return cudaSuccess;
     k_debug_phase<<<int((total + 255) / 256), 256, 0, s>>>(t, d_asg, n, d_out);
@@ -404,10 +543,12 @@ cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_
     return cudaGetLastError();
 }
 
-cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_t n,
-                               uint32_t* d_out5, cudaStream_t s, uint64_t* launches) {
+cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_t n, uint32_t* d_out5,
+                               cudaStream_t s, uint64_t* launches) {
     const uint64_t total = t.n_terms * n;
     if (total == 0) return cudaSuccess;
+    if (t.lut_layout.bytes > 48 * 1024)
+        cudaFuncSetAttribute(k_debug_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(t.lut_layout.bytes));
     k_debug_codes<<<int((total + 255) / 256), 256, t.lut_layout.bytes, s>>>(t, d_asg, n, d_out5);
     ++*launches;
     return cudaGetLastError();
