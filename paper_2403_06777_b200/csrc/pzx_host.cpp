@@ -426,14 +426,27 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
-    // grid policy: enough CTAs for >= ~4 per SM; otherwise split the terms
+    // grid policy: split the terms into chunks so that the grid is >= kWaves
+    // full waves of resident CTAs (keeps the last-wave tail small); chunk
+    // partials are bounded to ~1 GiB of scratch
     const int ablocks = grid_assign_blocks(t->dev, r, kc);
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
-    const int target = 4 * ctx->n_sm;
+    constexpr int kWaves = 8;
+    const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc);
+    const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
-        chunks = int(std::min<uint64_t>((target + ablocks - 1) / ablocks, nterms));
-        chunks = std::min(chunks, 65535);
+        uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;
+        c = std::min<uint64_t>(c, nterms);
+        c = std::min<uint64_t>(c, std::max<uint64_t>(1, (uint64_t(1) << 30) / (r.n * 16 + 1)));
+        chunks = int(std::min<uint64_t>(c, 65535));
+        // round the grid up to whole waves when that does not need more chunks than terms
+        const uint64_t total = uint64_t(chunks) * ablocks;
+        if (total % wave) {
+            const uint64_t want = (total / wave + 1) * wave;
+            const uint64_t c2 = (want + ablocks - 1) / ablocks;
+            if (c2 <= nterms && c2 <= 65535 && c2 * (r.n * 16) <= (uint64_t(1) << 30)) chunks = int(c2);
+        }
     }
     r.n_chunks = chunks;
     if (chunks > 1) {

@@ -84,6 +84,7 @@ struct LaunchReq {
 // Grid policy helpers (host)
 int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
+int resident_ctas_per_sm(const DevTable& t, KernelChoice kc);
 
 // Launchers; each returns the CUDA error of the launch and adds the number of
 // kernel launches to *launches.

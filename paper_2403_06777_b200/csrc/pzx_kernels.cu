@@ -109,18 +109,20 @@ __device__ __forceinline__ void term_epilogue(uint32_t jraw, uint32_t z, uint32_
     if (z != 0) return;
     const uint32_t j = (jraw + 6u * s1) & 7u;
     double2 w = L.om[j];
-    double r = L.u[s1];
-    if (a | b) {
-        const uint32_t mn = a < b ? a : b;
-        r *= L.p3[mn];
-        const double2 pd = L.pd[int(a) - int(b)];
-        const double wr = w.x * pd.x - w.y * pd.y;
-        const double wi = w.x * pd.y + w.y * pd.x;
-        w.x = wr;
-        w.y = wi;
+    if (s1 | a | b) {  // non-monomial factors present
+        double r = L.u[s1];
+        if (a | b) {
+            const uint32_t mn = a < b ? a : b;
+            r *= L.p3[mn];
+            const double2 pd = L.pd[int(a) - int(b)];
+            const double wr = w.x * pd.x - w.y * pd.y;
+            const double wi = w.x * pd.y + w.y * pd.x;
+            w.x = wr;
+            w.y = wi;
+        }
+        w.x *= r;
+        w.y *= r;
     }
-    w.x *= r;
-    w.y *= r;
     amp.x += C.x * w.x - C.y * w.y;
     amp.y += C.x * w.y + C.y * w.x;
 }
@@ -351,7 +353,9 @@ struct GrayCons {
         const uint32_t cb = L.codes_s + (v.code & kCodeMask);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            const uint32_t sh = g == 0 ? (xi << 2) : (xi >> (2 * g - 2));
+            // xi >> (2g - 2) as a multiply-high: keeps the shift on the FMA pipe
+            // (IMAD.HI) so the ALU pipe only carries the LOP3 and half the adds
+            const uint32_t sh = g == 0 ? (xi << 2) : g == 1 ? xi : __umulhi(xi, 1u << (34 - 2 * g));
             acc[g] += lds_u32(cb | (sh & 0xCu));
         }
     }
@@ -508,6 +512,23 @@ KernelChoice choose_kernel(const DevTable&, const LaunchReq& r) {
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
     const uint64_t per = kc == KC_GRAY ? uint64_t(kThreads) * kGray : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
+}
+
+int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
+    const bool lng = t.max_rows > uint32_t(kSegRows);
+    int nb = 0;
+    size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
+    cudaError_t e;
+#define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
+    if (kc == KC_GRAY) {
+        if (t.p64) { if (lng) PZX_OCC((k_eval_gray<true, kGrayBits, true>)); else PZX_OCC((k_eval_gray<true, kGrayBits, false>)); }
+        else { if (lng) PZX_OCC((k_eval_gray<false, kGrayBits, true>)); else PZX_OCC((k_eval_gray<false, kGrayBits, false>)); }
+    } else {
+        if (t.p64) { if (lng) PZX_OCC((k_eval_general<true, kGeneralK, true>)); else PZX_OCC((k_eval_general<true, kGeneralK, false>)); }
+        else { if (lng) PZX_OCC((k_eval_general<false, kGeneralK, true>)); else PZX_OCC((k_eval_general<false, kGeneralK, false>)); }
+    }
+#undef PZX_OCC
+    return (e == cudaSuccess && nb > 0) ? nb : 1;
 }
 
 cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice kc, uint64_t* launches) {
