@@ -71,7 +71,8 @@ enum {
     PZX_PROB_ABS2 = 1u << 0,  /* prob[i] = |amp_i|^2 (Born rule)            */
     PZX_PROB_REAL = 1u << 1,  /* prob[i] = Re(amp_i) (doubled diagram)      */
     PZX_KERNEL_GENERAL = 1u << 8, /* force the per-assignment POPC kernel          */
-    PZX_KERNEL_GRAY = 1u << 9     /* force the enumerated (low-bit Walsh) kernel   */
+    PZX_KERNEL_GRAY = 1u << 9,    /* force the enumerated (low-bit Walsh) kernel   */
+    PZX_KERNEL_SLICE = 1u << 10   /* force the bit-sliced enumerated kernel        */
 };
 
 typedef struct pzx_ctx pzx_ctx;
@@ -139,6 +140,11 @@ pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out);
 /* Host-only: the per-class variant codes [64 classes][4 variants], sqrt2
  * exponent e[64] and lambda/mu flag lm[64] the kernels use. */
 pzx_status pzx_class_table(uint32_t codes[256], int32_t e[64], int32_t lm[64]);
+/* Host-only: the bit-sliced kernel's 129 row ops (class * 2 + single, 128 =
+ * unit row): per op {jbase, w'[4], zero_tt, lambda_tt, pi_tt, pi'_tt, lm}
+ * (pzx_classes.h); returns PZX_E_DOMAIN if it disagrees with the generated
+ * PTX tables (pzx_slice_dispatch.inc). */
+pzx_status pzx_slice_op_table(int32_t out[129 * 10]);
 /* shape: n_params, n_terms, n_rows (genuine rows), max rows in one term */
 pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_terms,
                            uint64_t* n_rows, uint32_t* max_term_rows);

@@ -18,6 +18,7 @@ EXPORTS = (
     "pzx_table_shape", "pzx_table_term_info", "pzx_evaluate", "pzx_evaluate_range",
     "pzx_evaluate_device", "pzx_amp_to_prob_device", "pzx_synchronize",
     "pzx_debug_phase_indices", "pzx_debug_term_codes", "pzx_table_compile_host", "pzx_class_table",
+    "pzx_slice_op_table",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -86,6 +87,7 @@ def lib() -> C.CDLL:
     L.pzx_debug_term_codes.argtypes = [vp, vp, u64p, C.c_uint64, C.POINTER(TermCode)]
     L.pzx_table_compile_host.argtypes = [C.POINTER(ExprView), C.POINTER(vp)]
     L.pzx_class_table.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.pzx_slice_op_table.argtypes = [C.POINTER(C.c_int32)]
     _lib = L
     return L
 

@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES_CU = ["pzx_kernels.cu"]
 SOURCES_CPP = ["pzx_host.cpp"]
-HEADERS = ["pzx_internal.h", "pzx_math.hpp"]
+HEADERS = ["pzx_internal.h", "pzx_math.hpp", "pzx_classes.h", "pzx_slice_dispatch.inc"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -40,6 +40,8 @@ def _stale(out: str, deps: list[str]) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    from . import gen_slice_ops  # regenerate the bit-sliced PTX dispatch if its generator changed
+    gen_slice_ops.main()
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INC, "pzx_gpu.h")]
     objs = []
     for src in SOURCES_CU:
@@ -62,4 +64,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    sys.path.insert(0, ROOT)
+    from paper_2403_06777_b200 import build as _b
+    print(_b.build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -20,7 +20,9 @@
 #include <vector>
 
 #include "pzx_gpu.h"
+#include "pzx_classes.h"
 #include "pzx_internal.h"
+#include "pzx_slice_dispatch.inc"
 #include "pzx_math.hpp"
 
 using namespace pzxb;
@@ -66,6 +68,23 @@ struct Classes {
             }
     }
 };
+
+// slice-op tables as the generated PTX sees them (pzx_slice_dispatch.inc)
+const int kSliceJbase[kSliceOps] = PZX_SLICE_JBASE;
+const int kSliceKindFlags[kSliceOps] = PZX_SLICE_KIND_FLAGS;
+
+bool slice_tables_ok() {
+    static const bool ok = [] {
+        for (int op = 0; op < kSliceOps; ++op) {
+            const SliceOp so = slice_op(op);
+            const int flags = (so.lam_tt ? int(kSliceLamFlag) : 0) | (so.pi_tt ? int(kSlicePiFlag) : 0) |
+                              (so.pip_tt ? int(kSlicePipFlag) : 0);
+            if (so.jbase != kSliceJbase[op] || flags != kSliceKindFlags[op]) return false;
+        }
+        return true;
+    }();
+    return ok;
+}
 
 const Classes& classes() {
     static const Classes k;
@@ -134,6 +153,9 @@ struct HostTable {
     std::vector<uint4> rows;                // P <= 32: {psi, phi, code, pat}; P > 32: 2 records per row
     std::vector<uint8_t> swapped;           // row stored with psi/phi exchanged
     std::vector<uint8_t> unit;              // placeholder row of a row-less term
+    std::vector<uint4> srows;               // bit-sliced kernel rows (2 per row)
+    std::vector<double> sterm_c;            // its term constants (2 per term)
+    int jb_term = 0;                        // running sum of slice jbase in the open term
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
     uint32_t max_rows = 0;
@@ -148,8 +170,19 @@ uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
     return pat;
 }
 
+uint32_t walsh32(uint64_t m) {
+    uint32_t w = 0;
+    for (int g = 0; g < 32; ++g) w |= uint32_t(__builtin_parityll(m & uint64_t(g))) << g;
+    return w;
+}
+
 void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, uint32_t pat, uint8_t sw,
                      uint8_t unit) {
+    const uint32_t cls = (code & kCodeMask) >> 4;
+    const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
+    h.jb_term += kSliceJbase[op];
+    h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), op | uint32_t(kSliceKindFlags[op]), walsh32(psi)));
+    h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
     if (h.n_params <= 32) {
         h.rows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, pat));
     } else {  // 32-byte record: masks, then {code, pattern}
@@ -190,6 +223,7 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
     for (uint64_t i = 0; i + 1 < n_rows_term; ++i)
         if ((i + 1) % kSegRows == 0) code_word(h, row0 + i) |= kSegFlag;
     code_word(h, row0 + n_rows_term - 1) |= kEndFlag;
+    h.srows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
     h.max_rows = std::max<uint32_t>(h.max_rows, uint32_t(n_rows_term));
     h.coef.push_back(c);
     h.e_t.push_back(e);
@@ -203,6 +237,11 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
     for (int i = 0; i < lm; ++i) v = cmul(v, mu);
     h.term_c.push_back(double(v.re));
     h.term_c.push_back(double(v.im));
+    const C128 wj = zw_to_c128(zw_pow_w(h.jb_term & 7));  // slice kernel: w^(sum of row jbase)
+    const C128 vs = cmul(v, wj);
+    h.sterm_c.push_back(double(vs.re));
+    h.sterm_c.push_back(double(vs.im));
+    h.jb_term = 0;
     h.term_row.push_back(h.n_dev_rows());
     return PZX_OK;
 }
@@ -340,6 +379,8 @@ struct pzx_table {
     void* d_term_row = nullptr;
     void* d_term_c = nullptr;
     void* d_lut = nullptr;
+    void* d_srows = nullptr;
+    void* d_sterm_c = nullptr;
 };
 
 namespace {
@@ -381,6 +422,11 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     if ((st = cuda_err(ctx, upload_vec(&t->d_rows, h.rows), "upload rows"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_row, h.term_row), "upload term offsets"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_c, h.term_c), "upload term constants"))) return st;
+    const bool slice_ok = h.max_rows <= uint32_t(kSegRows) && slice_tables_ok();
+    if (slice_ok) {
+        if ((st = cuda_err(ctx, upload_vec(&t->d_srows, h.srows), "upload slice rows"))) return st;
+        if ((st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
+    }
     LutLayout L;
     std::vector<unsigned char> blob = build_lut(h.max_rows, L);
     if ((st = cuda_err(ctx, upload_vec(&t->d_lut, blob), "upload lut"))) return st;
@@ -395,6 +441,9 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     d.n_params = h.n_params;
     d.max_rows = h.max_rows;
     d.p64 = h.n_params > 32;
+    d.slice_ok = slice_ok ? 1 : 0;
+    d.srows = static_cast<const uint4*>(t->d_srows);
+    d.sterm_c = static_cast<const double2*>(t->d_sterm_c);
     t->ctx = ctx;
     t->device = ctx->device;
     *out = t.release();
@@ -420,9 +469,14 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     if (t->device != ctx->device) return set_err(ctx, PZX_E_INVALID, "table belongs to another device");
     if (r.term_end > t->dev.n_terms) r.term_end = t->dev.n_terms;
     if (r.term_begin > r.term_end) return set_err(ctx, PZX_E_INVALID, "bad term range");
-    r.kernel = (flags & PZX_KERNEL_GENERAL) ? KC_GENERAL : (flags & PZX_KERNEL_GRAY) ? KC_GRAY : KC_AUTO;
-    if (r.kernel == KC_GRAY && ((r.d_asg && !r.words_contiguous) || r.first % kGray))
-        return set_err(ctx, PZX_E_INVALID, "enumerated kernel needs a device-generated batch starting at a multiple of 16");
+    r.kernel = (flags & PZX_KERNEL_GENERAL) ? KC_GENERAL
+             : (flags & PZX_KERNEL_GRAY)    ? KC_GRAY
+             : (flags & PZX_KERNEL_SLICE)   ? KC_SLICE
+                                            : KC_AUTO;
+    if (r.kernel != KC_AUTO && !kernel_supported(t->dev, r, r.kernel))
+        return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "
+                                           "(enumerated kernels need a contiguous batch starting at a multiple "
+                                           "of 16 (gray) or 32 (slice); slice needs terms of <= 127 rows)");
     const KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
@@ -560,6 +614,18 @@ pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out) {
     return PZX_OK;
 }
 
+pzx_status pzx_slice_op_table(int32_t out[129 * 10]) {
+    if (!out) return PZX_E_INVALID;
+    for (int op = 0; op < kSliceOps; ++op) {
+        const SliceOp so = slice_op(op);
+        int32_t* o = out + op * 10;
+        o[0] = so.jbase;
+        for (int v = 0; v < 4; ++v) o[1 + v] = so.w[v];
+        o[5] = so.zero_tt; o[6] = so.lam_tt; o[7] = so.pi_tt; o[8] = so.pip_tt; o[9] = so.lm;
+    }
+    return slice_tables_ok() ? PZX_OK : PZX_E_DOMAIN;
+}
+
 pzx_status pzx_class_table(uint32_t codes[256], int32_t e[64], int32_t lm[64]) {
     const Classes& k = classes();
     if (!k.ok) return PZX_E_DOMAIN;
@@ -576,7 +642,7 @@ void pzx_table_free(pzx_table* t) {
     if (!t) return;
     if (t->device < 0) { delete t; return; }
     cudaSetDevice(t->device);
-    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut})
+    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c})
         if (p) cudaFree(p);
     delete t;
 }
@@ -620,7 +686,7 @@ static pzx_status eval_host(pzx_ctx* ctx, const pzx_table* t, const uint64_t* as
         r.d_asg = static_cast<const uint64_t*>(ctx->d_asg);
         // a contiguous, 16-aligned word list (a sweep over output bitstrings)
         // can use the enumerated kernel; the kernel still reads its base words
-        bool contig = n >= uint64_t(kGray) && asg[0] % kGray == 0;
+        bool contig = n >= uint64_t(kGray);
         for (uint64_t i = 1; contig && i < n; ++i) contig = asg[i] == asg[0] + i;
         if (contig) { r.words_contiguous = 1; r.first = asg[0]; }
     }

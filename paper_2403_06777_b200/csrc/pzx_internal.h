@@ -60,9 +60,15 @@ struct DevTable {
     uint64_t n_terms = 0, n_rows = 0;
     uint32_t n_params = 0, max_rows = 0;
     int p64 = 0;
+    // bit-sliced kernel (only when every term has <= kSegRows rows):
+    // rows as 2 x uint4 {psi, phi, op | kEndFlag, Walsh32(psi)}, {Walsh32(phi), psi_hi, phi_hi, 0}
+    // (op = class * 2 + single, pzx_classes.h), constants C''_t * w^(sum of row jbase)
+    const uint4* srows = nullptr;
+    const double2* sterm_c = nullptr;
+    int slice_ok = 0;
 };
 
-enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2 };
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3 };
 
 struct LaunchReq {
     const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1
@@ -73,7 +79,7 @@ struct LaunchReq {
     int prob_mode = 0;                // 0 none, 1 |amp|^2, 2 Re(amp)
     int accumulate = 0;               // add into d_amp instead of overwriting
     KernelChoice kernel = KC_AUTO;
-    int words_contiguous = 0;         // host verified d_asg[i] == first + i, first % kGray == 0
+    int words_contiguous = 0;         // host verified d_asg[i] == first + i (i < n)
     cudaStream_t stream = 0;
     // scratch owned by the context
     double2* d_partial = nullptr;     // [n_chunks][n] when n_chunks > 1
@@ -85,6 +91,7 @@ struct LaunchReq {
 int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
 int resident_ctas_per_sm(const DevTable& t, KernelChoice kc);
+bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 
 // Launchers; each returns the CUDA error of the launch and adds the number of
 // kernel launches to *launches.

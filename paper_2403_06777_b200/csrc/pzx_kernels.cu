@@ -25,7 +25,9 @@
 //                                  host-precomputed Walsh pattern.
 #include <cuda_runtime.h>
 
+#include "pzx_classes.h"
 #include "pzx_internal.h"
+#include "pzx_slice_dispatch.inc"
 
 namespace pzxb {
 
@@ -178,9 +180,13 @@ struct Row<true> {
     }
 };
 
+template <int RW>
+__host__ __device__ constexpr uint32_t tile_bytes_w() {
+    return uint32_t(kTileRows) * RW * 16u;
+}
 template <bool P64>
 __host__ __device__ constexpr uint32_t tile_bytes() {
-    return uint32_t(kTileRows) * Row<P64>::kWords * 16u;
+    return tile_bytes_w<Row<P64>::kWords>();
 }
 
 // Shared memory: [tile 0][tile 1][2 mbarriers][LUT]
@@ -192,12 +198,12 @@ __host__ __device__ constexpr uint32_t smem_lut_offset() {
 // Walk the flat row stream of terms [tb, te) -- staged by TMA bulk copies --
 // calling cons.row(row) per row, cons.end_term(C) at term ends and
 // cons.flush() at 7-bit-field flush points (long terms only).
-template <bool P64, bool LONG, class Cons>
-__device__ __forceinline__ void stream_rows(const DevTable& t, uint64_t tb, uint64_t te, unsigned char* smem,
-                                            Cons& cons) {
-    constexpr int RW = Row<P64>::kWords;
+template <class RowT, bool LONG, class Cons>
+__device__ __forceinline__ void stream_rows(const DevTable& t, const uint4* rows, const double2* term_c,
+                                            uint64_t tb, uint64_t te, unsigned char* smem, Cons& cons) {
+    constexpr int RW = RowT::kWords;
     uint4* tiles = reinterpret_cast<uint4*>(smem);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * tile_bytes<P64>());
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * tile_bytes_w<RW>());
     const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
     const uint32_t ntiles = uint32_t((R1 - R0 + kTileRows - 1) / kTileRows);
     auto issue = [&](uint32_t tile) {
@@ -206,29 +212,29 @@ __device__ __forceinline__ void stream_rows(const DevTable& t, uint64_t tb, uint
         const uint32_t bytes = uint32_t(n) * RW * 16u;
         uint64_t* bar = &bars[tile & 1];
         mbar_expect_tx(bar, bytes);
-        tma_load_1d(tiles + (tile & 1) * kTileRows * RW, t.rows + r * RW, bytes, bar);
+        tma_load_1d(tiles + (tile & 1) * kTileRows * RW, rows + r * RW, bytes, bar);
     };
     if (threadIdx.x == 0) {
         if (ntiles > 0) issue(0);
         if (ntiles > 1) issue(1);
     }
     uint64_t term = tb;
-    double2 C = __ldg(t.term_c + tb);
-    double2 Cn = (tb + 1 < te) ? __ldg(t.term_c + tb + 1) : make_double2(0.0, 0.0);
+    double2 C = __ldg(term_c + tb);
+    double2 Cn = (tb + 1 < te) ? __ldg(term_c + tb + 1) : make_double2(0.0, 0.0);
     for (uint32_t i = 0; i < ntiles; ++i) {
         const uint4* buf = tiles + (i & 1) * kTileRows * RW;
         mbar_wait(&bars[i & 1], (i >> 1) & 1u);
         const uint64_t rem = R1 - R0 - uint64_t(i) * kTileRows;
         const uint32_t n = rem < uint64_t(kTileRows) ? uint32_t(rem) : uint32_t(kTileRows);
         for (uint32_t k = 0; k < n; ++k) {
-            Row<P64> row;
+            RowT row;
             row.load(buf + k * RW);
             cons.row(row);
             if (row.code & kEndFlag) {
                 cons.end_term(C);
                 C = Cn;
                 ++term;
-                Cn = (term + 1 < te) ? __ldg(t.term_c + term + 1) : make_double2(0.0, 0.0);
+                Cn = (term + 1 < te) ? __ldg(term_c + term + 1) : make_double2(0.0, 0.0);
             } else if (LONG && (row.code & kSegFlag)) {
                 cons.flush();
             }
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_general(const DevTable t, con
         c.amp[k] = make_double2(0.0, 0.0);
         if constexpr (LONG) c.w[k] = Wide{0, 0, 0, 0, 0};
     }
-    if (tb < te) stream_rows<P64, LONG>(t, tb, te, smem, c);
+    if (tb < te) stream_rows<Row<P64>, LONG>(t, t.rows, t.term_c, tb, te, smem, c);
 #pragma unroll
     for (int k = 0; k < K; ++k) store_result(r, idx0 + uint64_t(k) * kThreads, c.amp[k]);
 }
@@ -398,9 +404,174 @@ __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const 
         c.amp[g] = make_double2(0.0, 0.0);
         if constexpr (LONG) c.w[g] = Wide{0, 0, 0, 0, 0};
     }
-    if (tb < te) stream_rows<P64, LONG>(t, tb, te, smem, c);
+    if (tb < te) stream_rows<Row<P64>, LONG>(t, t.rows, t.term_c, tb, te, smem, c);
 #pragma unroll
     for (int g = 0; g < G; ++g) store_result(r, off + g, c.amp[g]);
+}
+
+// --------------------------------------------------------- slice kernel ----
+// Bit-sliced evaluation of enumerated / contiguous batches:
+// a thread owns 32 assignments base + g; each 32-bit register holds one bit
+// of a per-assignment quantity for all 32 of them. Per row:
+//   X = Walsh32(psi) ^ -(parity(psi & base)),  Y likewise   (bit g = p_g, q_g)
+// then a class-specialised LOP3 chain (truth tables are compile-time
+// constants of the row's class, see pzx_classes.h) adds the row's phase
+// exponent w'(p,q) into the mod-8 counter (J2 J1 J0), ORs zero indicators
+// into Z, and bumps bit-sliced lambda / pi / pi' counters. One warp-uniform
+// indirect branch per row selects the chain.
+
+constexpr int kSliceThreads = 128;
+constexpr int kSliceBits = 5;
+constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread
+constexpr int kPlanes = 7;                // counters up to 127 (terms <= kSegRows rows)
+
+struct RowS {
+    uint32_t psi, phi, code, wpsi, wphi, psi_hi, phi_hi;
+    static constexpr int kWords = 2;
+    __device__ __forceinline__ void load(const uint4* p) {
+        const uint4 a = p[0];
+        const uint4 b = p[1];
+        psi = a.x; phi = a.y; code = a.z; wpsi = a.w;
+        wphi = b.x; psi_hi = b.y; phi_hi = b.z;
+    }
+};
+
+struct SliceState {
+    uint32_t J0, J1, J2, Z;
+    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
+    uint32_t nS, nA, nB;  // rows so far that can bump each counter (warp-uniform)
+};
+
+__device__ __forceinline__ void slice_inc(uint32_t (&P)[kPlanes], uint32_t& n, uint32_t v) {
+    ++n;
+    uint32_t t = v;
+#pragma unroll
+    for (int i = 0; i < kPlanes; ++i) {
+        if ((n >> i) == 0) break;  // warp-uniform: plane i needed only once n >= 2^i
+        const uint32_t u = P[i] & t;
+        P[i] ^= t;
+        t = u;
+    }
+}
+
+__device__ __forceinline__ uint32_t slice_decode(const uint32_t (&P)[kPlanes], uint32_t n, int g) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < kPlanes; ++i) {
+        if ((n >> i) == 0) break;
+        x |= ((P[i] >> g) & 1u) << i;
+    }
+    return x;
+}
+
+template <bool P64>
+struct SliceCons {
+    const SmemLut& L;
+    uint64_t base;
+    SliceState s;
+    double2* amp_s;  // [kSliceG][kSliceThreads]
+    double2* crot;   // per-warp [8]
+    __device__ __forceinline__ explicit SliceCons(const SmemLut& l) : L(l) {}
+
+    __device__ __forceinline__ void reset() {
+        s.J0 = s.J1 = s.J2 = s.Z = 0;
+#pragma unroll
+        for (int i = 0; i < kPlanes; ++i) s.S[i] = s.A[i] = s.B[i] = 0;
+        s.nS = s.nA = s.nB = 0;
+    }
+    __device__ __forceinline__ uint32_t parity(uint32_t lo, uint32_t hi) const {
+        if constexpr (P64) return __popc((lo & uint32_t(base)) ^ (hi & uint32_t(base >> 32))) & 1u;
+        else return __popc(lo & uint32_t(base)) & 1u;
+    }
+    __device__ __forceinline__ void row(const RowS& v) {
+        const uint32_t X = v.wpsi ^ (0u - parity(v.psi, v.psi_hi));
+        const uint32_t Y = v.wphi ^ (0u - parity(v.phi, v.phi_hi));
+        uint32_t vl = 0, vpi = 0, vpip = 0;
+        const uint32_t op = v.code & 0xFFu;
+        // generated LOP3 chains, one jump-table branch (pzx_slice_dispatch.inc)
+        asm(PZX_SLICE_DISPATCH_ASM
+            : "+r"(s.J0), "+r"(s.J1), "+r"(s.J2), "+r"(s.Z), "+r"(vl), "+r"(vpi), "+r"(vpip)
+            : "r"(X), "r"(Y), "r"(op));
+        if (v.code & kSliceLamFlag) slice_inc(s.S, s.nS, vl);
+        if (v.code & kSlicePiFlag) slice_inc(s.A, s.nA, vpi);
+        if (v.code & kSlicePipFlag) slice_inc(s.B, s.nB, vpip);
+    }
+    __device__ __forceinline__ void flush() {}
+    __device__ __forceinline__ void end_term(const double2 C) {
+        const uint32_t lane = threadIdx.x & 31u;
+        __syncwarp();
+        if (lane < 8) {
+            const double2 w = L.om[lane];
+            crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+        }
+        __syncwarp();
+        const bool kinds = (s.nS | s.nA | s.nB) != 0;
+        uint32_t alive = ~s.Z;
+        while (alive) {
+            const int g = __ffs(alive) - 1;
+            alive &= alive - 1;
+            uint32_t j = ((s.J0 >> g) & 1u) | (((s.J1 >> g) & 1u) << 1) | (((s.J2 >> g) & 1u) << 2);
+            double2 v;
+            if (kinds) {
+                const uint32_t s1 = slice_decode(s.S, s.nS, g);
+                const uint32_t a = slice_decode(s.A, s.nA, g);
+                const uint32_t b = slice_decode(s.B, s.nB, g);
+                v = crot[(j + 6u * s1) & 7u];
+                double r = L.u[s1];
+                if (a | b) {
+                    const uint32_t mn = a < b ? a : b;
+                    r *= L.p3[mn];
+                    const double2 pd = L.pd[int(a) - int(b)];
+                    const double vr = v.x * pd.x - v.y * pd.y;
+                    v.y = v.x * pd.y + v.y * pd.x;
+                    v.x = vr;
+                }
+                v.x *= r;
+                v.y *= r;
+            } else {
+                v = crot[j];
+            }
+            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+            double2 o = *ap;
+            o.x += v.x;
+            o.y += v.y;
+            *ap = o;
+        }
+        reset();
+    }
+};
+
+template <bool P64>
+__host__ __device__ constexpr uint32_t slice_lut_offset() {
+    return 2 * tile_bytes_w<RowS::kWords>() + 16;
+}
+
+template <bool P64>
+size_t slice_smem_bytes(const DevTable& t) {
+    const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16;
+}
+
+template <bool P64>
+__global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, const LaunchReq r) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLut L = kernel_prologue(t, smem, slice_lut_offset<P64>());
+    const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
+    double2* crot = amp_s + kSliceG * kSliceThreads + (threadIdx.x >> 5) * 8;
+#pragma unroll
+    for (int g = 0; g < kSliceG; ++g) amp_s[g * kSliceThreads + threadIdx.x] = make_double2(0.0, 0.0);
+    uint64_t tb, te;
+    term_range(r, tb, te);
+    SliceCons<P64> c(L);
+    const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
+    c.base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    c.amp_s = amp_s;
+    c.crot = crot;
+    c.reset();
+    if (tb < te) stream_rows<RowS, false>(t, t.srows, t.sterm_c, tb, te, smem, c);
+#pragma unroll 4
+    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
@@ -494,6 +665,13 @@ cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, con
 
 template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
+    if (kc == KC_SLICE) {
+        const size_t sm = slice_smem_bytes<P64>(t);
+        cudaError_t e = cudaFuncSetAttribute(k_eval_slice<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        k_eval_slice<P64><<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        return cudaGetLastError();
+    }
     const size_t sm = smem_lut_offset<P64>() + t.lut_layout.bytes;
     if (kc == KC_GRAY) return launch_one(k_eval_gray<P64, kGrayBits, LONG>, grid, sm, r.stream, t, r);
     return launch_one(k_eval_general<P64, kGeneralK, LONG>, grid, sm, r.stream, t, r);
@@ -503,16 +681,28 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
 
 // ------------------------------------------------------------------ host ----
 
-KernelChoice choose_kernel(const DevTable&, const LaunchReq& r) {
+KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     if (r.kernel != KC_AUTO) return r.kernel;
-    if ((r.d_asg == nullptr || r.words_contiguous) && (r.first % kGray) == 0) return KC_GRAY;
+    const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
+    if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
+    if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
     return KC_GENERAL;
 }
 
+bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
+    const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
+    if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
+    if (kc == KC_GRAY) return enumerated && (r.first % kGray) == 0;
+    return true;
+}
+
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = kc == KC_GRAY ? uint64_t(kThreads) * kGray : uint64_t(kThreads) * kGeneralK;
+    const uint64_t per = kc == KC_SLICE ? uint64_t(kSliceThreads) * kSliceG
+                       : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
+                                        : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
 }
+
 
 int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
     const bool lng = t.max_rows > uint32_t(kSegRows);
@@ -520,7 +710,17 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
-    if (kc == KC_GRAY) {
+    if (kc == KC_SLICE) {
+        if (t.p64) {
+            sm = slice_smem_bytes<true>(t);
+            cudaFuncSetAttribute(k_eval_slice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_slice<true>, kSliceThreads, sm);
+        } else {
+            sm = slice_smem_bytes<false>(t);
+            cudaFuncSetAttribute(k_eval_slice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_slice<false>, kSliceThreads, sm);
+        }
+    } else if (kc == KC_GRAY) {
         if (t.p64) { if (lng) PZX_OCC((k_eval_gray<true, kGrayBits, true>)); else PZX_OCC((k_eval_gray<true, kGrayBits, false>)); }
         else { if (lng) PZX_OCC((k_eval_gray<false, kGrayBits, true>)); else PZX_OCC((k_eval_gray<false, kGrayBits, false>)); }
     } else {

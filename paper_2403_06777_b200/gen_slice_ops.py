@@ -1,0 +1,231 @@
+"""Generate csrc/pzx_slice_dispatch.inc: the bit-sliced kernel's per-row
+update as ONE inline-PTX block with a jump table (brx.idx -> SASS BRX).
+
+Each of the 129 slice ops (op = class * 2 + single, 128 = unit row;
+pzx_classes.h) gets a straight-line LOP3 chain with compile-time truth tables:
+
+  (J2 J1 J0) += w'(X, Y)  mod 8     ripple carry over the three bit planes
+  Z          |= zero(X, Y)           parity-constraint rows
+  vl / vpi / vpip = lambda / pi / pi' indicator vectors (consumed in C++)
+
+X (Y) holds parity(psi & a) (parity(phi & a)) for the thread's 32 assignments.
+The op table is re-derived here by exact Z[w] factorisation; tests compare it
+with the constexpr table the C++ side uses (pzx_slice_op_table).
+"""
+from __future__ import annotations
+
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(HERE, "csrc", "pzx_slice_dispatch.inc")
+
+# ---------------------------------------------------------------- Z[w] ----
+
+
+def wpow(k):
+    k %= 8
+    c = [0, 0, 0, 0]
+    if k < 4:
+        c[k] = 1
+    else:
+        c[k - 4] = -1
+    return tuple(c)
+
+
+def mul(x, y):
+    t = [0] * 8
+    for i in range(4):
+        for j in range(4):
+            t[i + j] += x[i] * y[j]
+    return tuple(t[i] - t[i + 4] for i in range(4))
+
+
+def add(x, y):
+    return tuple(a + b for a, b in zip(x, y))
+
+
+def sigma(x, s):
+    r = (0, 0, 0, 0)
+    for i, c in enumerate(x):
+        r = add(r, tuple(c * v for v in wpow(s * i)))
+    return r
+
+
+def norm(x):
+    return mul(mul(x, sigma(x, 3)), mul(sigma(x, 5), sigma(x, 7)))[0]
+
+
+def div(x, y):
+    co = mul(mul(sigma(y, 3), sigma(y, 5)), sigma(y, 7))
+    n = norm(y)
+    t = mul(x, co)
+    if all(v % n == 0 for v in t):
+        return tuple(v // n for v in t)
+    return None
+
+
+KNONE, KLAMBDA, KMU, KPI, KPIP, KZERO = range(6)
+GEN = {KNONE: (1, 0, 0, 0), KLAMBDA: (1, -1, 0, 0), KMU: (1, 1, 0, 0), KPI: (1, 1, 0, 1), KPIP: (1, -1, 0, -1)}
+SQRT2 = (0, 1, 0, -1)
+
+
+def factor_pair(x, y):
+    v = add(add(add((1, 0, 0, 0), wpow(x)), wpow(y)), tuple(-c for c in wpow(x + y)))
+    if v == (0, 0, 0, 0):
+        return (KZERO, 0, 0)
+    for kind in (KNONE, KLAMBDA, KMU, KPI, KPIP):
+        q = div(v, GEN[kind])
+        if q is None:
+            continue
+        p = (1, 0, 0, 0)
+        for e in range(7):
+            for j in range(8):
+                if mul(p, wpow(j)) == q:
+                    return (kind, j, e)
+            p = mul(p, SQRT2)
+    raise AssertionError((x, y))
+
+
+def slice_op(op):
+    """(jbase, w[4], zero_tt, lam_tt, pi_tt, pip_tt, lm) -- mirrors pzx_classes.h."""
+    if op >= 128:
+        return (0, [0, 0, 0, 0], 0, 0, 0, 0, 0)
+    cls, single = op >> 1, op & 1
+    ka, kb = cls >> 3, cls & 7
+    reach = [True, True, not single, not single]
+    var = [factor_pair(ka + 4 * (v & 1), kb + 4 * (v >> 1)) for v in range(4)]
+    first = next((v for v in range(4) if reach[v] and var[v][0] != KZERO), None)
+    jbase = var[first][1] if first is not None else 0
+    w = [0, 0, 0, 0]
+    z = lam = pi = pip = lm = 0
+    for v in range(4):
+        if not reach[v]:
+            continue
+        k = var[v][0]
+        if k == KZERO:
+            z |= 1 << v
+            continue
+        w[v] = (var[v][1] - jbase) % 8
+        if k == KLAMBDA:
+            lam |= 1 << v
+        if k == KPI:
+            pi |= 1 << v
+        if k == KPIP:
+            pip |= 1 << v
+        if k in (KLAMBDA, KMU):
+            lm = 1
+    return (jbase, w, z, lam, pi, pip, lm)
+
+
+# -------------------------------------------------------- LOP3 immediates ----
+def tt_bit(f, p, q):
+    return (f >> (p | (q << 1))) & 1
+
+
+def imm(fn):
+    """lop3 immLut of fn(a, b, c) with a = 0xF0, b = 0xCC, c = 0xAA."""
+    r = 0
+    for i in range(8):
+        r |= (fn((i >> 2) & 1, (i >> 1) & 1, i & 1) & 1) << i
+    return r
+
+
+def imm_f(f):            # f(b = X, c = Y)
+    return imm(lambda a, b, c: tt_bit(f, b, c))
+
+
+def imm_af(f, op):       # a OP f(b = X, c = Y)
+    ops = {"and": lambda x, y: x & y, "xor": lambda x, y: x ^ y, "or": lambda x, y: x | y}
+    return imm(lambda a, b, c: ops[op](a, tt_bit(f, b, c)))
+
+
+def imm_fxc(f):          # f(a = X, b = Y) ^ c
+    return imm(lambda a, b, c: tt_bit(f, a, b) ^ c)
+
+
+MAJ, XOR3 = 0xE8, 0x96
+
+# operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 Y, %9 op
+
+
+def case_body(op):
+    _, w, z, lam, pi, pip, _ = slice_op(op)
+    t = [sum(((w[v] >> b) & 1) << v for v in range(4)) for b in range(3)]
+    L = []
+    c0 = c1 = False
+    if t[0]:
+        L.append(f"lop3.b32 c0, %0, %7, %8, {imm_af(t[0], 'and'):#04x};")
+        L.append(f"lop3.b32 %0, %0, %7, %8, {imm_af(t[0], 'xor'):#04x};")
+        c0 = True
+    if t[1] and c0:
+        L.append(f"lop3.b32 w1, %7, %7, %8, {imm_f(t[1]):#04x};")
+        L.append(f"lop3.b32 c1, %1, w1, c0, {MAJ:#04x};")
+        L.append(f"lop3.b32 %1, %1, w1, c0, {XOR3:#04x};")
+        c1 = True
+    elif t[1]:
+        L.append(f"lop3.b32 c1, %1, %7, %8, {imm_af(t[1], 'and'):#04x};")
+        L.append(f"lop3.b32 %1, %1, %7, %8, {imm_af(t[1], 'xor'):#04x};")
+        c1 = True
+    elif c0:
+        L.append("and.b32 c1, %1, c0;")
+        L.append("xor.b32 %1, %1, c0;")
+        c1 = True
+    if t[2] and c1:
+        L.append(f"lop3.b32 w1, %7, %8, c1, {imm_fxc(t[2]):#04x};")
+        L.append("xor.b32 %2, %2, w1;")
+    elif t[2]:
+        L.append(f"lop3.b32 %2, %2, %7, %8, {imm_af(t[2], 'xor'):#04x};")
+    elif c1:
+        L.append("xor.b32 %2, %2, c1;")
+    if z:
+        L.append(f"lop3.b32 %3, %3, %7, %8, {imm_af(z, 'or'):#04x};")
+    if lam:
+        L.append(f"lop3.b32 %4, %7, %7, %8, {imm_f(lam):#04x};")
+    if pi:
+        L.append(f"lop3.b32 %5, %7, %7, %8, {imm_f(pi):#04x};")
+    if pip:
+        L.append(f"lop3.b32 %6, %7, %7, %8, {imm_f(pip):#04x};")
+    return L
+
+
+def kind_flags(op):
+    """Row code-word flag bits the C++ side reads: bit 8 lambda, 9 pi, 10 pi'."""
+    _, _, _, lam, pi, pip, _ = slice_op(op)
+    return (1 << 8 if lam else 0) | (1 << 9 if pi else 0) | (1 << 10 if pip else 0)
+
+
+def generate() -> str:
+    n = 129
+    lines = ["// GENERATED by paper_2403_06777_b200/gen_slice_ops.py -- do not edit.",
+             "// Bit-sliced per-row update, one jump-table dispatch (brx.idx) per row.",
+             "// operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 Y, %9 op",
+             "#define PZX_SLICE_DISPATCH_ASM \\"]
+    body = ["{", ".reg .b32 c0, c1, w1;",
+            "ts%=: .branchtargets " + ", ".join(f"L{i}_%=" for i in range(n)) + ";",
+            "brx.idx.uni %9, ts%=;"]
+    for i in range(n):
+        body.append(f"L{i}_%=:")
+        body.extend(case_body(i))
+        body.append("bra.uni D%=;")
+    body.append("D%=:")
+    body.append("}")
+    for b in body:
+        lines.append(f'    "{b}\\n" \\')
+    lines.append("")
+    lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
+    lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
+    lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")
+    return "\n".join(lines) + "\n"
+
+
+def main() -> str:
+    text = generate()
+    old = open(OUT).read() if os.path.exists(OUT) else None
+    if old != text:
+        with open(OUT, "w") as f:
+            f.write(text)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(main())

@@ -296,6 +296,7 @@ PROB_ABS2 = 1
 PROB_REAL = 2
 KERNEL_GENERAL = 1 << 8
 KERNEL_GRAY = 1 << 9
+KERNEL_SLICE = 1 << 10
 
 
 class DeviceTable:
@@ -465,6 +466,13 @@ def class_table():
     return codes.reshape(64, 4), e, lm
 
 
+def slice_op_table() -> np.ndarray:
+    """[129, 10] int32: the bit-sliced kernel's row ops (pzx_slice_op_table)."""
+    out = np.zeros(129 * 10, np.int32)
+    _check(N.lib().pzx_slice_op_table(N.ptr(out, C.c_int32)))
+    return out.reshape(129, 10)
+
+
 def compile_bit_table(expr: ScalarExpression, ctx: Context) -> DeviceTable:
     """SPEC compile_bit_table: normalise, classify, upload."""
     return ctx.compile_bit_table(expr)
@@ -484,6 +492,6 @@ __all__ = [
     "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
-    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY",
+    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "slice_op_table",
 ]
 _ = builtins

@@ -93,10 +93,29 @@ def test_enumerated_range_kernels(ctx, path):
     n = len(z["words"])
     a_gray = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GRAY)
     a_gen = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GENERAL)
+    a_slice = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_SLICE)
     assert_close(a_gray, z["amp"])
     assert_close(a_gen, z["amp"])
+    assert_close(a_slice, z["amp"])
+    # explicit contiguous word list (what pzx_evaluate sees from a user sweep)
+    assert_close(ctx.evaluate_batch(t, np.arange(n, dtype=np.uint64)), z["amp"])
     # unaligned start (general kernel) and ragged length
     assert_close(ctx.evaluate_range(t, 3, n - 7), z["amp"][3:n - 4])
+
+
+@pytest.mark.parametrize("P_", [3, 5, 12, 20, 33, 64])
+def test_slice_kernel_vs_oracle(ctx, P_):
+    """Bit-sliced kernel on enumerated batches, against the reference oracle."""
+    e = synth.generate(P_, 700, 1, 40, 300 + P_)
+    t = ctx.compile_bit_table(e)
+    n = 1 << min(P_, 11)
+    first = 0 if P_ <= 11 else 32 * 12345
+    amp = ctx.evaluate_range(t, first, n, flags=P.KERNEL_SLICE)
+    words = np.arange(first, first + n, dtype=np.uint64)
+    idx = np.random.default_rng(P_).choice(n, min(n, 96), replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+    assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
 
 
 def test_random_assignments_mid_size(ctx):
@@ -192,6 +211,8 @@ def test_full_size_c2_properties(ctx):
     # shard invariance (what the multi-GPU assignment split relies on)
     half = ctx.evaluate_range(t, N // 2, N // 2)
     assert_close(half, amp[N // 2:], 1e-13)
+    # the other enumerated kernels agree (auto picks the bit-sliced one here)
+    assert_close(ctx.evaluate_range(t, 0, N, flags=P.KERNEL_GRAY), amp, 1e-13)
     # general kernel on a random subset of the same words
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(N, 2048, replace=False)).astype(np.uint64)
