@@ -422,32 +422,25 @@ __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const 
 
 constexpr int kSliceThreads = 128;
 constexpr int kSliceBits = 5;
-constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread
-constexpr int kPlanes = 7;                // counters up to 127 (terms <= kSegRows rows)
+constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread, one bit each
+constexpr int kSliceTile = 64;            // rows (32 B each) per TMA-staged tile (3 CTAs/SM fit)
+constexpr int kPlanes = 7;                // bit-sliced counters up to 127 (terms <= kSegRows rows)
 
-struct RowS {
-    uint32_t psi, phi, code, wpsi, wphi, psi_hi, phi_hi;
-    static constexpr int kWords = 2;
-    __device__ __forceinline__ void load(const uint4* p) {
-        const uint4 a = p[0];
-        const uint4 b = p[1];
-        psi = a.x; phi = a.y; code = a.z; wpsi = a.w;
-        wphi = b.x; psi_hi = b.y; phi_hi = b.z;
-    }
-};
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
 
-struct SliceState {
-    uint32_t J0, J1, J2, Z;
-    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
-    uint32_t nS, nA, nB;  // rows so far that can bump each counter (warp-uniform)
-};
-
-__device__ __forceinline__ void slice_inc(uint32_t (&P)[kPlanes], uint32_t& n, uint32_t v) {
-    ++n;
+// bit-sliced counter += v (one bit per assignment); n = rows that could have
+// bumped it so far (warp-uniform), so only planes below bit_length(n) move
+__device__ __forceinline__ void slice_bump(uint32_t (&P)[kPlanes], uint32_t n, uint32_t v) {
     uint32_t t = v;
 #pragma unroll
     for (int i = 0; i < kPlanes; ++i) {
-        if ((n >> i) == 0) break;  // warp-uniform: plane i needed only once n >= 2^i
+        if (i > 0 && (n >> i) == 0) break;
         const uint32_t u = P[i] & t;
         P[i] ^= t;
         t = u;
@@ -455,9 +448,9 @@ __device__ __forceinline__ void slice_inc(uint32_t (&P)[kPlanes], uint32_t& n, u
 }
 
 __device__ __forceinline__ uint32_t slice_decode(const uint32_t (&P)[kPlanes], uint32_t n, int g) {
-    uint32_t x = 0;
+    uint32_t x = (P[0] >> g) & 1u;
 #pragma unroll
-    for (int i = 0; i < kPlanes; ++i) {
+    for (int i = 1; i < kPlanes; ++i) {
         if ((n >> i) == 0) break;
         x |= ((P[i] >> g) & 1u) << i;
     }
@@ -465,85 +458,8 @@ __device__ __forceinline__ uint32_t slice_decode(const uint32_t (&P)[kPlanes], u
 }
 
 template <bool P64>
-struct SliceCons {
-    const SmemLut& L;
-    uint64_t base;
-    SliceState s;
-    double2* amp_s;  // [kSliceG][kSliceThreads]
-    double2* crot;   // per-warp [8]
-    __device__ __forceinline__ explicit SliceCons(const SmemLut& l) : L(l) {}
-
-    __device__ __forceinline__ void reset() {
-        s.J0 = s.J1 = s.J2 = s.Z = 0;
-#pragma unroll
-        for (int i = 0; i < kPlanes; ++i) s.S[i] = s.A[i] = s.B[i] = 0;
-        s.nS = s.nA = s.nB = 0;
-    }
-    __device__ __forceinline__ uint32_t parity(uint32_t lo, uint32_t hi) const {
-        if constexpr (P64) return __popc((lo & uint32_t(base)) ^ (hi & uint32_t(base >> 32))) & 1u;
-        else return __popc(lo & uint32_t(base)) & 1u;
-    }
-    __device__ __forceinline__ void row(const RowS& v) {
-        const uint32_t X = v.wpsi ^ (0u - parity(v.psi, v.psi_hi));
-        const uint32_t Y = v.wphi ^ (0u - parity(v.phi, v.phi_hi));
-        uint32_t vl = 0, vpi = 0, vpip = 0;
-        const uint32_t op = v.code & 0xFFu;
-        // generated LOP3 chains, one jump-table branch (pzx_slice_dispatch.inc)
-        asm(PZX_SLICE_DISPATCH_ASM
-            : "+r"(s.J0), "+r"(s.J1), "+r"(s.J2), "+r"(s.Z), "+r"(vl), "+r"(vpi), "+r"(vpip)
-            : "r"(X), "r"(Y), "r"(op));
-        if (v.code & kSliceLamFlag) slice_inc(s.S, s.nS, vl);
-        if (v.code & kSlicePiFlag) slice_inc(s.A, s.nA, vpi);
-        if (v.code & kSlicePipFlag) slice_inc(s.B, s.nB, vpip);
-    }
-    __device__ __forceinline__ void flush() {}
-    __device__ __forceinline__ void end_term(const double2 C) {
-        const uint32_t lane = threadIdx.x & 31u;
-        __syncwarp();
-        if (lane < 8) {
-            const double2 w = L.om[lane];
-            crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
-        }
-        __syncwarp();
-        const bool kinds = (s.nS | s.nA | s.nB) != 0;
-        uint32_t alive = ~s.Z;
-        while (alive) {
-            const int g = __ffs(alive) - 1;
-            alive &= alive - 1;
-            uint32_t j = ((s.J0 >> g) & 1u) | (((s.J1 >> g) & 1u) << 1) | (((s.J2 >> g) & 1u) << 2);
-            double2 v;
-            if (kinds) {
-                const uint32_t s1 = slice_decode(s.S, s.nS, g);
-                const uint32_t a = slice_decode(s.A, s.nA, g);
-                const uint32_t b = slice_decode(s.B, s.nB, g);
-                v = crot[(j + 6u * s1) & 7u];
-                double r = L.u[s1];
-                if (a | b) {
-                    const uint32_t mn = a < b ? a : b;
-                    r *= L.p3[mn];
-                    const double2 pd = L.pd[int(a) - int(b)];
-                    const double vr = v.x * pd.x - v.y * pd.y;
-                    v.y = v.x * pd.y + v.y * pd.x;
-                    v.x = vr;
-                }
-                v.x *= r;
-                v.y *= r;
-            } else {
-                v = crot[j];
-            }
-            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
-            double2 o = *ap;
-            o.x += v.x;
-            o.y += v.y;
-            *ap = o;
-        }
-        reset();
-    }
-};
-
-template <bool P64>
 __host__ __device__ constexpr uint32_t slice_lut_offset() {
-    return 2 * tile_bytes_w<RowS::kWords>() + 16;
+    return 2 * kSliceTile * 32 + 16;
 }
 
 template <bool P64>
@@ -552,6 +468,17 @@ size_t slice_smem_bytes(const DevTable& t) {
     return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16;
 }
 
+// Bit-sliced evaluation of enumerated / contiguous batches.
+// A thread owns 32 assignments base + g (base % 32 == 0); register bit g of
+// every accumulator belongs to assignment g:
+//   J2 J1 J0 : sum of phase exponents mod 8      Z : some factor was zero
+//   S / A / B: lambda / pi / pi' counts (bit-sliced, 7 planes)
+// Per row: X = Walsh32(psi) ^ -parity(psi & base) in C++, then ONE generated
+// inline-PTX block (pzx_slice_dispatch.inc) jumps (BRX) to the row class's
+// LOP3 chain, which also forms Y for two-parity rows. Per term: the phase
+// table C * w^j (8 entries) is built once per warp, then every live
+// assignment adds C * w^j' * (stuff from S, A, B) into its fp64 accumulator in
+// shared memory.
 template <bool P64>
 __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, const LaunchReq r) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -561,15 +488,131 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
     double2* crot = amp_s + kSliceG * kSliceThreads + (threadIdx.x >> 5) * 8;
 #pragma unroll
     for (int g = 0; g < kSliceG; ++g) amp_s[g * kSliceThreads + threadIdx.x] = make_double2(0.0, 0.0);
+
     uint64_t tb, te;
     term_range(r, tb, te);
-    SliceCons<P64> c(L);
     const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
-    c.base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
-    c.amp_s = amp_s;
-    c.crot = crot;
-    c.reset();
-    if (tb < te) stream_rows<RowS, false>(t, t.srows, t.sterm_c, tb, te, smem, c);
+    const uint64_t base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    const uint32_t blo = uint32_t(base), bhi = uint32_t(base >> 32);
+
+    uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
+    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
+#pragma unroll
+    for (int i = 0; i < kPlanes; ++i) S[i] = A[i] = B[i] = 0;
+    uint32_t nS = 0, nA = 0, nB = 0;
+
+    if (tb < te) {
+        uint4* tiles = reinterpret_cast<uint4*>(smem);
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSliceTile * 32);
+        const uint32_t tiles_s = smem_u32(tiles);
+        const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
+        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        auto issue = [&](uint32_t tile) {
+            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
+            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint32_t bytes = uint32_t(n) * 32u;
+            uint64_t* bar = &bars[tile & 1];
+            mbar_expect_tx(bar, bytes);
+            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.srows + rr * 2, bytes, bar);
+        };
+        if (threadIdx.x == 0) {
+            if (ntiles > 0) issue(0);
+            if (ntiles > 1) issue(1);
+        }
+        uint64_t term = tb;
+        double2 C = __ldg(t.sterm_c + tb);
+        double2 Cn = (tb + 1 < te) ? __ldg(t.sterm_c + tb + 1) : make_double2(0.0, 0.0);
+        for (uint32_t i = 0; i < ntiles; ++i) {
+            mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
+            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
+            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint32_t aend = a0 + n * 32;
+            for (uint32_t ad = a0; ad < aend; ad += 32) {
+                const uint4 ra = lds128(ad);       // psi, phi, code, Walsh32(psi)
+                const uint4 rb = lds128(ad + 16);  // Walsh32(phi), psi_hi, phi_hi, 0
+                uint32_t pp;
+                if constexpr (P64) pp = __popc((ra.x & blo) ^ (rb.y & bhi)) & 1u;
+                else pp = __popc(ra.x & blo) & 1u;
+                const uint32_t X = ra.w ^ (0u - pp);
+                const uint32_t op = ra.z & 0xFFu;
+                uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
+                if constexpr (P64) {
+                    asm(PZX_SLICE_DISPATCH_ASM_P64
+                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                        : "r"(X), "r"(op), "r"(ra.y), "r"(rb.x), "r"(blo), "r"(rb.z), "r"(bhi));
+                } else {
+                    asm(PZX_SLICE_DISPATCH_ASM_P32
+                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                        : "r"(X), "r"(op), "r"(ra.y), "r"(rb.x), "r"(blo));
+                }
+                if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
+                    if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
+                    if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
+                    if (ra.z & kEndFlag) {
+                        // ---- term epilogue -------------------------------------
+                        const uint32_t lane = threadIdx.x & 31u;
+                        __syncwarp();
+                        if (lane < 8) {
+                            const double2 w = L.om[lane];
+                            crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+                        }
+                        __syncwarp();
+                        if (nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
+                            const uint32_t w1 = S[0], w2 = S[0] ^ S[1];
+                            const uint32_t c1 = J1 & w1;
+                            J1 ^= w1;
+                            J2 ^= w2 ^ c1;
+                        }
+                        const bool kinds = (nS | nA | nB) != 0;
+                        uint32_t alive = ~Z;
+                        while (alive) {
+                            const int g = __ffs(alive) - 1;
+                            alive &= alive - 1;
+                            const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+                            double2 v = crot[j];
+                            if (kinds) {
+                                const uint32_t s1 = slice_decode(S, nS, g);
+                                const uint32_t a = slice_decode(A, nA, g);
+                                const uint32_t b = slice_decode(B, nB, g);
+                                double rr = L.u[s1];
+                                if (a | b) {
+                                    const uint32_t mn = a < b ? a : b;
+                                    rr *= L.p3[mn];
+                                    const double2 pd = L.pd[int(a) - int(b)];
+                                    const double vr = v.x * pd.x - v.y * pd.y;
+                                    v.y = v.x * pd.y + v.y * pd.x;
+                                    v.x = vr;
+                                }
+                                v.x *= rr;
+                                v.y *= rr;
+                            }
+                            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+                            double2 o = *ap;
+                            o.x += v.x;
+                            o.y += v.y;
+                            *ap = o;
+                        }
+                        J0 = J1 = J2 = Z = 0;
+                        if (kinds) {
+#pragma unroll
+                            for (int k = 0; k < kPlanes; ++k) S[k] = A[k] = B[k] = 0;
+                            nS = nA = nB = 0;
+                        }
+                        C = Cn;
+                        ++term;
+                        Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
+                    }
+                }
+            }
+            __syncthreads();  // every thread is done with buffer (i & 1)
+            if (threadIdx.x == 0 && i + 2 < ntiles) {
+                fence_proxy_async();
+                issue(i + 2);
+            }
+        }
+    }
 #pragma unroll 4
     for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
 }
@@ -629,7 +672,7 @@ __global__ void k_debug_phase(const DevTable t, const uint64_t* __restrict__ asg
 // Per (term, assignment) exact product codes, one thread each, wide counters
 // (an independent re-derivation of what the SWAR kernels accumulate).
 __global__ void k_debug_codes(const DevTable t, const uint64_t* __restrict__ asg, uint64_t n, uint32_t* out5) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const SmemLut L = stage_lut(t, smem);
     __syncthreads();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -145,46 +145,73 @@ def imm_fxc(f):          # f(a = X, b = Y) ^ c
 
 MAJ, XOR3 = 0xE8, 0x96
 
-# operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 Y, %9 op
+# operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 op,
+#           %9 phi, %10 Walsh32(phi), %11 base_lo [, %12 phi_hi, %13 base_hi]
+# Double-parity cases compute Y = Walsh32(phi) ^ -parity(phi & base) into the
+# local register yy themselves; single-parity cases never read it (their
+# truth tables are made independent of the q input).
 
 
-def case_body(op):
-    _, w, z, lam, pi, pip, _ = slice_op(op)
+def _single_tables(op):
+    """Truth tables of single-parity ops copied from the q = 0 column to q = 1."""
+    jb, w, z, lam, pi, pip, lm = slice_op(op)
+    if op < 128 and (op & 1):
+        w = [w[0], w[1], w[0], w[1]]
+        dup = lambda t: (t & 3) | ((t & 3) << 2)  # noqa: E731
+        z, lam, pi, pip = dup(z), dup(lam), dup(pi), dup(pip)
+    return jb, w, z, lam, pi, pip, lm
+
+
+def case_body(op, p64=False):
+    _, w, z, lam, pi, pip, _ = _single_tables(op)
     t = [sum(((w[v] >> b) & 1) << v for v in range(4)) for b in range(3)]
     L = []
+    double = op < 128 and not (op & 1)
+    Y = "yy" if double else "%7"
+    if double and (any(t) or bool(z | lam | pi | pip)):
+        if p64:
+            L.append("and.b32 yy, %9, %11;")
+            L.append("and.b32 c0, %12, %13;")
+            L.append("xor.b32 yy, yy, c0;")
+        else:
+            L.append("and.b32 yy, %9, %11;")
+        L.append("popc.b32 yy, yy;")
+        L.append("and.b32 yy, yy, 1;")
+        L.append("neg.s32 yy, yy;")
+        L.append("xor.b32 yy, yy, %10;")
     c0 = c1 = False
     if t[0]:
-        L.append(f"lop3.b32 c0, %0, %7, %8, {imm_af(t[0], 'and'):#04x};")
-        L.append(f"lop3.b32 %0, %0, %7, %8, {imm_af(t[0], 'xor'):#04x};")
+        L.append(f"lop3.b32 c0, %0, %7, {Y}, {imm_af(t[0], 'and'):#04x};")
+        L.append(f"lop3.b32 %0, %0, %7, {Y}, {imm_af(t[0], 'xor'):#04x};")
         c0 = True
     if t[1] and c0:
-        L.append(f"lop3.b32 w1, %7, %7, %8, {imm_f(t[1]):#04x};")
+        L.append(f"lop3.b32 w1, %7, %7, {Y}, {imm_f(t[1]):#04x};")
         L.append(f"lop3.b32 c1, %1, w1, c0, {MAJ:#04x};")
         L.append(f"lop3.b32 %1, %1, w1, c0, {XOR3:#04x};")
         c1 = True
     elif t[1]:
-        L.append(f"lop3.b32 c1, %1, %7, %8, {imm_af(t[1], 'and'):#04x};")
-        L.append(f"lop3.b32 %1, %1, %7, %8, {imm_af(t[1], 'xor'):#04x};")
+        L.append(f"lop3.b32 c1, %1, %7, {Y}, {imm_af(t[1], 'and'):#04x};")
+        L.append(f"lop3.b32 %1, %1, %7, {Y}, {imm_af(t[1], 'xor'):#04x};")
         c1 = True
     elif c0:
         L.append("and.b32 c1, %1, c0;")
         L.append("xor.b32 %1, %1, c0;")
         c1 = True
     if t[2] and c1:
-        L.append(f"lop3.b32 w1, %7, %8, c1, {imm_fxc(t[2]):#04x};")
+        L.append(f"lop3.b32 w1, %7, {Y}, c1, {imm_fxc(t[2]):#04x};")
         L.append("xor.b32 %2, %2, w1;")
     elif t[2]:
-        L.append(f"lop3.b32 %2, %2, %7, %8, {imm_af(t[2], 'xor'):#04x};")
+        L.append(f"lop3.b32 %2, %2, %7, {Y}, {imm_af(t[2], 'xor'):#04x};")
     elif c1:
         L.append("xor.b32 %2, %2, c1;")
     if z:
-        L.append(f"lop3.b32 %3, %3, %7, %8, {imm_af(z, 'or'):#04x};")
+        L.append(f"lop3.b32 %3, %3, %7, {Y}, {imm_af(z, 'or'):#04x};")
     if lam:
-        L.append(f"lop3.b32 %4, %7, %7, %8, {imm_f(lam):#04x};")
+        L.append(f"lop3.b32 %4, %7, %7, {Y}, {imm_f(lam):#04x};")
     if pi:
-        L.append(f"lop3.b32 %5, %7, %7, %8, {imm_f(pi):#04x};")
+        L.append(f"lop3.b32 %5, %7, %7, {Y}, {imm_f(pi):#04x};")
     if pip:
-        L.append(f"lop3.b32 %6, %7, %7, %8, {imm_f(pip):#04x};")
+        L.append(f"lop3.b32 %6, %7, %7, {Y}, {imm_f(pip):#04x};")
     return L
 
 
@@ -194,24 +221,40 @@ def kind_flags(op):
     return (1 << 8 if lam else 0) | (1 << 9 if pi else 0) | (1 << 10 if pip else 0)
 
 
-def generate() -> str:
+def _asm_block(name, p64):
     n = 129
-    lines = ["// GENERATED by paper_2403_06777_b200/gen_slice_ops.py -- do not edit.",
-             "// Bit-sliced per-row update, one jump-table dispatch (brx.idx) per row.",
-             "// operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 Y, %9 op",
-             "#define PZX_SLICE_DISPATCH_ASM \\"]
-    body = ["{", ".reg .b32 c0, c1, w1;",
-            "ts%=: .branchtargets " + ", ".join(f"L{i}_%=" for i in range(n)) + ";",
-            "brx.idx.uni %9, ts%=;"]
+    # identical case bodies share one label (smaller code, fewer I-cache misses)
+    bodies, label_of = {}, []
     for i in range(n):
-        body.append(f"L{i}_%=:")
-        body.extend(case_body(i))
+        key = tuple(case_body(i, p64))
+        if key not in bodies:
+            bodies[key] = len(bodies)
+        label_of.append(bodies[key])
+    lines = [f"#define {name} \\"]
+    body = ["{", ".reg .b32 c0, c1, w1, yy;",
+            "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
+            "brx.idx.uni %8, ts%=;"]
+    for key, lab in sorted(bodies.items(), key=lambda kv: kv[1]):
+        body.append(f"L{lab}_%=:")
+        body.extend(key)
         body.append("bra.uni D%=;")
     body.append("D%=:")
     body.append("}")
     for b in body:
         lines.append(f'    "{b}\\n" \\')
     lines.append("")
+    return lines, len(bodies)
+
+
+def generate() -> str:
+    n = 129
+    lines = ["// GENERATED by paper_2403_06777_b200/gen_slice_ops.py -- do not edit.",
+             "// Bit-sliced per-row update, one jump-table dispatch (brx.idx) per row.",
+             "// operands: %0 J0, %1 J1, %2 J2, %3 Z, %4 vl, %5 vpi, %6 vpip, %7 X, %8 op,",
+             "//           %9 phi, %10 Walsh32(phi), %11 base_lo [, %12 phi_hi, %13 base_hi]"]
+    b32, n32 = _asm_block("PZX_SLICE_DISPATCH_ASM_P32", False)
+    b64, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_P64", True)
+    lines += [f"// {n32} distinct case bodies"] + b32 + b64
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")

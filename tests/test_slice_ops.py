@@ -30,9 +30,14 @@ def test_generated_include_is_current():
     assert open(G.OUT).read() == G.generate()
 
 
-def _bodies():
+def _bodies(p64=False):
     text = G.generate()
-    lines = re.findall(r'"(.*?)\\n"', text)
+    name = "PZX_SLICE_DISPATCH_ASM_P64" if p64 else "PZX_SLICE_DISPATCH_ASM_P32"
+    block = text[text.index(name):]
+    block = block[:block.index("\n\n")]
+    lines = re.findall(r'"(.*?)\\n"', block)
+    table = next(ln for ln in lines if ".branchtargets" in ln)
+    targets = [int(x.strip().split("_")[0][1:]) for x in table.split(".branchtargets")[1].rstrip(";").split(",")]
     bodies, cur = {}, None
     for ln in lines:
         m = re.match(r"L(\d+)_%=:", ln)
@@ -43,34 +48,38 @@ def _bodies():
             cur = None
         elif cur is not None:
             bodies[cur].append(ln)
-    return bodies
+    return {op: bodies[targets[op]] for op in range(len(targets))}
 
 
 def _run(body, regs):
-    """Interpret lop3/and/xor on 1-bit values."""
+    """Interpret the generated PTX subset on 1-bit lanes."""
     r = dict(regs)
 
     def val(tok):
-        return r[tok]
+        return int(tok, 0) & 1 if tok[0].isdigit() else r[tok]
     for ins in body:
-        m = re.match(r"(lop3\.b32|and\.b32|xor\.b32) (.*);", ins)
+        m = re.match(r"(lop3\.b32|and\.b32|xor\.b32|popc\.b32|neg\.s32) (.*);", ins)
         assert m, ins
         ops = [o.strip() for o in m.group(2).split(",")]
-        if m.group(1) == "lop3.b32":
+        kind = m.group(1)
+        if kind == "lop3.b32":
             d, a, b, c, imm = ops
             i = (val(a) << 2) | (val(b) << 1) | val(c)
             r[d] = (int(imm, 16) >> i) & 1
-        elif m.group(1) == "and.b32":
-            d, a, b = ops
-            r[d] = val(a) & val(b)
+        elif kind == "and.b32":
+            r[ops[0]] = val(ops[1]) & val(ops[2])
+        elif kind == "xor.b32":
+            r[ops[0]] = val(ops[1]) ^ val(ops[2])
+        elif kind == "popc.b32":
+            r[ops[0]] = val(ops[1])          # 1-bit lane: popcount parity == the bit
         else:
-            d, a, b = ops
-            r[d] = val(a) ^ val(b)
+            r[ops[0]] = val(ops[1])          # -x on one bit is x (all-ones mask)
     return r
 
 
-def test_every_generated_chain_is_a_correct_mod8_add():
-    bodies = _bodies()
+@pytest.mark.parametrize("p64", [False, True])
+def test_every_generated_chain_is_a_correct_mod8_add(p64):
+    bodies = _bodies(p64)
     assert len(bodies) == 129
     for op in range(129):
         jb, w, z, lam, pi, pip, _ = G.slice_op(op)
@@ -81,8 +90,10 @@ def test_every_generated_chain_is_a_correct_mod8_add():
                 continue
             for j0 in range(8):
                 for zin in (0, 1):
+                    # Y = Walsh(phi) ^ -parity(phi & base): phi = 1, base = q, Walsh = 0 -> q
                     regs = {"%0": j0 & 1, "%1": (j0 >> 1) & 1, "%2": (j0 >> 2) & 1, "%3": zin,
-                            "%4": 0, "%5": 0, "%6": 0, "%7": p, "%8": q}
+                            "%4": 0, "%5": 0, "%6": 0, "%7": p, "%9": 1, "%10": 0, "%11": q,
+                            "%12": 0, "%13": 0}
                     out = _run(bodies[op], regs)
                     jn = out["%0"] | (out["%1"] << 1) | (out["%2"] << 2)
                     if not (z >> v) & 1:
