@@ -85,6 +85,7 @@ struct SmemLut {
     const double* u;
     const double* p3;
     const double2* pd;  // centred: pd[d], d in [-max_rows, max_rows]
+    const double2* ab;  // pi^a pi'^b, a, b < 4, index a | b << 2
 };
 
 __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* dst_bytes) {
@@ -99,6 +100,7 @@ __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* d
     L.u = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.u_off);
     L.p3 = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.p3_off);
     L.pd = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.pd_off) + t.lut_layout.max_rows;
+    L.ab = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.ab_off);
     return L;
 }
 
@@ -528,9 +530,15 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
             const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
+            // software-pipelined: the next row's record is loaded before this
+            // row's dispatch (the read past the last row stays inside shared
+            // memory and is never used)
+            uint4 na = lds128(a0), nb = lds128(a0 + 16);
             for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint4 ra = lds128(ad);       // psi, phi, code, Walsh32(psi)
-                const uint4 rb = lds128(ad + 16);  // Walsh32(phi), psi_hi, phi_hi, 0
+                const uint4 ra = na;  // psi, phi, code, Walsh32(psi)
+                const uint4 rb = nb;  // Walsh32(phi), psi_hi, phi_hi, 0
+                na = lds128(ad + 32);
+                nb = lds128(ad + 48);
                 uint32_t pp;
                 if constexpr (P64) pp = __popc((ra.x & blo) ^ (rb.y & bhi)) & 1u;
                 else pp = __popc(ra.x & blo) & 1u;
@@ -567,6 +575,28 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                         }
                         const bool kinds = (nS | nA | nB) != 0;
                         uint32_t alive = ~Z;
+                        if (kinds && nS < 8 && nA < 4 && nB < 4) {
+                            // fast path: s1 < 8 and a, b < 4 -> fixed-width decode, one
+                            // real (sqrt2-1)^s1 and one complex pi^a pi'^b table lookup
+                            while (alive) {
+                                const int g = 31 - __clz(alive);
+                                alive ^= 1u << g;
+                                const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+                                const uint32_t s1 = ((S[0] >> g) & 1u) | (((S[1] >> g) & 1u) << 1) | (((S[2] >> g) & 1u) << 2);
+                                const uint32_t ab = ((A[0] >> g) & 1u) | (((A[1] >> g) & 1u) << 1) |
+                                                    (((B[0] >> g) & 1u) << 2) | (((B[1] >> g) & 1u) << 3);
+                                const double2 cj = crot[j];
+                                const double2 f = L.ab[ab];
+                                const double rr = L.u[s1];
+                                const double fr = f.x * rr, fi = f.y * rr;
+                                double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+                                double2 o = *ap;
+                                o.x += cj.x * fr - cj.y * fi;
+                                o.y += cj.x * fi + cj.y * fr;
+                                *ap = o;
+                            }
+                            alive = 0;
+                        }
                         while (alive) {
                             const int g = __ffs(alive) - 1;
                             alive &= alive - 1;

@@ -162,13 +162,14 @@ def _single_tables(op):
     return jb, w, z, lam, pi, pip, lm
 
 
-def case_body(op, p64=False):
+def case_body(op, p64=False, y_in=False):
+    """y_in: Y arrives as operand %9 (random-batch kernel) instead of being formed here."""
     _, w, z, lam, pi, pip, _ = _single_tables(op)
     t = [sum(((w[v] >> b) & 1) << v for v in range(4)) for b in range(3)]
     L = []
     double = op < 128 and not (op & 1)
-    Y = "yy" if double else "%7"
-    if double and (any(t) or bool(z | lam | pi | pip)):
+    Y = ("%9" if y_in else "yy") if double else "%7"
+    if double and not y_in and (any(t) or bool(z | lam | pi | pip)):
         if p64:
             L.append("and.b32 yy, %9, %11;")
             L.append("and.b32 c0, %12, %13;")
@@ -221,12 +222,12 @@ def kind_flags(op):
     return (1 << 8 if lam else 0) | (1 << 9 if pi else 0) | (1 << 10 if pip else 0)
 
 
-def _asm_block(name, p64):
+def _asm_block(name, p64, y_in=False):
     n = 129
     # identical case bodies share one label (smaller code, fewer I-cache misses)
     bodies, label_of = {}, []
     for i in range(n):
-        key = tuple(case_body(i, p64))
+        key = tuple(case_body(i, p64, y_in))
         if key not in bodies:
             bodies[key] = len(bodies)
         label_of.append(bodies[key])
@@ -254,7 +255,9 @@ def generate() -> str:
              "//           %9 phi, %10 Walsh32(phi), %11 base_lo [, %12 phi_hi, %13 base_hi]"]
     b32, n32 = _asm_block("PZX_SLICE_DISPATCH_ASM_P32", False)
     b64, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_P64", True)
-    lines += [f"// {n32} distinct case bodies"] + b32 + b64
+    bxy, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_XY", False, True)
+    lines += [f"// {n32} distinct case bodies",
+              "// _XY variant (random batches): operand %9 is Y itself"] + b32 + b64 + bxy
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")
