@@ -482,6 +482,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     r.kernel = (flags & PZX_KERNEL_GENERAL) ? KC_GENERAL
              : (flags & PZX_KERNEL_GRAY)    ? KC_GRAY
              : (flags & PZX_KERNEL_SLICE)   ? KC_SLICE
+             : (flags & PZX_KERNEL_SLICE_RAND) ? KC_SLICER
                                             : KC_AUTO;
     if (r.kernel != KC_AUTO && !kernel_supported(t->dev, r, r.kernel))
         return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "

@@ -69,7 +69,7 @@ struct DevTable {
     int slice_ok = 0;
 };
 
-enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3 };
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4 };
 
 struct LaunchReq {
     const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1

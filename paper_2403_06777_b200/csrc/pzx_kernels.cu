@@ -464,10 +464,43 @@ __host__ __device__ constexpr uint32_t slice_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
-template <bool P64>
+// Random batches: the thread's 32 words are transposed into bit planes
+// (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
+template <bool P64, bool RAND>
 size_t slice_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
-    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16;
+    const size_t planes = RAND ? size_t(P64 ? 64 : 32) * kSliceThreads * 4 : 0;
+    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16 + planes;
+}
+
+// 32 x 32 bit-matrix transpose: afterwards a[i] bit g = (old a[g]) bit i.
+__device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                         : j == 2  ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            if ((k & j) == 0) {
+                const uint32_t tt = ((a[k] >> j) ^ a[k + j]) & m;
+                a[k + j] ^= tt;
+                a[k] ^= tt << j;
+            }
+        }
+    }
+}
+
+// X = XOR of the planes of the parameters set in mask (uniform loop over set bits)
+__device__ __forceinline__ uint32_t planes_parity(uint32_t mask, uint32_t plane_addr) {
+    uint32_t x = 0;
+    while (mask) {
+        const int i = __ffs(mask) - 1;
+        mask &= mask - 1;
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(plane_addr + uint32_t(i) * (kSliceThreads * 4)));
+        x ^= v;
+    }
+    return x;
 }
 
 // Bit-sliced evaluation of enumerated / contiguous batches.
@@ -481,7 +514,7 @@ size_t slice_smem_bytes(const DevTable& t) {
 // table C * w^j (8 entries) is built once per warp, then every live
 // assignment adds C * w^j' * (stuff from S, A, B) into its fp64 accumulator in
 // shared memory.
-template <bool P64>
+template <bool P64, bool RAND>
 __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, const LaunchReq r) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemLut L = kernel_prologue(t, smem, slice_lut_offset<P64>());
@@ -494,7 +527,28 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
     uint64_t tb, te;
     term_range(r, tb, te);
     const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
-    const uint64_t base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    uint64_t base = 0;
+    uint32_t planes_s = 0;  // shared address of this thread's plane 0 (RAND)
+    if constexpr (RAND) {
+        // thread owns the 32 arbitrary words off .. off+31: transpose into planes
+        uint32_t* planes = reinterpret_cast<uint32_t*>(crot + (kSliceThreads / 32 - (threadIdx.x >> 5)) * 8);
+        planes_s = smem_u32(planes) + threadIdx.x * 4;
+        uint32_t w[32];
+#pragma unroll
+        for (int h = 0; h < (P64 ? 2 : 1); ++h) {
+#pragma unroll
+            for (int g = 0; g < 32; ++g) {
+                const uint64_t idx = off + g;
+                const uint64_t word = idx < r.n ? (r.d_asg ? r.d_asg[idx] : r.first + idx) : 0;
+                w[g] = uint32_t(word >> (32 * h));
+            }
+            transpose32(w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) planes[(32 * h + i) * kSliceThreads + threadIdx.x] = w[i];
+        }
+    } else {
+        base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    }
     const uint32_t blo = uint32_t(base), bhi = uint32_t(base >> 32);
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
@@ -539,12 +593,23 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                 const uint4 rb = nb;  // Walsh32(phi), psi_hi, phi_hi, 0
                 na = lds128(ad + 32);
                 nb = lds128(ad + 48);
+                const uint32_t op = ra.z & 0xFFu;
+                uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
+                if constexpr (RAND) {
+                    uint32_t X = planes_parity(ra.x, planes_s), Y = 0;
+                    if (ra.y) Y = planes_parity(ra.y, planes_s);
+                    if constexpr (P64) {
+                        X ^= planes_parity(rb.y, planes_s + 32 * kSliceThreads * 4);
+                        if (rb.z) Y ^= planes_parity(rb.z, planes_s + 32 * kSliceThreads * 4);
+                    }
+                    asm(PZX_SLICE_DISPATCH_ASM_XY
+                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                        : "r"(X), "r"(op), "r"(Y));
+                } else {
                 uint32_t pp;
                 if constexpr (P64) pp = __popc((ra.x & blo) ^ (rb.y & bhi)) & 1u;
                 else pp = __popc(ra.x & blo) & 1u;
                 const uint32_t X = ra.w ^ (0u - pp);
-                const uint32_t op = ra.z & 0xFFu;
-                uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
                 if constexpr (P64) {
                     asm(PZX_SLICE_DISPATCH_ASM_P64
                         : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
@@ -553,6 +618,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                     asm(PZX_SLICE_DISPATCH_ASM_P32
                         : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
                         : "r"(X), "r"(op), "r"(ra.y), "r"(rb.x), "r"(blo));
+                }
                 }
                 if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
                     if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
@@ -738,11 +804,13 @@ cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, con
 
 template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
-    if (kc == KC_SLICE) {
-        const size_t sm = slice_smem_bytes<P64>(t);
-        cudaError_t e = cudaFuncSetAttribute(k_eval_slice<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (kc == KC_SLICE || kc == KC_SLICER) {
+        const bool rnd = kc == KC_SLICER;
+        const size_t sm = rnd ? slice_smem_bytes<P64, true>(t) : slice_smem_bytes<P64, false>(t);
+        auto kern = rnd ? k_eval_slice<P64, true> : k_eval_slice<P64, false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
-        k_eval_slice<P64><<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     const size_t sm = smem_lut_offset<P64>() + t.lut_layout.bytes;
@@ -759,18 +827,20 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
+    if (t.slice_ok) return KC_SLICER;
     return KC_GENERAL;
 }
 
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
+    if (kc == KC_SLICER) return t.slice_ok != 0;
     if (kc == KC_GRAY) return enumerated && (r.first % kGray) == 0;
     return true;
 }
 
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = kc == KC_SLICE ? uint64_t(kSliceThreads) * kSliceG
+    const uint64_t per = (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(kSliceThreads) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
@@ -783,16 +853,14 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
-    if (kc == KC_SLICE) {
-        if (t.p64) {
-            sm = slice_smem_bytes<true>(t);
-            cudaFuncSetAttribute(k_eval_slice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_slice<true>, kSliceThreads, sm);
-        } else {
-            sm = slice_smem_bytes<false>(t);
-            cudaFuncSetAttribute(k_eval_slice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_slice<false>, kSliceThreads, sm);
-        }
+    if (kc == KC_SLICE || kc == KC_SLICER) {
+        const bool rnd = kc == KC_SLICER;
+        auto kern = t.p64 ? (rnd ? k_eval_slice<true, true> : k_eval_slice<true, false>)
+                          : (rnd ? k_eval_slice<false, true> : k_eval_slice<false, false>);
+        sm = t.p64 ? (rnd ? slice_smem_bytes<true, true>(t) : slice_smem_bytes<true, false>(t))
+                   : (rnd ? slice_smem_bytes<false, true>(t) : slice_smem_bytes<false, false>(t));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_GRAY) {
         if (t.p64) { if (lng) PZX_OCC((k_eval_gray<true, kGrayBits, true>)); else PZX_OCC((k_eval_gray<true, kGrayBits, false>)); }
         else { if (lng) PZX_OCC((k_eval_gray<false, kGrayBits, true>)); else PZX_OCC((k_eval_gray<false, kGrayBits, false>)); }

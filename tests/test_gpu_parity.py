@@ -118,6 +118,19 @@ def test_slice_kernel_vs_oracle(ctx, P_):
     assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
 
 
+@pytest.mark.parametrize("P_", [7, 20, 32, 33, 64])
+def test_slice_rand_kernel_vs_oracle(ctx, P_):
+    """Bit-sliced kernel on arbitrary word lists (transposed parameter planes)."""
+    e = synth.generate(P_, 600, 1, 40, 500 + P_)
+    t = ctx.compile_bit_table(e)
+    words = np.random.default_rng(P_).integers(0, 2**64, 3000, dtype=np.uint64)  # high bits ignored
+    amp = ctx.evaluate_batch(t, words, flags=P.KERNEL_SLICE_RAND)
+    idx = np.random.default_rng(1).choice(words.size, 64, replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+    assert_close(amp, ctx.evaluate_batch(t, words, flags=P.KERNEL_GENERAL), 1e-13)
+
+
 def test_random_assignments_mid_size(ctx):
     e = synth.generate(20, 4096, 16, 48, 77)
     t = ctx.compile_bit_table(e)
