@@ -205,7 +205,7 @@ def run_ours(args):
     table = ctx.compile_bit_table(expr)
     log(f"[bench] rank {rank}: table compiled+uploaded in {time.time() - t0:.1f}s "
         f"({table.n_rows} rows, max {table.max_term_rows}/term)")
-    N = cfg.n_assign                        # per-rank batch (weak scaling)
+    N = args.assign or cfg.n_assign         # per-rank batch (weak scaling)
     first = rank * N
     words_host = None
     if not cfg.enumerated:
@@ -220,10 +220,13 @@ def run_ours(args):
     d_words = torch.from_numpy(words_host.view(np.int64)).to(dev) if words_host is not None else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    kflag = {"auto": 0, "general": P.KERNEL_GENERAL, "gray": P.KERNEL_GRAY, "slice": P.KERNEL_SLICE,
+             "slice_rand": P.KERNEL_SLICE_RAND}[args.kernel]
+
     def step():
         ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
                             first=first, d_amp=d_amp.data_ptr(), d_prob=d_prob.data_ptr(),
-                            flags=P.PROB_REAL if cfg.prob_real else P.PROB_ABS2, stream=sh)
+                            flags=(P.PROB_REAL if cfg.prob_real else P.PROB_ABS2) | kflag, stream=sh)
 
     for _ in range(args.warmup):
         step()
@@ -254,43 +257,45 @@ def run_ours(args):
     value = world * N * args.steps / (tot_ms / 1e3)
 
     # ---- end to end through the public API (host buffers) -------------------
-    if words_host is None:
-        words_e2e = np.arange(first, first + N, dtype=np.uint64)
-    else:
-        words_e2e = words_host
-    pinned_w = torch.from_numpy(words_e2e.view(np.int64)).pin_memory()
-    pinned_amp = torch.empty(2 * N, dtype=torch.float64).pin_memory()
-    pinned_prob = torch.empty(N, dtype=torch.float64).pin_memory()
-    import ctypes as C
-    from paper_2403_06777_b200 import _native as NV
-    L = NV.lib()
-    fl = P.PROB_REAL if cfg.prob_real else P.PROB_ABS2
+    e2e_value, same = None, None
+    if not args.no_e2e:
+        if words_host is None:
+            words_e2e = np.arange(first, first + N, dtype=np.uint64)
+        else:
+            words_e2e = words_host
+        pinned_w = torch.from_numpy(words_e2e.view(np.int64)).pin_memory()
+        pinned_amp = torch.empty(2 * N, dtype=torch.float64).pin_memory()
+        pinned_prob = torch.empty(N, dtype=torch.float64).pin_memory()
+        import ctypes as C
+        from paper_2403_06777_b200 import _native as NV
+        L = NV.lib()
+        fl = (P.PROB_REAL if cfg.prob_real else P.PROB_ABS2) | kflag
 
-    def e2e_step():
-        st = L.pzx_evaluate(ctx.handle, table.handle,
-                            C.cast(pinned_w.data_ptr(), C.POINTER(C.c_uint64)), N,
-                            C.cast(pinned_amp.data_ptr(), NV.dblp), C.cast(pinned_prob.data_ptr(), NV.dblp), fl)
-        if st:
-            raise RuntimeError(L.pzx_last_error(ctx.handle).decode())
+        def e2e_step():
+            st = L.pzx_evaluate(ctx.handle, table.handle,
+                                C.cast(pinned_w.data_ptr(), C.POINTER(C.c_uint64)), N,
+                                C.cast(pinned_amp.data_ptr(), NV.dblp), C.cast(pinned_prob.data_ptr(), NV.dblp), fl)
+            if st:
+                raise RuntimeError(L.pzx_last_error(ctx.handle).decode())
 
-    e2e_step()
-    e2e_times = []
-    if world > 1:
-        dist.barrier()
-    for _ in range(max(1, args.steps)):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
         e2e_step()
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_tot = sum(e2e_times)
-    if world > 1:
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_tot = float(t.item())
-    e2e_value = world * N * len(e2e_times) / e2e_tot
-    # sanity: e2e results equal the device-resident ones (same kernel, same words)
-    same = np.allclose(pinned_amp.numpy(), d_amp.cpu().numpy(), rtol=0, atol=0)
+        e2e_times = []
+        if world > 1:
+            dist.barrier()
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            e2e_step()
+            e2e_times.append(time.perf_counter() - t0)
+        e2e_tot = sum(e2e_times)
+        if world > 1:
+            t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_tot = float(t.item())
+        e2e_value = world * N * len(e2e_times) / e2e_tot
+        # sanity: e2e results equal the device-resident ones (same kernel, same words)
+        same = np.allclose(pinned_amp.numpy(), d_amp.cpu().numpy(), rtol=0, atol=0)
 
     # ---- roofline (ALU / INT issue bound) -------------------
     mean_ms = tot_ms / args.steps
@@ -328,9 +333,10 @@ def run_ours(args):
             "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": m, "n_rows": R,
                        "assignments_per_gpu": N, "batch": "enumerated" if cfg.enumerated else "random",
                        "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                       "parallelism": f"assignment shards x{world}"},
-            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
-                    "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
+                       "parallelism": f"assignment shards x{world}", "kernel": args.kernel},
+            "e2e": None if e2e_value is None else {
+                "value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
+                "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
                          "frac": achieved / peak_tops, "traffic": traffic,
@@ -357,8 +363,12 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand"],
+                    help="force one evaluation kernel (default: the library's choice)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
