@@ -827,7 +827,8 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
-    if (t.slice_ok) return KC_SLICER;
+    // arbitrary word lists: the POPC kernel (2.0e12 row-evals/s on C3) still
+    // beats the plane-XOR bit-sliced variant (1.65e12, profiles/README.md)
     return KC_GENERAL;
 }
 
