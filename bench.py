@@ -221,7 +221,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     kflag = {"auto": 0, "general": P.KERNEL_GENERAL, "gray": P.KERNEL_GRAY, "slice": P.KERNEL_SLICE,
-             "slice_rand": P.KERNEL_SLICE_RAND}[args.kernel]
+             "slice_rand": P.KERNEL_SLICE_RAND, "sorted": P.KERNEL_SORTED}[args.kernel]
 
     def step():
         ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
@@ -367,7 +367,7 @@ def main():
     ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand", "sorted"],
                     help="force one evaluation kernel (default: the library's choice)")
     args = ap.parse_args()
     if args.impl == "reference":

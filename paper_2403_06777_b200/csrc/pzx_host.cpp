@@ -154,6 +154,7 @@ struct HostTable {
     std::vector<uint8_t> swapped;           // row stored with psi/phi exchanged
     std::vector<uint8_t> unit;              // placeholder row of a row-less term
     std::vector<uint4> srows;               // bit-sliced kernel rows (2 per row)
+    std::vector<uint4> qrows;               // sorted-batch kernel rows (2 per row, n_params <= 32)
     std::vector<double> sterm_c;            // its term constants (2 per term)
     int jb_term = 0;                        // running sum of slice jbase in the open term
     uint64_t n_dev_rows() const { return unit.size(); }
@@ -183,6 +184,15 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     h.jb_term += kSliceJbase[op];
     h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), op | uint32_t(kSliceKindFlags[op]), walsh32(psi)));
     h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
+    if (h.n_params <= 32) {
+        auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)
+            return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * kSortedTableStride);
+        };
+        const uint32_t code = op | uint32_t(kSliceKindFlags[op]);
+        h.qrows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, 0));
+        h.qrows.push_back(make_uint4(offs(psi, 0) | (offs(psi, 1) << 16), offs(psi, 2) | (offs(psi, 3) << 16),
+                                     offs(phi, 0) | (offs(phi, 1) << 16), offs(phi, 2) | (offs(phi, 3) << 16)));
+    }
     if (h.n_params <= 32) {
         h.rows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, pat));
     } else {  // 32-byte record: masks, then {code, pattern}
@@ -224,6 +234,7 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
         if ((i + 1) % kSegRows == 0) code_word(h, row0 + i) |= kSegFlag;
     code_word(h, row0 + n_rows_term - 1) |= kEndFlag;
     h.srows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
+    if (!h.qrows.empty()) h.qrows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
     h.max_rows = std::max<uint32_t>(h.max_rows, uint32_t(n_rows_term));
     h.coef.push_back(c);
     h.e_t.push_back(e);
@@ -378,6 +389,7 @@ struct pzx_ctx {
     void* d_partial = nullptr; size_t partial_cap = 0;
     void* d_chunks = nullptr; size_t chunks_cap = 0;
     void* d_dbg = nullptr; size_t dbg_cap = 0;
+    void* d_sort = nullptr; size_t sort_cap = 0;
 };
 
 struct pzx_table {
@@ -391,6 +403,7 @@ struct pzx_table {
     void* d_lut = nullptr;
     void* d_srows = nullptr;
     void* d_sterm_c = nullptr;
+    void* d_qrows = nullptr;
 };
 
 namespace {
@@ -437,6 +450,8 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
         if ((st = cuda_err(ctx, upload_vec(&t->d_srows, h.srows), "upload slice rows"))) return st;
         if ((st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
     }
+    const bool sorted_ok = slice_ok && h.n_params <= 32;
+    if (sorted_ok && (st = cuda_err(ctx, upload_vec(&t->d_qrows, h.qrows), "upload sorted-kernel rows"))) return st;
     LutLayout L;
     std::vector<unsigned char> blob = build_lut(h.max_rows, L);
     if ((st = cuda_err(ctx, upload_vec(&t->d_lut, blob), "upload lut"))) return st;
@@ -454,6 +469,8 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     d.slice_ok = slice_ok ? 1 : 0;
     d.srows = static_cast<const uint4*>(t->d_srows);
     d.sterm_c = static_cast<const double2*>(t->d_sterm_c);
+    d.sorted_ok = sorted_ok ? 1 : 0;
+    d.qrows = static_cast<const uint4*>(t->d_qrows);
     t->ctx = ctx;
     t->device = ctx->device;
     *out = t.release();
@@ -483,14 +500,32 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
              : (flags & PZX_KERNEL_GRAY)    ? KC_GRAY
              : (flags & PZX_KERNEL_SLICE)   ? KC_SLICE
              : (flags & PZX_KERNEL_SLICE_RAND) ? KC_SLICER
+             : (flags & PZX_KERNEL_SORTED)  ? KC_SORTED
                                             : KC_AUTO;
     if (r.kernel != KC_AUTO && !kernel_supported(t->dev, r, r.kernel))
         return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "
                                            "(enumerated kernels need a contiguous batch starting at a multiple "
                                            "of 16 (gray) or 32 (slice); slice needs terms of <= 127 rows)");
-    const KernelChoice kc = choose_kernel(t->dev, r);
+    KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    if (kc == KC_SORTED) {  // sort word|position pairs; results are scattered back by position
+        if (r.n > uint64_t(UINT32_MAX)) return set_err(ctx, PZX_E_CAPACITY, "sorted kernel: batch > 2^32");
+        if (!r.d_asg) return set_err(ctx, PZX_E_INVALID, "sorted kernel needs an explicit word list");
+        if ((st = cuda_err(ctx, grow(&ctx->d_sort, &ctx->sort_cap, sort_scratch_bytes(r.n) + 256), "alloc sort scratch"))) return st;
+        if ((st = cuda_err(ctx, sort_words(r.d_asg, r.n, t->dev.n_params, ctx->d_sort, &r.d_sorted, &r.d_perm,
+                                           r.stream, &ctx->launches), "sort words"))) return st;
+        uint64_t spread = 0;
+        void* tmp8 = static_cast<unsigned char*>(ctx->d_sort) + sort_scratch_bytes(r.n);
+        if ((st = cuda_err(ctx, sorted_max_spread(r.d_sorted, r.n, tmp8, &spread, r.stream, &ctx->launches), "spread"))) return st;
+        if (spread >= (uint64_t(1) << kSortedLowBits)) {  // too sparse for two high parts per thread
+            if (r.kernel == KC_SORTED)
+                return set_err(ctx, PZX_E_INVALID, "sorted kernel: batch too sparse (32-word groups span >= 2^16)");
+            kc = KC_GENERAL;
+            r.d_sorted = nullptr;
+            r.d_perm = nullptr;
+        }
+    }
     // grid policy: split the terms into chunks so that the grid is >= kWaves
     // full waves of resident CTAs (keeps the last-wave tail small); chunk
     // partials are bounded to ~1 GiB of scratch
@@ -576,7 +611,7 @@ void pzx_destroy(pzx_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg})
+    for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg, ctx->d_sort})
         if (p) cudaFree(p);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -653,7 +688,7 @@ void pzx_table_free(pzx_table* t) {
     if (!t) return;
     if (t->device < 0) { delete t; return; }
     cudaSetDevice(t->device);
-    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c})
+    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows})
         if (p) cudaFree(p);
     delete t;
 }

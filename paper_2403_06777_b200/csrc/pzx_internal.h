@@ -67,9 +67,20 @@ struct DevTable {
     const uint4* srows = nullptr;
     const double2* sterm_c = nullptr;
     int slice_ok = 0;
+    // sorted-batch bit-sliced kernel (arbitrary word lists, n_params <= 32):
+    // rows as 2 x uint4 {psi, phi, op | flags, 0}, {psi offsets 0|1, psi offsets 2|3,
+    // phi offsets 0|1, phi offsets 2|3}; offset k = (k * 16 + nibble_k(mask)) *
+    // kSortedTableStride (16-bit byte offsets into the per-thread Four-Russians
+    // tables of the low 16 parameter bits)
+    const uint4* qrows = nullptr;
+    int sorted_ok = 0;
 };
 
-enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4 };
+constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables
+constexpr int kSortedLowBits = 4 * kSortedGroups;
+constexpr uint32_t kSortedTableStride = 128 * 4;  // bytes between table rows (128 threads x 4 B)
+
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5 };
 
 struct LaunchReq {
     const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1
@@ -86,7 +97,20 @@ struct LaunchReq {
     double2* d_partial = nullptr;     // [n_chunks][n] when n_chunks > 1
     const uint64_t* d_chunk_terms = nullptr;  // [n_chunks + 1] term boundaries
     int n_chunks = 1;
+    // KC_SORTED: the batch sorted by (masked) word; results go to d_perm[i]
+    const uint64_t* d_sorted = nullptr;
+    const uint32_t* d_perm = nullptr;
 };
+
+// Sort an arbitrary word list (masked to n_params bits) with its positions:
+// scratch must hold sort_scratch_bytes(n) bytes; outputs live inside scratch.
+size_t sort_scratch_bytes(uint64_t n);
+// max over 32-word groups of (last - first) of the sorted batch (device -> host)
+cudaError_t sorted_max_spread(const uint64_t* d_sorted, uint64_t n, void* d_tmp8, uint64_t* h_out,
+                              cudaStream_t s, uint64_t* launches);
+cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, void* scratch,
+                       const uint64_t** d_sorted, const uint32_t** d_perm, cudaStream_t s,
+                       uint64_t* launches);
 
 // Grid policy helpers (host)
 int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);

@@ -25,6 +25,8 @@
 //                                  host-precomputed Walsh pattern.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "pzx_classes.h"
 #include "pzx_internal.h"
 #include "pzx_slice_dispatch.inc"
@@ -265,6 +267,7 @@ __device__ __forceinline__ void store_result(const LaunchReq& r, uint64_t idx, d
         r.d_partial[uint64_t(blockIdx.y) * r.n + idx] = amp;
         return;
     }
+    if (r.d_perm) idx = r.d_perm[idx];  // sorted batch: back to the caller's order
     if (r.accumulate) {
         const double2 o = r.d_amp[idx];
         amp.x += o.x;
@@ -464,6 +467,87 @@ __host__ __device__ constexpr uint32_t slice_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
+// Term epilogue shared by the bit-sliced kernels: fold 6*s1 into J, build
+// the warp's C * w^j table, and add every live assignment's term value into its
+// fp64 accumulator; resets the per-term state.
+__device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemLut& L, double2* crot,
+                                                    double2* amp_s, uint32_t& J0, uint32_t& J1,
+                                                    uint32_t& J2, uint32_t& Z, uint32_t (&S)[kPlanes],
+                                                    uint32_t (&A)[kPlanes], uint32_t (&B)[kPlanes],
+                                                    uint32_t& nS, uint32_t& nA, uint32_t& nB) {
+    // ---- term epilogue -------------------------------------
+    const uint32_t lane = threadIdx.x & 31u;
+    __syncwarp();
+    if (lane < 8) {
+        const double2 w = L.om[lane];
+        crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+    }
+    __syncwarp();
+    if (nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
+        const uint32_t w1 = S[0], w2 = S[0] ^ S[1];
+        const uint32_t c1 = J1 & w1;
+        J1 ^= w1;
+        J2 ^= w2 ^ c1;
+    }
+    const bool kinds = (nS | nA | nB) != 0;
+    uint32_t alive = ~Z;
+    if (kinds && nS < 8 && nA < 4 && nB < 4) {
+        // fast path: s1 < 8 and a, b < 4 -> fixed-width decode, one
+        // real (sqrt2-1)^s1 and one complex pi^a pi'^b table lookup
+        while (alive) {
+            const int g = 31 - __clz(alive);
+            alive ^= 1u << g;
+            const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+            const uint32_t s1 = ((S[0] >> g) & 1u) | (((S[1] >> g) & 1u) << 1) | (((S[2] >> g) & 1u) << 2);
+            const uint32_t ab = ((A[0] >> g) & 1u) | (((A[1] >> g) & 1u) << 1) |
+                                (((B[0] >> g) & 1u) << 2) | (((B[1] >> g) & 1u) << 3);
+            const double2 cj = crot[j];
+            const double2 f = L.ab[ab];
+            const double rr = L.u[s1];
+            const double fr = f.x * rr, fi = f.y * rr;
+            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+            double2 o = *ap;
+            o.x += cj.x * fr - cj.y * fi;
+            o.y += cj.x * fi + cj.y * fr;
+            *ap = o;
+        }
+        alive = 0;
+    }
+    while (alive) {
+        const int g = __ffs(alive) - 1;
+        alive &= alive - 1;
+        const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+        double2 v = crot[j];
+        if (kinds) {
+            const uint32_t s1 = slice_decode(S, nS, g);
+            const uint32_t a = slice_decode(A, nA, g);
+            const uint32_t b = slice_decode(B, nB, g);
+            double rr = L.u[s1];
+            if (a | b) {
+                const uint32_t mn = a < b ? a : b;
+                rr *= L.p3[mn];
+                const double2 pd = L.pd[int(a) - int(b)];
+                const double vr = v.x * pd.x - v.y * pd.y;
+                v.y = v.x * pd.y + v.y * pd.x;
+                v.x = vr;
+            }
+            v.x *= rr;
+            v.y *= rr;
+        }
+        double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+        double2 o = *ap;
+        o.x += v.x;
+        o.y += v.y;
+        *ap = o;
+    }
+    J0 = J1 = J2 = Z = 0;
+    if (kinds) {
+#pragma unroll
+        for (int k = 0; k < kPlanes; ++k) S[k] = A[k] = B[k] = 0;
+        nS = nA = nB = 0;
+    }
+}
+
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
 template <bool P64, bool RAND>
@@ -625,77 +709,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                     if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
                     if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
                     if (ra.z & kEndFlag) {
-                        // ---- term epilogue -------------------------------------
-                        const uint32_t lane = threadIdx.x & 31u;
-                        __syncwarp();
-                        if (lane < 8) {
-                            const double2 w = L.om[lane];
-                            crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
-                        }
-                        __syncwarp();
-                        if (nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
-                            const uint32_t w1 = S[0], w2 = S[0] ^ S[1];
-                            const uint32_t c1 = J1 & w1;
-                            J1 ^= w1;
-                            J2 ^= w2 ^ c1;
-                        }
-                        const bool kinds = (nS | nA | nB) != 0;
-                        uint32_t alive = ~Z;
-                        if (kinds && nS < 8 && nA < 4 && nB < 4) {
-                            // fast path: s1 < 8 and a, b < 4 -> fixed-width decode, one
-                            // real (sqrt2-1)^s1 and one complex pi^a pi'^b table lookup
-                            while (alive) {
-                                const int g = 31 - __clz(alive);
-                                alive ^= 1u << g;
-                                const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
-                                const uint32_t s1 = ((S[0] >> g) & 1u) | (((S[1] >> g) & 1u) << 1) | (((S[2] >> g) & 1u) << 2);
-                                const uint32_t ab = ((A[0] >> g) & 1u) | (((A[1] >> g) & 1u) << 1) |
-                                                    (((B[0] >> g) & 1u) << 2) | (((B[1] >> g) & 1u) << 3);
-                                const double2 cj = crot[j];
-                                const double2 f = L.ab[ab];
-                                const double rr = L.u[s1];
-                                const double fr = f.x * rr, fi = f.y * rr;
-                                double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
-                                double2 o = *ap;
-                                o.x += cj.x * fr - cj.y * fi;
-                                o.y += cj.x * fi + cj.y * fr;
-                                *ap = o;
-                            }
-                            alive = 0;
-                        }
-                        while (alive) {
-                            const int g = __ffs(alive) - 1;
-                            alive &= alive - 1;
-                            const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
-                            double2 v = crot[j];
-                            if (kinds) {
-                                const uint32_t s1 = slice_decode(S, nS, g);
-                                const uint32_t a = slice_decode(A, nA, g);
-                                const uint32_t b = slice_decode(B, nB, g);
-                                double rr = L.u[s1];
-                                if (a | b) {
-                                    const uint32_t mn = a < b ? a : b;
-                                    rr *= L.p3[mn];
-                                    const double2 pd = L.pd[int(a) - int(b)];
-                                    const double vr = v.x * pd.x - v.y * pd.y;
-                                    v.y = v.x * pd.y + v.y * pd.x;
-                                    v.x = vr;
-                                }
-                                v.x *= rr;
-                                v.y *= rr;
-                            }
-                            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
-                            double2 o = *ap;
-                            o.x += v.x;
-                            o.y += v.y;
-                            *ap = o;
-                        }
-                        J0 = J1 = J2 = Z = 0;
-                        if (kinds) {
-#pragma unroll
-                            for (int k = 0; k < kPlanes; ++k) S[k] = A[k] = B[k] = 0;
-                            nS = nA = nB = 0;
-                        }
+                        slice_term_epilogue(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
                         C = Cn;
                         ++term;
                         Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
@@ -713,15 +727,174 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
     for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
 }
 
+// ------------------------------------------------------ sorted kernel ----
+// Bit-sliced evaluation of an ARBITRARY word list after sorting it (host side
+// sorts word|position pairs with cub and checks that every group of 32
+// consecutive sorted words spans < 2^16). A thread owns 32 consecutive sorted
+// words, so their high parts (bits >= 16) take at most two values H0, H0 + 1:
+//   X = parity(psi & a_g) for g < 32
+//     = XOR_k T_k[nibble_k(psi)]                 (parameters 0..15: per-thread
+//                                                  Four-Russians tables, 4 x 16 words)
+//     ^ (g in M ? -parity(psi & H1) : -parity(psi & H0))   (parameters >= 16)
+// with the tables built once per thread from its transposed low-bit planes.
+// The rest (dispatch, counters, epilogue) is the slice kernel's.
+template <int Dummy = 0>
+__host__ __device__ constexpr uint32_t sorted_lut_offset() {
+    return 2 * kSliceTile * 32 + 16;
+}
+
+size_t sorted_smem_bytes(const DevTable& t) {
+    const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16 +
+           size_t(kSortedGroups) * 16 * kSortedTableStride;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t, const LaunchReq r) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset());
+    const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
+    double2* crot = amp_s + kSliceG * kSliceThreads + (threadIdx.x >> 5) * 8;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + kSliceG * kSliceThreads + (kSliceThreads / 32) * 8);
+#pragma unroll
+    for (int g = 0; g < kSliceG; ++g) amp_s[g * kSliceThreads + threadIdx.x] = make_double2(0.0, 0.0);
+
+    uint64_t tb, te;
+    term_range(r, tb, te);
+    const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
+    // ---- this thread's 32 sorted words -> planes -> Four-Russians tables ----
+    uint32_t w[32];
+#pragma unroll
+    for (int g = 0; g < 32; ++g) {
+        const uint64_t idx = off + g < r.n ? off + g : r.n - 1;  // pad with the last word (keeps order)
+        w[g] = uint32_t(r.d_sorted[idx]);
+    }
+    const uint32_t hmask = ~((1u << kSortedLowBits) - 1u);
+    const uint32_t H0 = w[0] & hmask, H1 = H0 + (1u << kSortedLowBits);
+    uint32_t M = 0;  // assignments whose high part is H1 (the host guarantees spread < 2^16)
+#pragma unroll
+    for (int g = 0; g < 32; ++g) M |= uint32_t((w[g] & hmask) != H0) << g;
+    transpose32(w);  // w[i] = plane i (bit g = bit i of word g)
+#pragma unroll
+    for (int k = 0; k < kSortedGroups; ++k) {
+        uint32_t e[16];
+        e[0] = 0;
+#pragma unroll
+        for (int v = 1; v < 16; ++v) e[v] = e[v & (v - 1)] ^ w[4 * k + ((v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : 3)];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) tab[(k * 16 + v) * kSliceThreads + threadIdx.x] = e[v];
+    }
+    const uint32_t tab_s = smem_u32(tab) + threadIdx.x * 4;
+    auto parity_vec = [&](uint32_t mask, uint32_t o01, uint32_t o23) -> uint32_t {
+        const uint32_t x = lds32(tab_s + (o01 & 0xFFFFu)) ^ lds32(tab_s + (o01 >> 16)) ^
+                           lds32(tab_s + (o23 & 0xFFFFu)) ^ lds32(tab_s + (o23 >> 16));
+        const uint32_t p0 = __popc(mask & H0) & 1u, p1 = __popc(mask & H1) & 1u;
+        return x ^ (0u - p0) ^ (M & (0u - (p0 ^ p1)));
+    };
+
+    uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
+    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
+#pragma unroll
+    for (int i = 0; i < kPlanes; ++i) S[i] = A[i] = B[i] = 0;
+    uint32_t nS = 0, nA = 0, nB = 0;
+    __syncwarp();
+
+    if (tb < te) {
+        uint4* tiles = reinterpret_cast<uint4*>(smem);
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSliceTile * 32);
+        const uint32_t tiles_s = smem_u32(tiles);
+        const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
+        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        auto issue = [&](uint32_t tile) {
+            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
+            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint32_t bytes = uint32_t(n) * 32u;
+            uint64_t* bar = &bars[tile & 1];
+            mbar_expect_tx(bar, bytes);
+            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.qrows + rr * 2, bytes, bar);
+        };
+        if (threadIdx.x == 0) {
+            if (ntiles > 0) issue(0);
+            if (ntiles > 1) issue(1);
+        }
+        uint64_t term = tb;
+        double2 C = __ldg(t.sterm_c + tb);
+        double2 Cn = (tb + 1 < te) ? __ldg(t.sterm_c + tb + 1) : make_double2(0.0, 0.0);
+        for (uint32_t i = 0; i < ntiles; ++i) {
+            mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
+            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
+            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint32_t aend = a0 + n * 32;
+            uint4 na = lds128(a0), nb = lds128(a0 + 16);
+            for (uint32_t ad = a0; ad < aend; ad += 32) {
+                const uint4 ra = na;  // psi, phi, code, 0
+                const uint4 rb = nb;  // psi offsets 0|1, 2|3, phi offsets 0|1, 2|3
+                na = lds128(ad + 32);
+                nb = lds128(ad + 48);
+                const uint32_t X = parity_vec(ra.x, rb.x, rb.y);
+                const uint32_t Y = ra.y ? parity_vec(ra.y, rb.z, rb.w) : 0u;
+                const uint32_t op = ra.z & 0xFFu;
+                uint32_t vl, vpi, vpip;
+                asm(PZX_SLICE_DISPATCH_ASM_XY
+                    : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                    : "r"(X), "r"(op), "r"(Y));
+                if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
+                    if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
+                    if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
+                    if (ra.z & kEndFlag) {
+                        slice_term_epilogue(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
+                        C = Cn;
+                        ++term;
+                        Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && i + 2 < ntiles) {
+                fence_proxy_async();
+                issue(i + 2);
+            }
+        }
+    }
+#pragma unroll 4
+    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
+}
+
+__global__ void k_max_spread(const uint64_t* __restrict__ sorted, uint64_t n, unsigned long long* out) {
+    const uint64_t grp = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t i0 = grp * kSliceG;
+    if (i0 >= n) return;
+    const uint64_t i1 = i0 + kSliceG - 1 < n ? i0 + kSliceG - 1 : n - 1;
+    atomicMax(out, (unsigned long long)(sorted[i1] - sorted[i0]));
+}
+
+__global__ void k_mask_iota(const uint64_t* __restrict__ in, uint64_t n, uint64_t mask, uint64_t* keys,
+                            uint32_t* vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = in[i] & mask;
+    vals[i] = uint32_t(i);
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic fixed-order reduction of per-chunk partial amplitudes.
 __global__ void k_reduce_partials(const double2* __restrict__ partial, int n_chunks, uint64_t n,
-                                  double2* amp, double* prob, int prob_mode, int accumulate) {
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                                  double2* amp, double* prob, int prob_mode, int accumulate,
+                                  const uint32_t* __restrict__ perm) {
+    const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint64_t i = perm ? perm[k] : k;
     double2 s = make_double2(0.0, 0.0);
     for (int c = 0; c < n_chunks; ++c) {
-        const double2 v = partial[uint64_t(c) * n + i];
+        const double2 v = partial[uint64_t(c) * n + k];
         s.x += v.x;
         s.y += v.y;
     }
@@ -804,6 +977,13 @@ cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, con
 
 template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
+    if (kc == KC_SORTED) {
+        const size_t sm = sorted_smem_bytes(t);
+        cudaError_t e = cudaFuncSetAttribute(k_eval_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        k_eval_sorted<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        return cudaGetLastError();
+    }
     if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         const size_t sm = rnd ? slice_smem_bytes<P64, true>(t) : slice_smem_bytes<P64, false>(t);
@@ -827,8 +1007,9 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
-    // arbitrary word lists: the POPC kernel (2.0e12 row-evals/s on C3) still
-    // beats the plane-XOR bit-sliced variant (1.65e12, profiles/README.md)
+    // arbitrary word lists: sort, then the bit-sliced kernel with per-thread
+    // Four-Russians tables (needs n_params <= 32 and terms <= 127 rows)
+    if (t.sorted_ok && r.n >= uint64_t(kSliceG)) return KC_SORTED;
     return KC_GENERAL;
 }
 
@@ -836,12 +1017,13 @@ bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
     if (kc == KC_SLICER) return t.slice_ok != 0;
+    if (kc == KC_SORTED) return t.sorted_ok != 0;
     if (kc == KC_GRAY) return enumerated && (r.first % kGray) == 0;
     return true;
 }
 
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(kSliceThreads) * kSliceG
+    const uint64_t per = (kc == KC_SLICE || kc == KC_SLICER || kc == KC_SORTED) ? uint64_t(kSliceThreads) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
@@ -854,7 +1036,11 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
-    if (kc == KC_SLICE || kc == KC_SLICER) {
+    if (kc == KC_SORTED) {
+        sm = sorted_smem_bytes(t);
+        cudaFuncSetAttribute(k_eval_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_sorted, kSliceThreads, sm);
+    } else if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         auto kern = t.p64 ? (rnd ? k_eval_slice<true, true> : k_eval_slice<true, false>)
                           : (rnd ? k_eval_slice<false, true> : k_eval_slice<false, false>);
@@ -884,9 +1070,61 @@ cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice 
     if (e != cudaSuccess || r.n_chunks <= 1) return e;
     const int tpb = 256;
     k_reduce_partials<<<int((r.n + tpb - 1) / tpb), tpb, 0, r.stream>>>(r.d_partial, r.n_chunks, r.n, r.d_amp,
-                                                                        r.d_prob, r.prob_mode, r.accumulate);
+                                                                        r.d_prob, r.prob_mode, r.accumulate,
+                                                                        r.d_perm);
     ++*launches;
     return cudaGetLastError();
+}
+
+namespace {
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t cub_sort_temp(uint64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, int64_t(n));
+    return bytes;
+}
+}  // namespace
+
+cudaError_t sorted_max_spread(const uint64_t* d_sorted, uint64_t n, void* d_tmp8, uint64_t* h_out,
+                              cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(d_tmp8, 0, 8, s);
+    if (e != cudaSuccess) return e;
+    const uint64_t groups = (n + kSliceG - 1) / kSliceG;
+    k_max_spread<<<int((groups + 255) / 256), 256, 0, s>>>(d_sorted, n, static_cast<unsigned long long*>(d_tmp8));
+    ++*launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(h_out, d_tmp8, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    return cudaStreamSynchronize(s);
+}
+
+size_t sort_scratch_bytes(uint64_t n) {
+    return 2 * align256(n * 8) + 2 * align256(n * 4) + align256(cub_sort_temp(n));
+}
+
+cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, void* scratch,
+                       const uint64_t** d_sorted, const uint32_t** d_perm, cudaStream_t s, uint64_t* launches) {
+    unsigned char* p = static_cast<unsigned char*>(scratch);
+    uint64_t* keys_in = reinterpret_cast<uint64_t*>(p);
+    p += align256(n * 8);
+    uint64_t* keys_out = reinterpret_cast<uint64_t*>(p);
+    p += align256(n * 8);
+    uint32_t* vals_in = reinterpret_cast<uint32_t*>(p);
+    p += align256(n * 4);
+    uint32_t* vals_out = reinterpret_cast<uint32_t*>(p);
+    p += align256(n * 4);
+    size_t temp = cub_sort_temp(n);
+    const uint64_t mask = n_params >= 64 ? ~uint64_t(0) : ((uint64_t(1) << n_params) - 1);
+    k_mask_iota<<<int((n + 255) / 256), 256, 0, s>>>(d_words, n, mask, keys_in, vals_in);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int end_bit = n_params >= 64 ? 64 : int(n_params > 0 ? n_params : 1);
+    e = cub::DeviceRadixSort::SortPairs(p, temp, keys_in, keys_out, vals_in, vals_out, int64_t(n), 0, end_bit, s);
+    ++*launches;
+    *d_sorted = keys_out;
+    *d_perm = vals_out;
+    return e;
 }
 
 cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int mode, cudaStream_t s,

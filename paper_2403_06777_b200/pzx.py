@@ -298,6 +298,7 @@ KERNEL_GENERAL = 1 << 8
 KERNEL_GRAY = 1 << 9
 KERNEL_SLICE = 1 << 10
 KERNEL_SLICE_RAND = 1 << 11
+KERNEL_SORTED = 1 << 12
 
 
 class DeviceTable:
@@ -493,6 +494,6 @@ __all__ = [
     "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
-    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "slice_op_table",
+    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "slice_op_table",
 ]
 _ = builtins

@@ -131,6 +131,36 @@ def test_slice_rand_kernel_vs_oracle(ctx, P_):
     assert_close(amp, ctx.evaluate_batch(t, words, flags=P.KERNEL_GENERAL), 1e-13)
 
 
+@pytest.mark.parametrize("P_", [12, 20, 30, 32])
+def test_sorted_kernel_vs_oracle(ctx, P_):
+    """Sort + Four-Russians bit-sliced kernel on dense random batches (C3-like)."""
+    e = synth.generate(P_, 500, 1, 40, 700 + P_)
+    t = ctx.compile_bit_table(e)
+    n = min(1 << P_, 1 << 16) + 77                        # ragged tail, duplicates when P_ is small
+    rng = np.random.default_rng(P_)
+    words = rng.integers(0, 2**64, n, dtype=np.uint64)
+    if P_ >= 20:   # dense enough for 32-word groups spanning < 2^16 (density ~1/64 like C3)
+        words = (words & np.uint64((1 << 22) - 1)) | (np.uint64(5) << np.uint64(22 if P_ > 24 else 18))
+    amp = ctx.evaluate_batch(t, words, flags=P.KERNEL_SORTED)
+    idx = rng.choice(n, 64, replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+    assert_close(amp, ctx.evaluate_batch(t, words, flags=P.KERNEL_GENERAL), 1e-13)
+    # auto choice on the same batch agrees
+    assert_close(ctx.evaluate_batch(t, words), amp, 1e-13)
+
+
+def test_sorted_kernel_rejects_sparse_batches(ctx):
+    e = synth.generate(32, 64, 1, 20, 9)
+    t = ctx.compile_bit_table(e)
+    words = np.random.default_rng(3).integers(0, 2**32, 4096, dtype=np.uint64)  # gaps ~2^20
+    with pytest.raises(P.Error):
+        ctx.evaluate_batch(t, words, flags=P.KERNEL_SORTED)
+    # auto falls back to the POPC kernel
+    _, want = O.eval_batch(e, words[:16], 8)
+    assert_close(ctx.evaluate_batch(t, words)[:16], want)
+
+
 def test_random_assignments_mid_size(ctx):
     e = synth.generate(20, 4096, 16, 48, 77)
     t = ctx.compile_bit_table(e)
