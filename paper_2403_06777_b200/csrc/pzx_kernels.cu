@@ -1009,7 +1009,7 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
     // arbitrary word lists: sort, then the bit-sliced kernel with per-thread
     // Four-Russians tables (needs n_params <= 32 and terms <= 127 rows)
-    if (t.sorted_ok && r.n >= uint64_t(kSliceG)) return KC_SORTED;
+    if (t.sorted_ok && r.d_asg && !r.words_contiguous && r.n >= uint64_t(kSliceG)) return KC_SORTED;
     return KC_GENERAL;
 }
 
@@ -1017,7 +1017,7 @@ bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
     if (kc == KC_SLICER) return t.slice_ok != 0;
-    if (kc == KC_SORTED) return t.sorted_ok != 0;
+    if (kc == KC_SORTED) return t.sorted_ok != 0 && r.d_asg != nullptr;
     if (kc == KC_GRAY) return enumerated && (r.first % kGray) == 0;
     return true;
 }
