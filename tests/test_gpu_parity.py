@@ -139,8 +139,10 @@ def test_sorted_kernel_vs_oracle(ctx, P_):
     n = min(1 << P_, 1 << 16) + 77                        # ragged tail, duplicates when P_ is small
     rng = np.random.default_rng(P_)
     words = rng.integers(0, 2**64, n, dtype=np.uint64)
-    if P_ >= 20:   # dense enough for 32-word groups spanning < 2^16 (density ~1/64 like C3)
-        words = (words & np.uint64((1 << 22) - 1)) | (np.uint64(5) << np.uint64(22 if P_ > 24 else 18))
+    if P_ >= 20:   # a dense window (density ~1/64 like C3): 32-word groups span < 2^16
+        lo = 1 << (P_ - 3)
+        words = np.uint64(lo) + (words & np.uint64((1 << min(22, P_ - 3)) - 1))
+        words |= np.uint64(7) << np.uint64(P_ + 3)  # bits above n_params must be ignored
     amp = ctx.evaluate_batch(t, words, flags=P.KERNEL_SORTED)
     idx = rng.choice(n, 64, replace=False)
     _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
