@@ -491,27 +491,47 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
     }
     const bool kinds = (nS | nA | nB) != 0;
     uint32_t alive = ~Z;
-    if (kinds && nS < 8 && nA < 4 && nB < 4) {
+    // two live assignments per iteration: independent chains for latency hiding
+    auto add2 = [&](auto value_of) {
+        while (alive) {
+            const int g1 = 31 - __clz(alive);
+            alive ^= 1u << g1;
+            const bool two = alive != 0;
+            const int g2 = two ? 31 - __clz(alive) : g1;
+            if (two) alive ^= 1u << g2;
+            const double2 v1 = value_of(g1), v2 = value_of(g2);
+            double2* a1 = amp_s + g1 * kSliceThreads + threadIdx.x;
+            double2* a2 = amp_s + g2 * kSliceThreads + threadIdx.x;
+            double2 o1 = *a1;
+            o1.x += v1.x;
+            o1.y += v1.y;
+            *a1 = o1;
+            if (two) {
+                double2 o2 = *a2;
+                o2.x += v2.x;
+                o2.y += v2.y;
+                *a2 = o2;
+            }
+        }
+    };
+    auto jof = [&](int g) {
+        return ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+    };
+    if (!kinds) {
+        add2([&](int g) { return crot[jof(g)]; });
+    } else if (nS < 8 && nA < 4 && nB < 4) {
         // fast path: s1 < 8 and a, b < 4 -> fixed-width decode, one
         // real (sqrt2-1)^s1 and one complex pi^a pi'^b table lookup
-        while (alive) {
-            const int g = 31 - __clz(alive);
-            alive ^= 1u << g;
-            const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+        add2([&](int g) {
             const uint32_t s1 = ((S[0] >> g) & 1u) | (((S[1] >> g) & 1u) << 1) | (((S[2] >> g) & 1u) << 2);
             const uint32_t ab = ((A[0] >> g) & 1u) | (((A[1] >> g) & 1u) << 1) |
                                 (((B[0] >> g) & 1u) << 2) | (((B[1] >> g) & 1u) << 3);
-            const double2 cj = crot[j];
+            const double2 cj = crot[jof(g)];
             const double2 f = L.ab[ab];
             const double rr = L.u[s1];
             const double fr = f.x * rr, fi = f.y * rr;
-            double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
-            double2 o = *ap;
-            o.x += cj.x * fr - cj.y * fi;
-            o.y += cj.x * fi + cj.y * fr;
-            *ap = o;
-        }
-        alive = 0;
+            return make_double2(cj.x * fr - cj.y * fi, cj.x * fi + cj.y * fr);
+        });
     }
     while (alive) {
         const int g = __ffs(alive) - 1;
