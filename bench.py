@@ -319,10 +319,14 @@ def run_ours(args):
                 cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                        "sample": f"failed: {ex}"}
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        traffic = None
+        traffic, ncu_info = None, None
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.config)
+                ncu_info = json.load(f).get(args.config)
+            if ncu_info and args.kernel == "auto":
+                traffic = ncu_info["dram_bytes_per_launch"]
+            else:
+                ncu_info = None
         except Exception:
             pass
         line = {
@@ -343,7 +347,11 @@ def run_ours(args):
                          "peak_source": f"148 SM x 64 int32 lanes/clk x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
                                         "MEASURED_PEAKS.json clock; lane rate from the CUDA throughput table)",
                          "work_per_launch": work, "row_evals_per_s": row_evals,
-                         "hbm_gbs_if_table_streamed_once": table_bytes / (mean_ms / 1e3) / 1e9},
+                         "hbm_gbs_if_table_streamed_once": table_bytes / (mean_ms / 1e3) / 1e9,
+                         "ncu": None if ncu_info is None else {
+                             "issue_active_pct": ncu_info["issue_active_pct"],
+                             "warp_instructions_per_row_eval": ncu_info["warp_instructions"] / (N * R),
+                             "source": ncu_info["source"]}},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "step_ms": step_ms,

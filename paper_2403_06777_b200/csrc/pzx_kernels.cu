@@ -688,16 +688,10 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
             const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
-            // software-pipelined: the next row's record is loaded before this
-            // row's dispatch (the read past the last row stays inside shared
-            // memory and is never used)
-            uint4 na = lds128(a0), nb = lds128(a0 + 16);
             for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint4 ra = na;  // psi, phi, code, Walsh32(psi)
-                const uint4 rb = nb;  // Walsh32(phi), psi_hi, phi_hi, 0
-                na = lds128(ad + 32);
-                nb = lds128(ad + 48);
-                const uint32_t op = ra.z & 0xFFu;
+                const uint4 ra = lds128(ad);       // psi, phi, code, Walsh32(psi)
+                const uint4 rb = lds128(ad + 16);  // Walsh32(phi), psi_hi, phi_hi, 0
+                const uint32_t op = __shfl_sync(0xFFFFFFFFu, ra.z, 0) & 0xFFu;  // provably warp-uniform -> BRXU
                 uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
                 if constexpr (RAND) {
                     uint32_t X = planes_parity(ra.x, planes_s), Y = 0;
