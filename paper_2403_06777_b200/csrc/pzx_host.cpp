@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <thread>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -157,42 +160,53 @@ struct HostTable {
     std::vector<uint4> qrows;               // sorted-batch kernel rows (2 per row, n_params <= 32)
     std::vector<double> sterm_c;            // its term constants (2 per term)
     int jb_term = 0;                        // running sum of slice jbase in the open term
+    bool want_slice = true;                 // build the bit-sliced layouts (srows / qrows)
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
     uint32_t max_rows = 0;
 };
 
-uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
-    uint32_t pat = 0;
-    for (int g = 0; g < kGray; ++g) {
-        pat |= uint32_t(__builtin_parityll(psi & uint64_t(g))) << (2 * g);
-        pat |= uint32_t(__builtin_parityll(phi & uint64_t(g))) << (2 * g + 1);
+// Walsh patterns depend only on the low mask bits: tabulated once.
+struct WalshTables {
+    uint32_t w16[16][2];  // interleaved 2-bit pattern contribution of psi (slot 0) / phi (slot 1)
+    uint32_t w32[32];     // bit g = parity(m & g), g < 32
+    WalshTables() {
+        for (int m = 0; m < 16; ++m) {
+            uint32_t a = 0, b = 0;
+            for (int g = 0; g < kGray; ++g) {
+                a |= uint32_t(__builtin_parity(unsigned(m & g))) << (2 * g);
+                b |= uint32_t(__builtin_parity(unsigned(m & g))) << (2 * g + 1);
+            }
+            w16[m][0] = a;
+            w16[m][1] = b;
+        }
+        for (int m = 0; m < 32; ++m) {
+            uint32_t w = 0;
+            for (int g = 0; g < 32; ++g) w |= uint32_t(__builtin_parity(unsigned(m & g))) << g;
+            w32[m] = w;
+        }
     }
-    return pat;
+};
+const WalshTables& walsh() {
+    static const WalshTables t;
+    return t;
 }
 
-uint32_t walsh32(uint64_t m) {
-    uint32_t w = 0;
-    for (int g = 0; g < 32; ++g) w |= uint32_t(__builtin_parityll(m & uint64_t(g))) << g;
-    return w;
+uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
+    return walsh().w16[psi & 15][0] | walsh().w16[phi & 15][1];
+}
+
+uint32_t walsh32(uint64_t m) { return walsh().w32[m & 31]; }
+
+// PZX_LAYOUTS=base keeps only the base row layout (POPC / gray kernels) --
+// for tables too large to hold the bit-sliced copies as well
+bool layouts_base_only() {
+    const char* e = std::getenv("PZX_LAYOUTS");
+    return e && std::string(e) == "base";
 }
 
 void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, uint32_t pat, uint8_t sw,
                      uint8_t unit) {
-    const uint32_t cls = (code & kCodeMask) >> 4;
-    const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
-    h.jb_term += kSliceJbase[op];
-    h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), op | uint32_t(kSliceKindFlags[op]), walsh32(psi)));
-    h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
-    if (h.n_params <= 32) {
-        auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)
-            return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * kSortedTableStride);
-        };
-        const uint32_t code = op | uint32_t(kSliceKindFlags[op]);
-        h.qrows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, 0));
-        h.qrows.push_back(make_uint4(offs(psi, 0) | (offs(psi, 1) << 16), offs(psi, 2) | (offs(psi, 3) << 16),
-                                     offs(phi, 0) | (offs(phi, 1) << 16), offs(phi, 2) | (offs(phi, 3) << 16)));
-    }
     if (h.n_params <= 32) {
         h.rows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), code, pat));
     } else {  // 32-byte record: masks, then {code, pattern}
@@ -201,6 +215,21 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     }
     h.swapped.push_back(sw);
     h.unit.push_back(unit);
+    const uint32_t cls = (code & kCodeMask) >> 4;
+    const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
+    h.jb_term += kSliceJbase[op];
+    if (!h.want_slice) return;
+    const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
+    h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
+    h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
+    if (h.n_params <= 32) {
+        auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)
+            return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * kSortedTableStride);
+        };
+        h.qrows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, 0));
+        h.qrows.push_back(make_uint4(offs(psi, 0) | (offs(psi, 1) << 16), offs(psi, 2) | (offs(psi, 3) << 16),
+                                     offs(phi, 0) | (offs(phi, 1) << 16), offs(phi, 2) | (offs(phi, 3) << 16)));
+    }
 }
 
 void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
@@ -233,7 +262,7 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
     for (uint64_t i = 0; i + 1 < n_rows_term; ++i)
         if ((i + 1) % kSegRows == 0) code_word(h, row0 + i) |= kSegFlag;
     code_word(h, row0 + n_rows_term - 1) |= kEndFlag;
-    h.srows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
+    if (!h.srows.empty()) h.srows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
     if (!h.qrows.empty()) h.qrows[2 * (row0 + n_rows_term - 1)].z |= kEndFlag;
     h.max_rows = std::max<uint32_t>(h.max_rows, uint32_t(n_rows_term));
     h.coef.push_back(c);
@@ -264,11 +293,11 @@ bool canon_input(const int64_t* q, Quad& out) {
     return quad_canon(q[0], q[1], q[2], q[3], q[4], out);
 }
 
-int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
-    if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
+int compile_expr_range(const pzx_expr_view* v, uint64_t t_begin, uint64_t t_end, HostTable& h,
+                       std::string& err) {
     h.n_params = v->n_params;
     const uint64_t allowed = param_mask(v->n_params);
-    for (uint64_t t = 0; t < v->n_terms; ++t) {
+    for (uint64_t t = t_begin; t < t_end; ++t) {
         Quad c;
         if (!canon_input(v->term_scalar + 5 * t, c)) { err = "term scalar out of range"; return PZX_E_OVERFLOW; }
         int e = 0, lm = 0;
@@ -294,6 +323,55 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
         int st = finish_term(h, c, e, lm, row0);
         if (st) { err = "term has more rows than supported"; return st; }
     }
+    return PZX_OK;
+}
+
+// Append part (compiled with term_row starting at 0) to h.
+void merge_into(HostTable& h, HostTable& part) {
+    const uint64_t base = h.n_dev_rows();
+    for (size_t i = 1; i < part.term_row.size(); ++i) h.term_row.push_back(base + part.term_row[i]);
+    auto app = [](auto& dst, auto& src) {
+        dst.insert(dst.end(), src.begin(), src.end());
+        std::vector<typename std::decay_t<decltype(src)>::value_type>().swap(src);
+    };
+    app(h.coef, part.coef);
+    app(h.e_t, part.e_t);
+    app(h.nlm_t, part.nlm_t);
+    app(h.term_c, part.term_c);
+    app(h.sterm_c, part.sterm_c);
+    app(h.rows, part.rows);
+    app(h.srows, part.srows);
+    app(h.qrows, part.qrows);
+    app(h.swapped, part.swapped);
+    app(h.unit, part.unit);
+    h.max_rows = std::max(h.max_rows, part.max_rows);
+}
+
+// compile_bit_table over term ranges in parallel (terms are independent),
+// merged in term order: the table is identical to a serial compile.
+int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
+    if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
+    h.n_params = v->n_params;
+    const uint64_t m = v->n_terms;
+    const uint64_t rows_est = m ? v->term_offset[m] - v->term_offset[0] + m : 0;
+    h.want_slice = rows_est <= (uint64_t(1) << 28) && !layouts_base_only();
+    unsigned nth = std::max(1u, std::thread::hardware_concurrency());
+    nth = unsigned(std::min<uint64_t>(nth, std::max<uint64_t>(1, m / 2048)));
+    if (nth <= 1) return compile_expr_range(v, 0, m, h, err);
+    std::vector<HostTable> parts(nth);
+    std::vector<int> st(nth, PZX_OK);
+    std::vector<std::string> errs(nth);
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nth; ++i) {
+        parts[i].want_slice = h.want_slice;
+        th.emplace_back([&, i] {
+            st[i] = compile_expr_range(v, m * i / nth, m * (i + 1) / nth, parts[i], errs[i]);
+        });
+    }
+    for (auto& x : th) x.join();
+    for (unsigned i = 0; i < nth; ++i)
+        if (st[i]) { err = errs[i]; return st[i]; }
+    for (unsigned i = 0; i < nth; ++i) merge_into(h, parts[i]);
     return PZX_OK;
 }
 
@@ -445,7 +523,7 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     if ((st = cuda_err(ctx, upload_vec(&t->d_rows, h.rows), "upload rows"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_row, h.term_row), "upload term offsets"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_c, h.term_c), "upload term constants"))) return st;
-    const bool slice_ok = h.max_rows <= uint32_t(kSegRows) && slice_tables_ok();
+    const bool slice_ok = h.want_slice && h.max_rows <= uint32_t(kSegRows) && slice_tables_ok();
     if (slice_ok) {
         if ((st = cuda_err(ctx, upload_vec(&t->d_srows, h.srows), "upload slice rows"))) return st;
         if ((st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
@@ -473,6 +551,12 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     d.qrows = static_cast<const uint4*>(t->d_qrows);
     t->ctx = ctx;
     t->device = ctx->device;
+    // the device owns the row layouts now; keep only what host-side queries use
+    std::vector<uint4>().swap(h.rows);
+    std::vector<uint4>().swap(h.srows);
+    std::vector<uint4>().swap(h.qrows);
+    std::vector<double>().swap(h.term_c);
+    std::vector<double>().swap(h.sterm_c);
     *out = t.release();
     return PZX_OK;
 }
