@@ -617,7 +617,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
     constexpr int kWaves = 8;
-    const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc);
+    const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc, slice_threads(r));
     const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;

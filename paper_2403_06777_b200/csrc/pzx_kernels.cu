@@ -470,6 +470,7 @@ __host__ __device__ constexpr uint32_t slice_lut_offset() {
 // Term epilogue shared by the bit-sliced kernels: fold 6*s1 into J, build
 // the warp's C * w^j table, and add every live assignment's term value into its
 // fp64 accumulator; resets the per-term state.
+template <int NT>
 __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemLut& L, double2* crot,
                                                     double2* amp_s, uint32_t& J0, uint32_t& J1,
                                                     uint32_t& J2, uint32_t& Z, uint32_t (&S)[kPlanes],
@@ -500,8 +501,8 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
             const int g2 = two ? 31 - __clz(alive) : g1;
             if (two) alive ^= 1u << g2;
             const double2 v1 = value_of(g1), v2 = value_of(g2);
-            double2* a1 = amp_s + g1 * kSliceThreads + threadIdx.x;
-            double2* a2 = amp_s + g2 * kSliceThreads + threadIdx.x;
+            double2* a1 = amp_s + g1 * NT + threadIdx.x;
+            double2* a2 = amp_s + g2 * NT + threadIdx.x;
             double2 o1 = *a1;
             o1.x += v1.x;
             o1.y += v1.y;
@@ -554,7 +555,7 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
             v.x *= rr;
             v.y *= rr;
         }
-        double2* ap = amp_s + g * kSliceThreads + threadIdx.x;
+        double2* ap = amp_s + g * NT + threadIdx.x;
         double2 o = *ap;
         o.x += v.x;
         o.y += v.y;
@@ -570,11 +571,11 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
 
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
-template <bool P64, bool RAND>
+template <bool P64, bool RAND, int NT>
 size_t slice_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
-    const size_t planes = RAND ? size_t(P64 ? 64 : 32) * kSliceThreads * 4 : 0;
-    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16 + planes;
+    const size_t planes = RAND ? size_t(P64 ? 64 : 32) * NT * 4 : 0;
+    return amp_off + size_t(kSliceG) * NT * 16 + (NT / 32) * 8 * 16 + planes;
 }
 
 // 32 x 32 bit-matrix transpose: afterwards a[i] bit g = (old a[g]) bit i.
@@ -595,13 +596,14 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
 }
 
 // X = XOR of the planes of the parameters set in mask (uniform loop over set bits)
+template <int NT>
 __device__ __forceinline__ uint32_t planes_parity(uint32_t mask, uint32_t plane_addr) {
     uint32_t x = 0;
     while (mask) {
         const int i = __ffs(mask) - 1;
         mask &= mask - 1;
         uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(plane_addr + uint32_t(i) * (kSliceThreads * 4)));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(plane_addr + uint32_t(i) * (NT * 4)));
         x ^= v;
     }
     return x;
@@ -618,24 +620,24 @@ __device__ __forceinline__ uint32_t planes_parity(uint32_t mask, uint32_t plane_
 // table C * w^j (8 entries) is built once per warp, then every live
 // assignment adds C * w^j' * (stuff from S, A, B) into its fp64 accumulator in
 // shared memory.
-template <bool P64, bool RAND>
-__global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, const LaunchReq r) {
+template <bool P64, bool RAND, int NT>
+__global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const LaunchReq r) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemLut L = kernel_prologue(t, smem, slice_lut_offset<P64>());
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
-    double2* crot = amp_s + kSliceG * kSliceThreads + (threadIdx.x >> 5) * 8;
+    double2* crot = amp_s + kSliceG * NT + (threadIdx.x >> 5) * 8;
 #pragma unroll
-    for (int g = 0; g < kSliceG; ++g) amp_s[g * kSliceThreads + threadIdx.x] = make_double2(0.0, 0.0);
+    for (int g = 0; g < kSliceG; ++g) amp_s[g * NT + threadIdx.x] = make_double2(0.0, 0.0);
 
     uint64_t tb, te;
     term_range(r, tb, te);
-    const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
+    const uint64_t off = (uint64_t(blockIdx.x) * NT + threadIdx.x) * kSliceG;
     uint64_t base = 0;
     uint32_t planes_s = 0;  // shared address of this thread's plane 0 (RAND)
     if constexpr (RAND) {
         // thread owns the 32 arbitrary words off .. off+31: transpose into planes
-        uint32_t* planes = reinterpret_cast<uint32_t*>(crot + (kSliceThreads / 32 - (threadIdx.x >> 5)) * 8);
+        uint32_t* planes = reinterpret_cast<uint32_t*>(crot + (NT / 32 - (threadIdx.x >> 5)) * 8);
         planes_s = smem_u32(planes) + threadIdx.x * 4;
         uint32_t w[32];
 #pragma unroll
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
             }
             transpose32(w);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) planes[(32 * h + i) * kSliceThreads + threadIdx.x] = w[i];
+            for (int i = 0; i < 32; ++i) planes[(32 * h + i) * NT + threadIdx.x] = w[i];
         }
     } else {
         base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
@@ -694,11 +696,11 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                 const uint32_t op = __shfl_sync(0xFFFFFFFFu, ra.z, 0) & 0xFFu;  // provably warp-uniform -> BRXU
                 uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
                 if constexpr (RAND) {
-                    uint32_t X = planes_parity(ra.x, planes_s), Y = 0;
-                    if (ra.y) Y = planes_parity(ra.y, planes_s);
+                    uint32_t X = planes_parity<NT>(ra.x, planes_s), Y = 0;
+                    if (ra.y) Y = planes_parity<NT>(ra.y, planes_s);
                     if constexpr (P64) {
-                        X ^= planes_parity(rb.y, planes_s + 32 * kSliceThreads * 4);
-                        if (rb.z) Y ^= planes_parity(rb.z, planes_s + 32 * kSliceThreads * 4);
+                        X ^= planes_parity<NT>(rb.y, planes_s + 32 * NT * 4);
+                        if (rb.z) Y ^= planes_parity<NT>(rb.z, planes_s + 32 * NT * 4);
                     }
                     asm(PZX_SLICE_DISPATCH_ASM_XY
                         : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
@@ -723,7 +725,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
                     if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
                     if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
                     if (ra.z & kEndFlag) {
-                        slice_term_epilogue(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
+                        slice_term_epilogue<NT>(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
                         C = Cn;
                         ++term;
                         Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_slice(const DevTable t, 
         }
     }
 #pragma unroll 4
-    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
+    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * NT + threadIdx.x]);
 }
 
 // ------------------------------------------------------ sorted kernel ----
@@ -864,7 +866,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t,
                     if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
                     if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
                     if (ra.z & kEndFlag) {
-                        slice_term_epilogue(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
+                        slice_term_epilogue<kSliceThreads>(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
                         C = Cn;
                         ++term;
                         Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
@@ -1000,11 +1002,14 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
     }
     if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
-        const size_t sm = rnd ? slice_smem_bytes<P64, true>(t) : slice_smem_bytes<P64, false>(t);
-        auto kern = rnd ? k_eval_slice<P64, true> : k_eval_slice<P64, false>;
+        const bool small = slice_threads(r) == 32;
+        const size_t sm = rnd ? (small ? slice_smem_bytes<P64, true, 32>(t) : slice_smem_bytes<P64, true, 128>(t))
+                              : (small ? slice_smem_bytes<P64, false, 32>(t) : slice_smem_bytes<P64, false, 128>(t));
+        auto kern = rnd ? (small ? k_eval_slice<P64, true, 32> : k_eval_slice<P64, true, 128>)
+                        : (small ? k_eval_slice<P64, false, 32> : k_eval_slice<P64, false, 128>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
-        kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        kern<<<grid, small ? 32 : 128, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     const size_t sm = smem_lut_offset<P64>() + t.lut_layout.bytes;
@@ -1036,15 +1041,22 @@ bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     return true;
 }
 
+// bit-sliced kernels: 32-thread CTAs when the batch cannot give every SM a
+// 128-thread block (small enumerated batches with huge tables, e.g. C4)
+int slice_threads(const LaunchReq& r) {
+    return r.n < uint64_t(kSliceThreads) * kSliceG * 148 ? 32 : kSliceThreads;
+}
+
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = (kc == KC_SLICE || kc == KC_SLICER || kc == KC_SORTED) ? uint64_t(kSliceThreads) * kSliceG
+    const uint64_t per = kc == KC_SORTED                   ? uint64_t(kSliceThreads) * kSliceG
+                       : (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(slice_threads(r)) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
 }
 
 
-int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
+int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
     const bool lng = t.max_rows > uint32_t(kSegRows);
     int nb = 0;
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
@@ -1056,12 +1068,21 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_sorted, kSliceThreads, sm);
     } else if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
-        auto kern = t.p64 ? (rnd ? k_eval_slice<true, true> : k_eval_slice<true, false>)
-                          : (rnd ? k_eval_slice<false, true> : k_eval_slice<false, false>);
-        sm = t.p64 ? (rnd ? slice_smem_bytes<true, true>(t) : slice_smem_bytes<true, false>(t))
-                   : (rnd ? slice_smem_bytes<false, true>(t) : slice_smem_bytes<false, false>(t));
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+        if (nt == 32) {
+            auto kern = t.p64 ? (rnd ? k_eval_slice<true, true, 32> : k_eval_slice<true, false, 32>)
+                              : (rnd ? k_eval_slice<false, true, 32> : k_eval_slice<false, false, 32>);
+            sm = t.p64 ? (rnd ? slice_smem_bytes<true, true, 32>(t) : slice_smem_bytes<true, false, 32>(t))
+                       : (rnd ? slice_smem_bytes<false, true, 32>(t) : slice_smem_bytes<false, false, 32>(t));
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, sm);
+        } else {
+            auto kern = t.p64 ? (rnd ? k_eval_slice<true, true, 128> : k_eval_slice<true, false, 128>)
+                              : (rnd ? k_eval_slice<false, true, 128> : k_eval_slice<false, false, 128>);
+            sm = t.p64 ? (rnd ? slice_smem_bytes<true, true, 128>(t) : slice_smem_bytes<true, false, 128>(t))
+                       : (rnd ? slice_smem_bytes<false, true, 128>(t) : slice_smem_bytes<false, false, 128>(t));
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, sm);
+        }
     } else if (kc == KC_GRAY) {
         if (t.p64) { if (lng) PZX_OCC((k_eval_gray<true, kGrayBits, true>)); else PZX_OCC((k_eval_gray<true, kGrayBits, false>)); }
         else { if (lng) PZX_OCC((k_eval_gray<false, kGrayBits, true>)); else PZX_OCC((k_eval_gray<false, kGrayBits, false>)); }

@@ -11,7 +11,9 @@ tables are synthetic with the statistics SURVEY §8(d) fixes:
   never empty (an all-empty subterm would have been folded by push_subterm,
   diagram.cpp:114-120);
 * n_t ~ U[n_lo, n_hi] subterms per term;
-* C_t = RingQuad::make(U[-8, 8]^4, exp = n_t), never zero;
+* C_t = RingQuad::make(U[-8, 8]^4, exp = n_t), never zero (C3-C5 cap exp at 40:
+  the reference's ring_add throws when term exponents differ by > 62,
+  ring.cpp:61-63, which long terms would otherwise hit);
 * bit generator MT19937 seeded with 20261018 + config id.
 
 Everything is plain numpy; the same arrays feed the GPU path and both CPU
@@ -38,15 +40,17 @@ class Config:
     enumerated: bool
     prob_real: bool = False
     mix: str = "general"
+    exp_cap: int | None = None  # cap on the scalar's 2^-exp: keeps the reference's int64 ring_add in range
 
 
 CONFIGS = {
     "c1": Config(1, "C1: P=8, all 2^8 amplitudes (8 qubits, T=20)", 8, 1 << 10, 8, 24, 1 << 8, True),
     "c2": Config(2, "C2: P=20, all 2^20 amplitudes (20 qubits, T=40)", 20, 1 << 17, 16, 48, 1 << 20, True),
-    "c3": Config(3, "C3: P=30, 2^24 sampled probabilities (30 qubits, T=60)", 30, 1 << 18, 24, 56, 1 << 24, False),
+    "c3": Config(3, "C3: P=30, 2^24 sampled probabilities (30 qubits, T=60)", 30, 1 << 18, 24, 56, 1 << 24, False,
+                 exp_cap=40),
     "c4": Config(4, "C4: P=10 doubled-diagram marginals, 2^10 params (term split)", 10, 1 << 22, 32, 64, 1 << 10,
-                 True, prob_real=True),
-    "c5": Config(5, "C5: P=32, T>=100 term-split table (> L2)", 32, 1 << 24, 32, 64, 1 << 16, False),
+                 True, prob_real=True, exp_cap=40),
+    "c5": Config(5, "C5: P=32, T>=100 term-split table (> L2)", 32, 1 << 24, 32, 64, 1 << 16, False, exp_cap=40),
 }
 
 KIND_P = (0.2, 0.1, 0.2, 0.5)  # Node, PhasePair, HalfPi, PiPair  (SubtermKind order)
@@ -110,7 +114,7 @@ def generate(n_params: int, n_terms: int, n_lo: int, n_hi: int, seed: int, mix: 
 
 def generate_config(cfg: Config, n_terms: int | None = None) -> ScalarExpression:
     return generate(cfg.n_params, cfg.n_terms if n_terms is None else n_terms, cfg.n_lo, cfg.n_hi,
-                    20261018 + cfg.cid, cfg.mix)
+                    20261018 + cfg.cid, cfg.mix, exp_cap=cfg.exp_cap)
 
 
 def assignments(cfg: Config, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
