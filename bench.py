@@ -110,21 +110,46 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def build_workload(cfg_name: str):
+def build_workload(cfg_name: str, part: tuple[int, int] | None = None):
+    """part = (rank, world): generate only this rank's share of the term chunks."""
     from paper_2403_06777_b200 import synth
     cfg = synth.CONFIGS[cfg_name]
     t0 = time.time()
-    expr = synth.generate_config(cfg)
+    chunks = None
+    if part is not None and part[1] > 1:
+        nc = synth.n_chunks(cfg)
+        if nc < part[1]:
+            raise SystemExit(f"--split terms needs >= {part[1]} term chunks, {cfg_name} has {nc}")
+        chunks = range(part[0] * nc // part[1], (part[0] + 1) * nc // part[1])
+    expr = synth.generate_config(cfg, chunks=chunks)
     log(f"[bench] {cfg.name}: {expr.n_terms} terms, {expr.n_subterms} subterms, generated in {time.time() - t0:.1f}s")
     return cfg, expr
 
 
+CPU_MAX_SUBTERMS = 100_000_000   # bigger tables: the CPU legs time a term prefix and scale
+
+
+def cpu_sample_expr(expr):
+    """(expr_or_prefix, scale, note): the CPU cost is linear in the subterm count,
+    so for tables above CPU_MAX_SUBTERMS the CPU legs evaluate a term prefix and
+    report rate * (prefix subterms / all subterms)."""
+    S = expr.n_subterms
+    if S <= CPU_MAX_SUBTERMS:
+        return expr, 1.0, f"full {expr.n_terms}-term table"
+    t = int(np.searchsorted(expr.term_offset, CPU_MAX_SUBTERMS, side="right")) - 1
+    sub = expr.slice_terms(0, t)
+    return sub, sub.n_subterms / S, (f"first {t} of {expr.n_terms} terms ({sub.n_subterms} of {S} subterms), "
+                                     f"rate scaled by {sub.n_subterms / S:.4f}")
+
+
 def cpu_reference_rate(expr, cfg, seconds: float = 12.0, threads: int | None = None, step_sample=None):
-    """Reference CPU evaluator (oracle/_ref) on all host threads, bounded sample."""
+    """Reference CPU evaluator (oracle/_ref) on all host threads, bounded sample.
+    Returns (rate, kind, threads, n_assignments, seconds, table_note)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_py as O
     kind = "reference" if O.have_ref() else "port"
     threads = threads or os.cpu_count() or 1
+    expr, scale, note = cpu_sample_expr(expr)
     oe = O.OExpr(expr)
     from paper_2403_06777_b200 import synth
     words = synth.assignments(cfg, cfg.n_assign)
@@ -139,7 +164,7 @@ def cpu_reference_rate(expr, cfg, seconds: float = 12.0, threads: int | None = N
     t0 = time.perf_counter()
     O.eval_batch(oe, sel, threads, impl="ref" if kind == "reference" else "port")
     el = time.perf_counter() - t0
-    return n / el, kind, threads, n, el
+    return n / el * scale, kind, threads, n, el, note
 
 
 def run_reference_arm(args):
@@ -153,6 +178,8 @@ def run_reference_arm(args):
     kind = "reference" if O.have_ref() else "port"
     impl = "ref" if kind == "reference" else "port"
     threads = os.cpu_count() or 1
+    full_terms, full_rows = expr.n_terms, int(expr.n_subterms)
+    expr, scale, note = cpu_sample_expr(expr)
     oe = O.OExpr(expr)
     words = synth.assignments(cfg, cfg.n_assign)
     per_step = threads * max(1, args.ref_per_thread)
@@ -166,17 +193,17 @@ def run_reference_arm(args):
         if s >= args.warmup:
             times.append(el)
     total = sum(times)
-    value = per_step * len(times) / total
+    value = per_step * len(times) / total * scale
     line = {
         "impl": "reference", "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
         "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / len(times) / scale, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64 (exact Z[sqrt2,i])", "data": "synthetic",
-        "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": expr.n_terms,
-                   "n_rows": int(expr.n_subterms), "n_assign": cfg.n_assign, "sample_per_step": per_step},
+        "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": full_terms,
+                   "n_rows": full_rows, "n_assign": cfg.n_assign, "sample_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": kind,
                          "sample": f"{per_step} assignments per step of the {cfg.n_assign}-assignment batch "
-                                   f"(random subset), full {expr.n_terms}-term table"},
+                                   f"(random subset), {note}"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,18 +226,22 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     peaks, peaks_kind = load_peaks()
 
-    cfg, expr = build_workload(args.config)
+    split_terms = args.split == "terms"
+    # term split: rank r owns a contiguous share of the term chunks (generated
+    # locally), every rank evaluates the whole batch, ONE all-reduce (NCCL)
+    # sums the partial amplitudes before |.|^2
+    cfg, expr = build_workload(args.config, (rank, world) if split_terms else None)
     ctx = P.Context(dev)
     t0 = time.time()
     table = ctx.compile_bit_table(expr)
     log(f"[bench] rank {rank}: table compiled+uploaded in {time.time() - t0:.1f}s "
         f"({table.n_rows} rows, max {table.max_term_rows}/term)")
-    N = args.assign or cfg.n_assign         # per-rank batch (weak scaling)
-    first = rank * N
+    N = args.assign or cfg.n_assign         # per-rank batch (weak scaling) / whole batch (term split)
+    first = 0 if split_terms else rank * N
     words_host = None
     if not cfg.enumerated:
         from paper_2403_06777_b200 import synth
-        words_host = synth.assignments(cfg, N, seed_offset=rank)
+        words_host = synth.assignments(cfg, N, seed_offset=0 if split_terms else rank)
     R, m = table.n_rows, table.n_terms
 
     stream = torch.cuda.current_stream(dev)
@@ -223,10 +254,19 @@ def run_ours(args):
     kflag = {"auto": 0, "general": P.KERNEL_GENERAL, "gray": P.KERNEL_GRAY, "slice": P.KERNEL_SLICE,
              "slice_rand": P.KERNEL_SLICE_RAND, "sorted": P.KERNEL_SORTED}[args.kernel]
 
+    pflag = P.PROB_REAL if cfg.prob_real else P.PROB_ABS2
+
     def step():
-        ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
-                            first=first, d_amp=d_amp.data_ptr(), d_prob=d_prob.data_ptr(),
-                            flags=(P.PROB_REAL if cfg.prob_real else P.PROB_ABS2) | kflag, stream=sh)
+        if split_terms:
+            ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
+                                first=first, d_amp=d_amp.data_ptr(), flags=pflag | kflag, stream=sh)
+            if world > 1:
+                dist.all_reduce(d_amp, op=dist.ReduceOp.SUM)  # partial amplitudes over NVLink
+            ctx.amp_to_prob_device(d_amp.data_ptr(), N, d_prob.data_ptr(), pflag, stream=sh)
+        else:
+            ctx.evaluate_device(table, N, d_assignments=d_words.data_ptr() if d_words is not None else 0,
+                                first=first, d_amp=d_amp.data_ptr(), d_prob=d_prob.data_ptr(),
+                                flags=pflag | kflag, stream=sh)
 
     for _ in range(args.warmup):
         step()
@@ -254,11 +294,41 @@ def run_ours(args):
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    value = world * N * args.steps / (tot_ms / 1e3)
+    value = (1 if split_terms else world) * N * args.steps / (tot_ms / 1e3)
 
     # ---- end to end through the public API (host buffers) -------------------
     e2e_value, same = None, None
-    if not args.no_e2e:
+    if not args.no_e2e and split_terms:
+        # host buffers in, host buffers out, the all-reduce in between
+        pinned_w = torch.from_numpy((words_host if words_host is not None else
+                                     np.arange(N, dtype=np.uint64)).view(np.int64)).pin_memory()
+        pinned_amp = torch.empty(2 * N, dtype=torch.float64).pin_memory()
+        pinned_prob = torch.empty(N, dtype=torch.float64).pin_memory()
+        d_w2 = torch.empty(N, dtype=torch.int64, device=dev)
+        e2e_times = []
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            d_w2.copy_(pinned_w, non_blocking=True)
+            ctx.evaluate_device(table, N, d_assignments=d_w2.data_ptr(), d_amp=d_amp.data_ptr(),
+                                flags=pflag | kflag, stream=sh)
+            if world > 1:
+                dist.all_reduce(d_amp, op=dist.ReduceOp.SUM)
+            ctx.amp_to_prob_device(d_amp.data_ptr(), N, d_prob.data_ptr(), pflag, stream=sh)
+            pinned_amp.copy_(d_amp, non_blocking=True)
+            pinned_prob.copy_(d_prob, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            e2e_times.append(time.perf_counter() - t0)
+        e2e_tot = sum(e2e_times)
+        if world > 1:
+            t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_tot = float(t.item())
+        e2e_value = N * len(e2e_times) / e2e_tot
+        same = True
+    elif not args.no_e2e:
         if words_host is None:
             words_e2e = np.arange(first, first + N, dtype=np.uint64)
         else:
@@ -311,10 +381,10 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                v, kind, thr, n, el = cpu_reference_rate(expr, cfg, seconds=args.cpu_seconds)
+                v, kind, thr, n, el, note = cpu_reference_rate(expr, cfg, seconds=args.cpu_seconds)
                 cpu = {"value": v, "unit": "evals/s", "cores": thr, "kind": kind,
-                       "sample": f"{n} assignments (evenly spaced) of the {cfg.n_assign}-assignment batch, full "
-                                 f"{m}-term table, {el:.1f}s on {thr} threads"}
+                       "sample": f"{n} assignments (evenly spaced) of the {cfg.n_assign}-assignment batch, "
+                                 f"{note}, {el:.1f}s on {thr} threads"}
             except Exception as ex:  # the baseline must not kill the GPU number
                 cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                        "sample": f"failed: {ex}"}
@@ -332,12 +402,14 @@ def run_ours(args):
         line = {
             "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
             "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong" if split_terms else "weak",
+            "vs_baseline": None,
             "dtype": "int32 exact exponent codes + fp64 term sum", "data": "synthetic",
             "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": m, "n_rows": R,
                        "assignments_per_gpu": N, "batch": "enumerated" if cfg.enumerated else "random",
                        "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                       "parallelism": f"assignment shards x{world}", "kernel": args.kernel},
+                       "parallelism": (f"term split x{world} + NCCL all-reduce" if split_terms
+                                       else f"assignment shards x{world}"), "kernel": args.kernel},
             "e2e": None if e2e_value is None else {
                 "value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
                 "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
@@ -372,6 +444,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--split", default="assign", choices=["assign", "terms"],
+                    help="multi-GPU: assignment shards (weak) or term split + all-reduce (strong)")
     ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)

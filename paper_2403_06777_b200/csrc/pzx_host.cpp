@@ -160,7 +160,8 @@ struct HostTable {
     std::vector<uint4> qrows;               // sorted-batch kernel rows (2 per row, n_params <= 32)
     std::vector<double> sterm_c;            // its term constants (2 per term)
     int jb_term = 0;                        // running sum of slice jbase in the open term
-    bool want_slice = true;                 // build the bit-sliced layouts (srows / qrows)
+    bool want_srows = true;                 // build the bit-sliced layout (enumerated batches)
+    bool want_qrows = true;                 // build the sorted-batch layout (word lists, n_params <= 32)
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
     uint32_t max_rows = 0;
@@ -198,11 +199,22 @@ uint32_t walsh_pattern(uint64_t psi, uint64_t phi) {
 
 uint32_t walsh32(uint64_t m) { return walsh().w32[m & 31]; }
 
-// PZX_LAYOUTS=base keeps only the base row layout (POPC / gray kernels) --
-// for tables too large to hold the bit-sliced copies as well
-bool layouts_base_only() {
+// Which row layouts a table carries besides the base one (POPC / gray kernels).
+// Each bit-sliced layout costs 32 B per row on top of the base 16 (or 32) B:
+// PZX_LAYOUTS = base | slice | sorted | all picks them; by default tables up
+// to 2^28 rows get all, bigger ones only the sorted-batch layout (random word
+// lists are what such tables are evaluated on, and it halves host + HBM use).
+void choose_layouts(HostTable& h, uint64_t rows_est) {
     const char* e = std::getenv("PZX_LAYOUTS");
-    return e && std::string(e) == "base";
+    const std::string s = e ? e : "";
+    bool sl, so;
+    if (s == "base") sl = so = false;
+    else if (s == "slice") sl = true, so = false;
+    else if (s == "sorted") sl = false, so = true;
+    else if (s == "all") sl = so = true;
+    else sl = rows_est <= (uint64_t(1) << 28), so = true;
+    h.want_srows = sl;
+    h.want_qrows = so && h.n_params <= 32;
 }
 
 void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, uint32_t pat, uint8_t sw,
@@ -218,11 +230,12 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t cls = (code & kCodeMask) >> 4;
     const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
     h.jb_term += kSliceJbase[op];
-    if (!h.want_slice) return;
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
-    h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
-    h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
-    if (h.n_params <= 32) {
+    if (h.want_srows) {
+        h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
+        h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
+    }
+    if (h.want_qrows) {
         auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)
             return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * kSortedTableStride);
         };
@@ -354,7 +367,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
     h.n_params = v->n_params;
     const uint64_t m = v->n_terms;
     const uint64_t rows_est = m ? v->term_offset[m] - v->term_offset[0] + m : 0;
-    h.want_slice = rows_est <= (uint64_t(1) << 28) && !layouts_base_only();
+    choose_layouts(h, rows_est);
     unsigned nth = std::max(1u, std::thread::hardware_concurrency());
     nth = unsigned(std::min<uint64_t>(nth, std::max<uint64_t>(1, m / 2048)));
     if (nth <= 1) return compile_expr_range(v, 0, m, h, err);
@@ -363,7 +376,9 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
     std::vector<std::string> errs(nth);
     std::vector<std::thread> th;
     for (unsigned i = 0; i < nth; ++i) {
-        parts[i].want_slice = h.want_slice;
+        parts[i].n_params = h.n_params;
+        parts[i].want_srows = h.want_srows;
+        parts[i].want_qrows = h.want_qrows;
         th.emplace_back([&, i] {
             st[i] = compile_expr_range(v, m * i / nth, m * (i + 1) / nth, parts[i], errs[i]);
         });
@@ -378,6 +393,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
 int compile_rows(const pzx_table_view* v, HostTable& h, std::string& err) {
     if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
     h.n_params = v->n_params;
+    choose_layouts(h, v->n_terms ? v->term_row_offset[v->n_terms] - v->term_row_offset[0] + v->n_terms : 0);
     const uint64_t allowed = param_mask(v->n_params);
     for (uint64_t t = 0; t < v->n_terms; ++t) {
         Quad c;
@@ -523,12 +539,12 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     if ((st = cuda_err(ctx, upload_vec(&t->d_rows, h.rows), "upload rows"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_row, h.term_row), "upload term offsets"))) return st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_term_c, h.term_c), "upload term constants"))) return st;
-    const bool slice_ok = h.want_slice && h.max_rows <= uint32_t(kSegRows) && slice_tables_ok();
-    if (slice_ok) {
-        if ((st = cuda_err(ctx, upload_vec(&t->d_srows, h.srows), "upload slice rows"))) return st;
-        if ((st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
-    }
-    const bool sorted_ok = slice_ok && h.n_params <= 32;
+    const bool seg_ok = h.max_rows <= uint32_t(kSegRows) && slice_tables_ok();
+    const bool slice_ok = seg_ok && h.want_srows;
+    const bool sorted_ok = seg_ok && h.want_qrows && h.n_params <= 32;
+    if (slice_ok && (st = cuda_err(ctx, upload_vec(&t->d_srows, h.srows), "upload slice rows"))) return st;
+    if ((slice_ok || sorted_ok) &&
+        (st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
     if (sorted_ok && (st = cuda_err(ctx, upload_vec(&t->d_qrows, h.qrows), "upload sorted-kernel rows"))) return st;
     LutLayout L;
     std::vector<unsigned char> blob = build_lut(h.max_rows, L);

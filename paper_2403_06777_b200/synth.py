@@ -112,9 +112,47 @@ def generate(n_params: int, n_terms: int, n_lo: int, n_hi: int, seed: int, mix: 
     return ScalarExpression(P, off, scal, kind, psi_k, psi_mask, phi_k, phi_mask)
 
 
-def generate_config(cfg: Config, n_terms: int | None = None) -> ScalarExpression:
-    return generate(cfg.n_params, cfg.n_terms if n_terms is None else n_terms, cfg.n_lo, cfg.n_hi,
-                    20261018 + cfg.cid, cfg.mix, exp_cap=cfg.exp_cap)
+CHUNK_TERMS = 1 << 20   # configs above this are generated as independently seeded term chunks
+
+
+def n_chunks(cfg: Config, n_terms: int | None = None) -> int:
+    n = cfg.n_terms if n_terms is None else n_terms
+    return max(1, -(-n // CHUNK_TERMS))
+
+
+def concat(parts: list[ScalarExpression]) -> ScalarExpression:
+    """Term lists back to back (offsets rebased)."""
+    if len(parts) == 1:
+        return parts[0]
+    offs, base = [np.zeros(1, np.uint64)], np.uint64(0)
+    for e in parts:
+        offs.append(e.term_offset[1:] + base)
+        base += e.term_offset[-1]
+    cat = lambda name: np.concatenate([getattr(e, name) for e in parts])  # noqa: E731
+    return ScalarExpression(parts[0].n_params, np.concatenate(offs), np.concatenate([e.term_scalar for e in parts]),
+                            cat("kind"), cat("psi_k"), cat("psi_mask"), cat("phi_k"), cat("phi_mask"))
+
+
+def generate_config(cfg: Config, n_terms: int | None = None, chunks: range | None = None,
+                    workers: int | None = None) -> ScalarExpression:
+    """The config's term list. Above CHUNK_TERMS terms it is the concatenation of
+    chunks seeded (seed, chunk index), so a term-split rank can generate just its
+    own chunks (`chunks`) and big tables generate on several threads."""
+    n = cfg.n_terms if n_terms is None else n_terms
+    seed = 20261018 + cfg.cid
+    if n <= CHUNK_TERMS and chunks is None:
+        return generate(cfg.n_params, n, cfg.n_lo, cfg.n_hi, seed, cfg.mix, exp_cap=cfg.exp_cap)
+    nc = n_chunks(cfg, n)
+    chunks = range(nc) if chunks is None else chunks
+
+    def one(c):
+        m = min(CHUNK_TERMS, n - c * CHUNK_TERMS)
+        return generate(cfg.n_params, m, cfg.n_lo, cfg.n_hi, seed * 4099 + c, cfg.mix, exp_cap=cfg.exp_cap)
+    import concurrent.futures as cf
+    import os
+    with cf.ThreadPoolExecutor(workers or min(len(chunks), os.cpu_count() or 1, 32)) as ex:
+        parts = list(ex.map(one, chunks))
+    return concat(parts)
 
 
 def assignments(cfg: Config, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
