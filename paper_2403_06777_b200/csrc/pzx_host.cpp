@@ -427,8 +427,8 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
     L.u_off = align16(L.om_off + 8 * 16);
     L.p3_off = align16(L.u_off + 8 * (M + 1));
     L.pd_off = align16(L.p3_off + 8 * (M / 2 + 1));
-    L.ab_off = align16(L.pd_off + 16 * (2 * M + 1));
-    L.bytes = align16(L.ab_off + 16 * 16);
+    L.sab_off = align16(L.pd_off + 16 * (2 * M + 1));
+    L.bytes = align16(L.sab_off + 16 * 128);
     std::vector<unsigned char> blob(L.bytes, 0);
     uint32_t* codes = reinterpret_cast<uint32_t*>(blob.data() + L.codes_off);
     for (int c = 0; c < 64; ++c)
@@ -455,15 +455,20 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
         a = cmul(a, pi);
         b = cmul(b, pip);
     }
-    double* ab = reinterpret_cast<double*>(blob.data() + L.ab_off);
-    for (int ia = 0; ia < 4; ++ia)
-        for (int ib = 0; ib < 4; ++ib) {
-            C128 v{1, 0};
-            for (int k = 0; k < ia; ++k) v = cmul(v, pi);
-            for (int k = 0; k < ib; ++k) v = cmul(v, pip);
-            ab[2 * (ia | (ib << 2))] = double(v.re);
-            ab[2 * (ia | (ib << 2)) + 1] = double(v.im);
-        }
+    // (sqrt2-1)^s pi^a pi'^b for s < 8, a, b < 4 (slice-kernel fast path),
+    // index s | a << 3 | b << 5, each rounded once from f128
+    double* sab = reinterpret_cast<double*>(blob.data() + L.sab_off);
+    for (int is = 0; is < 8; ++is)
+        for (int ia = 0; ia < 4; ++ia)
+            for (int ib = 0; ib < 4; ++ib) {
+                C128 v{1, 0};
+                for (int k = 0; k < ia; ++k) v = cmul(v, pi);
+                for (int k = 0; k < ib; ++k) v = cmul(v, pip);
+                for (int k = 0; k < is; ++k) v = cmul(v, C128{f128_sqrt2() - 1, 0});
+                const int i = is | (ia << 3) | (ib << 5);
+                sab[2 * i] = double(v.re);
+                sab[2 * i + 1] = double(v.im);
+            }
     return blob;
 }
 

@@ -87,7 +87,7 @@ struct SmemLut {
     const double* u;
     const double* p3;
     const double2* pd;  // centred: pd[d], d in [-max_rows, max_rows]
-    const double2* ab;  // pi^a pi'^b, a, b < 4, index a | b << 2
+    const double2* sab;  // (sqrt2-1)^s pi^a pi'^b, s < 8, a, b < 4, index s | a << 3 | b << 5
 };
 
 __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* dst_bytes) {
@@ -102,7 +102,7 @@ __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* d
     L.u = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.u_off);
     L.p3 = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.p3_off);
     L.pd = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.pd_off) + t.lut_layout.max_rows;
-    L.ab = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.ab_off);
+    L.sab = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.sab_off);
     return L;
 }
 
@@ -467,21 +467,276 @@ __host__ __device__ constexpr uint32_t slice_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
+// ---- tensor memory (TMEM) accumulators --------------------------------------
+// The bit-sliced kernels keep 32 fp64 complex accumulators per thread. In TMEM
+// (128 lanes x 512 columns x 32 bit per SM) a 128-thread CTA holds them in 128
+// columns: thread (warp w, lane l) owns TMEM lane 32 w + l, assignment g at
+// columns 4g .. 4g+3 (re lo/hi, im lo/hi). That frees the 64 KB of shared
+// memory per CTA the accumulators would otherwise take: 4 CTAs (16 warps) per
+// SM instead of 3 (slice) or 2 (sorted).
+constexpr uint32_t kTmemCols = 128;
+constexpr size_t kTmemCtaSmem = 51200;  // dynamic smem floor: at most 4 CTAs/SM (= 512 TMEM columns)
+
+// PZX_ACC=smem keeps the accumulators in shared memory (A/B comparisons)
+bool tmem_accumulators() {
+    static const bool on = [] {
+        const char* e = std::getenv("PZX_ACC");
+        return !(e && std::string(e) == "smem");
+    }();
+    return on;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_sync_fence() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// warp 0 allocates kTmemCols columns; returns this thread's lane-quarter address
+__device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* base_s) {
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(base_s)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tmem_sync_fence();
+    return *base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16);
+}
+__device__ __forceinline__ uint32_t tmem_base_of(uint32_t taddr) { return taddr & 0x0000FFFFu; }
+__device__ __forceinline__ void tmem_free_cta(uint32_t base) {
+    tmem_sync_fence();
+    if ((threadIdx.x >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kTmemCols) : "memory");
+}
+__device__ __forceinline__ double2 v2d(const uint32_t* v) {
+    return make_double2(__hiloint2double(int(v[1]), int(v[0])), __hiloint2double(int(v[3]), int(v[2])));
+}
+__device__ __forceinline__ void d2v(double2 d, uint32_t* v) {
+    v[0] = uint32_t(__double2loint(d.x));
+    v[1] = uint32_t(__double2hiint(d.x));
+    v[2] = uint32_t(__double2loint(d.y));
+    v[3] = uint32_t(__double2hiint(d.y));
+}
+
+// Accumulator home of a bit-sliced kernel thread: shared memory ([g][NT]) or TMEM.
+template <int NT, bool TM>
+struct SliceAcc {
+    double2* amp_s;  // !TM
+    uint32_t taddr;  // TM: this thread's lane, column 0
+    __device__ __forceinline__ void zero() {
+        if constexpr (TM) {
+            uint32_t v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_st32(taddr + 32u * c, v);
+            tmem_wait_st();
+        } else {
+#pragma unroll
+            for (int g = 0; g < kSliceG; ++g) amp_s[g * NT + threadIdx.x] = make_double2(0.0, 0.0);
+        }
+    }
+};
+
+// Term constants reach the epilogue through two per-warp shared slots filled
+// by cp.async one term ahead (no registers live across the row loop).
+struct TermC {
+    double2* slot;   // this warp's 2 slots
+    uint64_t next;   // index of the next constant to prefetch
+    uint64_t end;
+};
+__device__ __forceinline__ void termc_fetch(TermC& tc, const double2* src) {
+    const uint32_t k = uint32_t(tc.next & 1u);  // term i lives in slot i & 1
+    // one commit group per call (empty past the end) keeps "wait_group 1" exact
+    if ((threadIdx.x & 31u) == 0) {
+        if (tc.next < tc.end)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(tc.slot + k)),
+                         "l"(src + tc.next));
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    ++tc.next;
+}
+__device__ __forceinline__ void termc_init(TermC& tc, double2* slot, const double2* src, uint64_t tb, uint64_t te) {
+    tc.slot = slot;
+    tc.next = tb;
+    tc.end = te;
+    termc_fetch(tc, src);
+    termc_fetch(tc, src);
+}
+// C of term (tc.next - 2); then refill its slot with term tc.next
+__device__ __forceinline__ double2 termc_take(TermC& tc, const double2* src) {
+    const uint32_t k = uint32_t(tc.next & 1u);  // == (tc.next - 2) & 1
+    if ((threadIdx.x & 31u) == 0) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncwarp();
+    const double2 C = tc.slot[k];
+    __syncwarp();
+    termc_fetch(tc, src);
+    return C;
+}
+
+constexpr int kCrot = 16;  // per-warp phase table: C * w^j for j < 8, zeros for Z-marked (dead) assignments
+constexpr int kWarpScratch = kCrot + 2;  // + the two TermC slots (double2 units per warp)
+
+// Fixed-width decode of bit-sliced counters, 4 assignments at a time:
+// nibble m of plane P (bits 4m..4m+3, pre-split into Q = P & 0x0F0F0F0F and
+// Q' = (P >> 4) & 0x0F0F0F0F so one PRMT isolates it) is spread to bit k of
+// bytes 0..3 by one multiply: bit i * (1 + 2^7 + 2^14 + 2^21) lands on 8i for
+// i < 4, and no two partial products overlap below 2^25, so masking the
+// product keeps exactly bit i -> byte i.
+struct Nib {
+    uint32_t lo, hi;
+};
+__device__ __forceinline__ Nib nib_split(uint32_t p) { return Nib{p & 0x0F0F0F0Fu, (p >> 4) & 0x0F0F0F0Fu}; }
+
+// m, k are compile-time constants after unrolling
+__device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
+    const uint32_t n = __byte_perm((m & 1) ? q.hi : q.lo, 0u, 0x4440u | uint32_t(m >> 1));
+    return (n * (0x00204081u << k)) & (0x01010101u << k);
+}
+
 // Term epilogue shared by the bit-sliced kernels: fold 6*s1 into J, build
 // the warp's C * w^j table, and add every live assignment's term value into its
-// fp64 accumulator; resets the per-term state.
-template <int NT>
-__device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemLut& L, double2* crot,
-                                                    double2* amp_s, uint32_t& J0, uint32_t& J1,
+// fp64 accumulator; resets the per-term state. Fast path (every counter fits
+// its field: s1 < 8, a, b < 4): per group of 4 assignments two byte-keys
+// words are built by nib_spread -- (j | Z << 3) and (s1 | a << 3 | b << 5) --
+// then each assignment is 2 table loads + 4 DFMA into its accumulator, no
+// branches (Z-marked assignments read a zero entry).
+template <int NT, bool TM, bool KINDS>
+__device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
+                                                    uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
+                                                    const uint32_t (&S)[kPlanes], const uint32_t (&A)[kPlanes],
+                                                    const uint32_t (&B)[kPlanes]) {
+    const Nib j0 = nib_split(J0), j1 = nib_split(J1), j2 = nib_split(J2), z = nib_split(Z);
+    Nib s0{}, s1{}, s2{}, a0{}, a1{}, b0{}, b1{};
+    if constexpr (KINDS) {
+        s0 = nib_split(S[0]); s1 = nib_split(S[1]); s2 = nib_split(S[2]);
+        a0 = nib_split(A[0]); a1 = nib_split(A[1]);
+        b0 = nib_split(B[0]); b1 = nib_split(B[1]);
+    }
+    auto mac = [&](double2& o, const double2 c, const double2 f) {
+        if constexpr (KINDS) {
+            o.x = fma(c.x, f.x, o.x);
+            o.y = fma(c.x, f.y, o.y);
+            o.x = fma(-c.y, f.y, o.x);
+            o.y = fma(c.y, f.x, o.y);
+        } else {
+            o.x += c.x;
+            o.y += c.y;
+        }
+    };
+    // the term values of group m (4 assignments): c[r] * f[r]
+    auto group = [&](int m, double2 (&c)[4], double2 (&f)[4]) {
+        const uint32_t kj = nib_spread(j0, m, 0) | nib_spread(j1, m, 1) | nib_spread(j2, m, 2) | nib_spread(z, m, 3);
+        uint32_t ks = 0;
+        if constexpr (KINDS)
+            ks = nib_spread(s0, m, 0) | nib_spread(s1, m, 1) | nib_spread(s2, m, 2) | nib_spread(a0, m, 3) |
+                 nib_spread(a1, m, 4) | nib_spread(b0, m, 5) | nib_spread(b1, m, 6);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            c[r] = crot[__byte_perm(kj, 0u, 0x4440u | uint32_t(r))];
+            if constexpr (KINDS) f[r] = L.sab[__byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
+        }
+    };
+    if constexpr (TM) {
+        // 8 groups of 4 assignments = 16 TMEM columns each; the load of group
+        // m + 1 is in flight while group m is computed (wait::ld waits for all)
+        tmem_wait_st();  // the previous term's stores have landed
+        uint32_t v[2][16];
+        tmem_ld16(acc.taddr, v[0]);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            double2 c[4], f[4];
+            group(m, c, f);
+            tmem_wait_ld();
+            if (m + 1 < 8) tmem_ld16(acc.taddr + 16u * (m + 1), v[(m + 1) & 1]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double2 o = v2d(v[m & 1] + 4 * r);
+                mac(o, c[r], f[r]);
+                d2v(o, v[m & 1] + 4 * r);
+            }
+            tmem_st16(acc.taddr + 16u * m, v[m & 1]);
+        }
+    } else {
+        double2* ap = acc.amp_s + threadIdx.x;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            // all loads of the group first: the accumulator stores below may alias
+            // them as far as the compiler knows, so this order is what buys ILP
+            double2 c[4], f[4], o[4];
+            group(m, c, f);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) o[r] = ap[(4 * m + r) * NT];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) mac(o[r], c[r], f[r]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) ap[(4 * m + r) * NT] = o[r];
+        }
+    }
+}
+
+// Any counter widths: one assignment's term value (0 when Z-marked).
+__device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const double2* crot, uint32_t J0, uint32_t J1,
+                                                    uint32_t J2, uint32_t Z, const uint32_t (&S)[kPlanes],
+                                                    const uint32_t (&A)[kPlanes], const uint32_t (&B)[kPlanes],
+                                                    uint32_t nS, uint32_t nA, uint32_t nB, int g) {
+    if ((Z >> g) & 1u) return make_double2(0.0, 0.0);
+    const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+    double2 v = crot[j];
+    const uint32_t s1 = slice_decode(S, nS, g);
+    const uint32_t a = slice_decode(A, nA, g);
+    const uint32_t b = slice_decode(B, nB, g);
+    double rr = L.u[s1];
+    if (a | b) {
+        const uint32_t mn = a < b ? a : b;
+        rr *= L.p3[mn];
+        const double2 pd = L.pd[int(a) - int(b)];
+        const double vr = v.x * pd.x - v.y * pd.y;
+        v.y = v.x * pd.y + v.y * pd.x;
+        v.x = vr;
+    }
+    v.x *= rr;
+    v.y *= rr;
+    return v;
+}
+
+template <int NT, bool TM>
+__device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
+                                                    SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
                                                     uint32_t& J2, uint32_t& Z, uint32_t (&S)[kPlanes],
                                                     uint32_t (&A)[kPlanes], uint32_t (&B)[kPlanes],
                                                     uint32_t& nS, uint32_t& nA, uint32_t& nB) {
-    // ---- term epilogue -------------------------------------
     const uint32_t lane = threadIdx.x & 31u;
-    __syncwarp();
-    if (lane < 8) {
-        const double2 w = L.om[lane];
-        crot[lane] = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+    const double2 C = termc_take(tc, src);
+    if (lane < uint32_t(kCrot)) {
+        double2 v = make_double2(0.0, 0.0);
+        if (lane < 8) {
+            const double2 w = L.om[lane];
+            v = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+        }
+        crot[lane] = v;
     }
     __syncwarp();
     if (nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
@@ -491,75 +746,39 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
         J2 ^= w2 ^ c1;
     }
     const bool kinds = (nS | nA | nB) != 0;
-    uint32_t alive = ~Z;
-    // two live assignments per iteration: independent chains for latency hiding
-    auto add2 = [&](auto value_of) {
-        while (alive) {
-            const int g1 = 31 - __clz(alive);
-            alive ^= 1u << g1;
-            const bool two = alive != 0;
-            const int g2 = two ? 31 - __clz(alive) : g1;
-            if (two) alive ^= 1u << g2;
-            const double2 v1 = value_of(g1), v2 = value_of(g2);
-            double2* a1 = amp_s + g1 * NT + threadIdx.x;
-            double2* a2 = amp_s + g2 * NT + threadIdx.x;
-            double2 o1 = *a1;
-            o1.x += v1.x;
-            o1.y += v1.y;
-            *a1 = o1;
-            if (two) {
-                double2 o2 = *a2;
-                o2.x += v2.x;
-                o2.y += v2.y;
-                *a2 = o2;
-            }
-        }
-    };
-    auto jof = [&](int g) {
-        return ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
-    };
     if (!kinds) {
-        add2([&](int g) { return crot[jof(g)]; });
+        slice_epilogue_fast<NT, TM, false>(L, crot, acc, J0, J1, J2, Z, S, A, B);
     } else if (nS < 8 && nA < 4 && nB < 4) {
-        // fast path: s1 < 8 and a, b < 4 -> fixed-width decode, one
-        // real (sqrt2-1)^s1 and one complex pi^a pi'^b table lookup
-        add2([&](int g) {
-            const uint32_t s1 = ((S[0] >> g) & 1u) | (((S[1] >> g) & 1u) << 1) | (((S[2] >> g) & 1u) << 2);
-            const uint32_t ab = ((A[0] >> g) & 1u) | (((A[1] >> g) & 1u) << 1) |
-                                (((B[0] >> g) & 1u) << 2) | (((B[1] >> g) & 1u) << 3);
-            const double2 cj = crot[jof(g)];
-            const double2 f = L.ab[ab];
-            const double rr = L.u[s1];
-            const double fr = f.x * rr, fi = f.y * rr;
-            return make_double2(cj.x * fr - cj.y * fi, cj.x * fi + cj.y * fr);
-        });
-    }
-    while (alive) {
-        const int g = __ffs(alive) - 1;
-        alive &= alive - 1;
-        const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
-        double2 v = crot[j];
-        if (kinds) {
-            const uint32_t s1 = slice_decode(S, nS, g);
-            const uint32_t a = slice_decode(A, nA, g);
-            const uint32_t b = slice_decode(B, nB, g);
-            double rr = L.u[s1];
-            if (a | b) {
-                const uint32_t mn = a < b ? a : b;
-                rr *= L.p3[mn];
-                const double2 pd = L.pd[int(a) - int(b)];
-                const double vr = v.x * pd.x - v.y * pd.y;
-                v.y = v.x * pd.y + v.y * pd.x;
-                v.x = vr;
+        slice_epilogue_fast<NT, TM, true>(L, crot, acc, J0, J1, J2, Z, S, A, B);
+    } else if constexpr (TM) {
+        tmem_wait_st();
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[32];
+            tmem_ld32(acc.taddr + 32u * ch, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double2 d = slice_value_slow(L, crot, J0, J1, J2, Z, S, A, B, nS, nA, nB, 8 * ch + q);
+                double2 o = v2d(v + 4 * q);
+                o.x += d.x;
+                o.y += d.y;
+                d2v(o, v + 4 * q);
             }
-            v.x *= rr;
-            v.y *= rr;
+            tmem_st32(acc.taddr + 32u * ch, v);
         }
-        double2* ap = amp_s + g * NT + threadIdx.x;
-        double2 o = *ap;
-        o.x += v.x;
-        o.y += v.y;
-        *ap = o;
+    } else {
+        uint32_t alive = ~Z;
+        while (alive) {
+            const int g = __ffs(alive) - 1;
+            alive &= alive - 1;
+            const double2 d = slice_value_slow(L, crot, J0, J1, J2, Z, S, A, B, nS, nA, nB, g);
+            double2* ap = acc.amp_s + g * NT + threadIdx.x;
+            double2 o = *ap;
+            o.x += d.x;
+            o.y += d.y;
+            *ap = o;
+        }
     }
     J0 = J1 = J2 = Z = 0;
     if (kinds) {
@@ -571,11 +790,31 @@ __device__ __forceinline__ void slice_term_epilogue(const double2 C, const SmemL
 
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
-template <bool P64, bool RAND, int NT>
+template <bool P64, bool RAND, int NT, bool TM = false>
 size_t slice_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t planes = RAND ? size_t(P64 ? 64 : 32) * NT * 4 : 0;
-    return amp_off + size_t(kSliceG) * NT * 16 + (NT / 32) * 8 * 16 + planes;
+    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * NT * 16) + (NT / 32) * kWarpScratch * 16 + planes;
+    return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
+}
+
+template <int NT, bool TM>
+__device__ __forceinline__ void slice_store_results(const LaunchReq& r, uint64_t off, SliceAcc<NT, TM>& acc) {
+    if constexpr (TM) {
+        tmem_wait_st();
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[32];
+            tmem_ld32(acc.taddr + 32u * ch, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) store_result(r, off + 8 * ch + q, v2d(v + 4 * q));
+        }
+        tmem_free_cta(tmem_base_of(acc.taddr));
+    } else {
+#pragma unroll 4
+        for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, acc.amp_s[g * NT + threadIdx.x]);
+    }
 }
 
 // 32 x 32 bit-matrix transpose: afterwards a[i] bit g = (old a[g]) bit i.
@@ -620,15 +859,18 @@ __device__ __forceinline__ uint32_t planes_parity(uint32_t mask, uint32_t plane_
 // table C * w^j (8 entries) is built once per warp, then every live
 // assignment adds C * w^j' * (stuff from S, A, B) into its fp64 accumulator in
 // shared memory.
-template <bool P64, bool RAND, int NT>
-__global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const LaunchReq r) {
+template <bool P64, bool RAND, int NT, bool TM = false>
+__global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t, const LaunchReq r) {
+    static_assert(!TM || NT == 128, "TMEM accumulators: one warp per TMEM lane quarter");
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t tmem_base_s;
     const SmemLut L = kernel_prologue(t, smem, slice_lut_offset<P64>());
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
-    double2* crot = amp_s + kSliceG * NT + (threadIdx.x >> 5) * 8;
-#pragma unroll
-    for (int g = 0; g < kSliceG; ++g) amp_s[g * NT + threadIdx.x] = make_double2(0.0, 0.0);
+    double2* crot = amp_s + (TM ? 0 : kSliceG * NT) + (threadIdx.x >> 5) * kWarpScratch;
+    SliceAcc<NT, TM> acc{amp_s, 0u};
+    if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
+    acc.zero();
 
     uint64_t tb, te;
     term_range(r, tb, te);
@@ -637,7 +879,7 @@ __global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const Launc
     uint32_t planes_s = 0;  // shared address of this thread's plane 0 (RAND)
     if constexpr (RAND) {
         // thread owns the 32 arbitrary words off .. off+31: transpose into planes
-        uint32_t* planes = reinterpret_cast<uint32_t*>(crot + (NT / 32 - (threadIdx.x >> 5)) * 8);
+        uint32_t* planes = reinterpret_cast<uint32_t*>(crot + (NT / 32 - (threadIdx.x >> 5)) * kWarpScratch);
         planes_s = smem_u32(planes) + threadIdx.x * 4;
         uint32_t w[32];
 #pragma unroll
@@ -681,18 +923,22 @@ __global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const Launc
             if (ntiles > 0) issue(0);
             if (ntiles > 1) issue(1);
         }
-        uint64_t term = tb;
-        double2 C = __ldg(t.sterm_c + tb);
-        double2 Cn = (tb + 1 < te) ? __ldg(t.sterm_c + tb + 1) : make_double2(0.0, 0.0);
+        TermC tc;
+        termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
         for (uint32_t i = 0; i < ntiles; ++i) {
             mbar_wait(&bars[i & 1], (i >> 1) & 1u);
             const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
             const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
+            // rows software-pipelined one ahead (the read past the last row
+            // stays inside the CTA's shared window and is never used)
+            uint4 na = lds128(a0), nb = lds128(a0 + 16);
             for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint4 ra = lds128(ad);       // psi, phi, code, Walsh32(psi)
-                const uint4 rb = lds128(ad + 16);  // Walsh32(phi), psi_hi, phi_hi, 0
+                const uint4 ra = na;  // psi, phi, code, Walsh32(psi)
+                const uint4 rb = nb;  // Walsh32(phi), psi_hi, phi_hi, 0
+                na = lds128(ad + 32);
+                nb = lds128(ad + 48);
                 const uint32_t op = __shfl_sync(0xFFFFFFFFu, ra.z, 0) & 0xFFu;  // provably warp-uniform -> BRXU
                 uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
                 if constexpr (RAND) {
@@ -724,12 +970,8 @@ __global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const Launc
                     if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
                     if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
                     if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
-                    if (ra.z & kEndFlag) {
-                        slice_term_epilogue<NT>(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
-                        C = Cn;
-                        ++term;
-                        Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
-                    }
+                    if (ra.z & kEndFlag)
+                        slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, S, A, B, nS, nA, nB);
                 }
             }
             __syncthreads();  // every thread is done with buffer (i & 1)
@@ -739,8 +981,7 @@ __global__ void __launch_bounds__(NT) k_eval_slice(const DevTable t, const Launc
             }
         }
     }
-#pragma unroll 4
-    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * NT + threadIdx.x]);
+    slice_store_results<NT, TM>(r, off, acc);
 }
 
 // ------------------------------------------------------ sorted kernel ----
@@ -759,10 +1000,12 @@ __host__ __device__ constexpr uint32_t sorted_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
+template <bool TM = false>
 size_t sorted_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
-    return amp_off + size_t(kSliceG) * kSliceThreads * 16 + (kSliceThreads / 32) * 8 * 16 +
-           size_t(kSortedGroups) * 16 * kSortedTableStride;
+    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * kSliceThreads * 16) +
+                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(kSortedGroups) * 16 * kSortedTableStride;
+    return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
@@ -771,15 +1014,19 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     return v;
 }
 
-__global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t, const LaunchReq r) {
+template <bool TM = false>
+__global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const DevTable t, const LaunchReq r) {
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t tmem_base_s;
     const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset());
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
-    double2* crot = amp_s + kSliceG * kSliceThreads + (threadIdx.x >> 5) * 8;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + kSliceG * kSliceThreads + (kSliceThreads / 32) * 8);
-#pragma unroll
-    for (int g = 0; g < kSliceG; ++g) amp_s[g * kSliceThreads + threadIdx.x] = make_double2(0.0, 0.0);
+    double2* crot = amp_s + (TM ? 0 : kSliceG * kSliceThreads) + (threadIdx.x >> 5) * kWarpScratch;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * kSliceThreads) +
+                                                (kSliceThreads / 32) * kWarpScratch);
+    SliceAcc<kSliceThreads, TM> acc{amp_s, 0u};
+    if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
+    acc.zero();
 
     uint64_t tb, te;
     term_range(r, tb, te);
@@ -839,9 +1086,8 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t,
             if (ntiles > 0) issue(0);
             if (ntiles > 1) issue(1);
         }
-        uint64_t term = tb;
-        double2 C = __ldg(t.sterm_c + tb);
-        double2 Cn = (tb + 1 < te) ? __ldg(t.sterm_c + tb + 1) : make_double2(0.0, 0.0);
+        TermC tc;
+        termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
         for (uint32_t i = 0; i < ntiles; ++i) {
             mbar_wait(&bars[i & 1], (i >> 1) & 1u);
             const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
@@ -865,12 +1111,9 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t,
                     if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
                     if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
                     if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
-                    if (ra.z & kEndFlag) {
-                        slice_term_epilogue<kSliceThreads>(C, L, crot, amp_s, J0, J1, J2, Z, S, A, B, nS, nA, nB);
-                        C = Cn;
-                        ++term;
-                        Cn = (term + 1 < te) ? __ldg(t.sterm_c + term + 1) : make_double2(0.0, 0.0);
-                    }
+                    if (ra.z & kEndFlag)
+                        slice_term_epilogue<kSliceThreads, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, S, A,
+                                                               B, nS, nA, nB);
                 }
             }
             __syncthreads();
@@ -880,8 +1123,7 @@ __global__ void __launch_bounds__(kSliceThreads) k_eval_sorted(const DevTable t,
             }
         }
     }
-#pragma unroll 4
-    for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, amp_s[g * kSliceThreads + threadIdx.x]);
+    slice_store_results<kSliceThreads, TM>(r, off, acc);
 }
 
 __global__ void k_max_spread(const uint64_t* __restrict__ sorted, uint64_t n, unsigned long long* out) {
@@ -993,20 +1235,26 @@ cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, con
 
 template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
+    const bool tm = tmem_accumulators();
     if (kc == KC_SORTED) {
-        const size_t sm = sorted_smem_bytes(t);
-        cudaError_t e = cudaFuncSetAttribute(k_eval_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        const size_t sm = tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t);
+        auto kern = tm ? k_eval_sorted<true> : k_eval_sorted<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
-        k_eval_sorted<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         const bool small = slice_threads(r) == 32;
         const size_t sm = rnd ? (small ? slice_smem_bytes<P64, true, 32>(t) : slice_smem_bytes<P64, true, 128>(t))
-                              : (small ? slice_smem_bytes<P64, false, 32>(t) : slice_smem_bytes<P64, false, 128>(t));
+                        : small ? slice_smem_bytes<P64, false, 32>(t)
+                        : tm    ? slice_smem_bytes<P64, false, 128, true>(t)
+                                : slice_smem_bytes<P64, false, 128>(t);
         auto kern = rnd ? (small ? k_eval_slice<P64, true, 32> : k_eval_slice<P64, true, 128>)
-                        : (small ? k_eval_slice<P64, false, 32> : k_eval_slice<P64, false, 128>);
+                  : small ? k_eval_slice<P64, false, 32>
+                  : tm    ? k_eval_slice<P64, false, 128, true>
+                          : k_eval_slice<P64, false, 128>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         kern<<<grid, small ? 32 : 128, sm, r.stream>>>(t, r);
@@ -1062,10 +1310,12 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
+    const bool tm = tmem_accumulators();
     if (kc == KC_SORTED) {
-        sm = sorted_smem_bytes(t);
-        cudaFuncSetAttribute(k_eval_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_sorted, kSliceThreads, sm);
+        sm = tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t);
+        auto kern = tm ? k_eval_sorted<true> : k_eval_sorted<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         if (nt == 32) {
@@ -1076,10 +1326,14 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, sm);
         } else {
-            auto kern = t.p64 ? (rnd ? k_eval_slice<true, true, 128> : k_eval_slice<true, false, 128>)
-                              : (rnd ? k_eval_slice<false, true, 128> : k_eval_slice<false, false, 128>);
-            sm = t.p64 ? (rnd ? slice_smem_bytes<true, true, 128>(t) : slice_smem_bytes<true, false, 128>(t))
-                       : (rnd ? slice_smem_bytes<false, true, 128>(t) : slice_smem_bytes<false, false, 128>(t));
+            auto kern = t.p64 ? (rnd ? k_eval_slice<true, true, 128>
+                                 : tm ? k_eval_slice<true, false, 128, true> : k_eval_slice<true, false, 128>)
+                              : (rnd ? k_eval_slice<false, true, 128>
+                                 : tm ? k_eval_slice<false, false, 128, true> : k_eval_slice<false, false, 128>);
+            sm = t.p64 ? (rnd ? slice_smem_bytes<true, true, 128>(t)
+                          : tm ? slice_smem_bytes<true, false, 128, true>(t) : slice_smem_bytes<true, false, 128>(t))
+                       : (rnd ? slice_smem_bytes<false, true, 128>(t)
+                          : tm ? slice_smem_bytes<false, false, 128, true>(t) : slice_smem_bytes<false, false, 128>(t));
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, sm);
         }
