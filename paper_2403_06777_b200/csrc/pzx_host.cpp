@@ -233,7 +233,12 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
     if (h.want_srows) {
         h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
-        h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), 0));
+        // P <= 32: the high-mask words carry ~Walsh32 instead, so the kernel
+        // selects X = parity ? ~W : W with one SEL
+        if (h.n_params <= 32)
+            h.srows.push_back(make_uint4(walsh32(phi), ~walsh32(psi), ~walsh32(phi), op));
+        else
+            h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), op));
     }
     if (h.want_qrows) {
         auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)

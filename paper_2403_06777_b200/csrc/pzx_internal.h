@@ -63,7 +63,8 @@ struct DevTable {
     uint32_t n_params = 0, max_rows = 0;
     int p64 = 0;
     // bit-sliced kernel (only when every term has <= kSegRows rows):
-    // rows as 2 x uint4 {psi, phi, op | kEndFlag, Walsh32(psi)}, {Walsh32(phi), psi_hi, phi_hi, 0}
+    // rows as 2 x uint4 {psi, phi, op | kind flags | kEndFlag, Walsh32(psi)}, {Walsh32(phi), psi_hi, phi_hi, op}
+    // (n_params <= 32: {Walsh32(phi), ~Walsh32(psi), ~Walsh32(phi), op})
     // (op = class * 2 + single, pzx_classes.h), constants C''_t * w^(sum of row jbase)
     const uint4* srows = nullptr;
     const double2* sterm_c = nullptr;

@@ -439,28 +439,85 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
-// bit-sliced counter += v (one bit per assignment); n = rows that could have
-// bumped it so far (warp-uniform), so only planes below bit_length(n) move
-__device__ __forceinline__ void slice_bump(uint32_t (&P)[kPlanes], uint32_t n, uint32_t v) {
-    uint32_t t = v;
-#pragma unroll
-    for (int i = 0; i < kPlanes; ++i) {
-        if (i > 0 && (n >> i) == 0) break;
-        const uint32_t u = P[i] & t;
-        P[i] ^= t;
-        t = u;
-    }
-}
+// Bit-sliced lambda / pi / pi' counters (one bit per assignment per plane,
+// up to kPlanes planes = counts < 128). The planes the epilogue fast path reads
+// (s1 < 8, a, b < 4) stay in registers; the rarely reached high planes live
+// in shared memory ([plane][NT], conflict-free) so they cost no registers.
+constexpr int kLoS = 3, kLoAB = 2;
+constexpr int kHiPlanes = (kPlanes - kLoS) + 2 * (kPlanes - kLoAB);  // 14 shared planes per thread
 
-__device__ __forceinline__ uint32_t slice_decode(const uint32_t (&P)[kPlanes], uint32_t n, int g) {
-    uint32_t x = (P[0] >> g) & 1u;
+template <int NT>
+struct KindCounters {
+    uint32_t S[kLoS], A[kLoAB], B[kLoAB];
+    uint32_t nS, nA, nB;
+    uint32_t* hi;  // this thread's column of the [kHiPlanes][NT] shared planes
+
+    __device__ __forceinline__ uint32_t* hs(int i) { return hi + (i - kLoS) * NT; }
+    __device__ __forceinline__ uint32_t* ha(int i) { return hi + (kPlanes - kLoS + i - kLoAB) * NT; }
+    __device__ __forceinline__ uint32_t* hb(int i) { return hi + (2 * kPlanes - kLoS - kLoAB + i - kLoAB) * NT; }
+
+    __device__ __forceinline__ void init(uint32_t* h) {
+        hi = h;
 #pragma unroll
-    for (int i = 1; i < kPlanes; ++i) {
-        if ((n >> i) == 0) break;
-        x |= ((P[i] >> g) & 1u) << i;
+        for (int i = 0; i < kLoS; ++i) S[i] = 0;
+#pragma unroll
+        for (int i = 0; i < kLoAB; ++i) A[i] = B[i] = 0;
+        nS = nA = nB = 0;
+#pragma unroll
+        for (int i = 0; i < kHiPlanes; ++i) hi[i * NT] = 0;
     }
-    return x;
-}
+    // counter += v; n = rows that could have bumped it so far (warp-uniform),
+    // so only planes below bit_length(n) move
+    template <int LO, typename HiPlane>
+    __device__ __forceinline__ static void bump(uint32_t (&P)[LO], uint32_t n, uint32_t v, HiPlane hp) {
+        uint32_t t = v;
+#pragma unroll
+        for (int i = 0; i < LO; ++i) {
+            if (i > 0 && (n >> i) == 0) return;
+            const uint32_t u = P[i] & t;
+            P[i] ^= t;
+            t = u;
+        }
+        for (int i = LO; i < kPlanes; ++i) {
+            if ((n >> i) == 0) return;
+            uint32_t* q = hp(i);
+            const uint32_t p = *q;
+            *q = p ^ t;
+            t &= p;
+        }
+    }
+    __device__ __forceinline__ void bump_s(uint32_t v) { bump<kLoS>(S, ++nS, v, [&](int i) { return hs(i); }); }
+    __device__ __forceinline__ void bump_a(uint32_t v) { bump<kLoAB>(A, ++nA, v, [&](int i) { return ha(i); }); }
+    __device__ __forceinline__ void bump_b(uint32_t v) { bump<kLoAB>(B, ++nB, v, [&](int i) { return hb(i); }); }
+
+    template <int LO, typename HiPlane>
+    __device__ __forceinline__ static uint32_t decode(const uint32_t (&P)[LO], uint32_t n, int g, HiPlane hp) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < LO; ++i) x |= ((P[i] >> g) & 1u) << i;
+        for (int i = LO; i < kPlanes; ++i) {
+            if ((n >> i) == 0) break;
+            x |= ((*hp(i) >> g) & 1u) << i;
+        }
+        return x;
+    }
+    __device__ __forceinline__ uint32_t s_of(int g) { return decode<kLoS>(S, nS, g, [&](int i) { return hs(i); }); }
+    __device__ __forceinline__ uint32_t a_of(int g) { return decode<kLoAB>(A, nA, g, [&](int i) { return ha(i); }); }
+    __device__ __forceinline__ uint32_t b_of(int g) { return decode<kLoAB>(B, nB, g, [&](int i) { return hb(i); }); }
+
+    __device__ __forceinline__ bool any() const { return (nS | nA | nB) != 0; }
+    __device__ __forceinline__ bool fits_fast() const { return nS < 8 && nA < 4 && nB < 4; }
+    __device__ __forceinline__ void reset() {
+        for (int i = kLoS; i < kPlanes && (nS >> i); ++i) *hs(i) = 0;
+        for (int i = kLoAB; i < kPlanes && (nA >> i); ++i) *ha(i) = 0;
+        for (int i = kLoAB; i < kPlanes && (nB >> i); ++i) *hb(i) = 0;
+#pragma unroll
+        for (int i = 0; i < kLoS; ++i) S[i] = 0;
+#pragma unroll
+        for (int i = 0; i < kLoAB; ++i) A[i] = B[i] = 0;
+        nS = nA = nB = 0;
+    }
+};
 
 template <bool P64>
 __host__ __device__ constexpr uint32_t slice_lut_offset() {
@@ -610,7 +667,7 @@ struct Nib {
 };
 __device__ __forceinline__ Nib nib_split(uint32_t p) { return Nib{p & 0x0F0F0F0Fu, (p >> 4) & 0x0F0F0F0Fu}; }
 
-// m, k are compile-time constants after unrolling
+// m (group of 4 assignments) may be a runtime value; k is a compile-time constant
 __device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
     const uint32_t n = __byte_perm((m & 1) ? q.hi : q.lo, 0u, 0x4440u | uint32_t(m >> 1));
     return (n * (0x00204081u << k)) & (0x01010101u << k);
@@ -623,11 +680,13 @@ __device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
 // words are built by nib_spread -- (j | Z << 3) and (s1 | a << 3 | b << 5) --
 // then each assignment is 2 table loads + 4 DFMA into its accumulator, no
 // branches (Z-marked assignments read a zero entry).
-template <int NT, bool TM, bool KINDS>
+template <int NT, bool TM, bool KINDS, bool ROLL>
 __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
                                                     uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
-                                                    const uint32_t (&S)[kPlanes], const uint32_t (&A)[kPlanes],
-                                                    const uint32_t (&B)[kPlanes]) {
+                                                    const KindCounters<NT>& K) {
+    const uint32_t(&S)[kLoS] = K.S;
+    const uint32_t(&A)[kLoAB] = K.A;
+    const uint32_t(&B)[kLoAB] = K.B;
     const Nib j0 = nib_split(J0), j1 = nib_split(J1), j2 = nib_split(J2), z = nib_split(Z);
     Nib s0{}, s1{}, s2{}, a0{}, a1{}, b0{}, b1{};
     if constexpr (KINDS) {
@@ -662,22 +721,34 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
     if constexpr (TM) {
         // 8 groups of 4 assignments = 16 TMEM columns each; the load of group
         // m + 1 is in flight while group m is computed (wait::ld waits for all)
+        // (ROLL: a rolled loop over pairs of groups keeps the epilogue's code
+        // small -- pays off in the sorted kernel, not in the slice kernel)
         tmem_wait_st();  // the previous term's stores have landed
         uint32_t v[2][16];
         tmem_ld16(acc.taddr, v[0]);
+        auto pair = [&](int m2) {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            double2 c[4], f[4];
-            group(m, c, f);
-            tmem_wait_ld();
-            if (m + 1 < 8) tmem_ld16(acc.taddr + 16u * (m + 1), v[(m + 1) & 1]);
+            for (int h = 0; h < 2; ++h) {
+                const int m = m2 + h;
+                double2 c[4], f[4];
+                group(m, c, f);
+                tmem_wait_ld();
+                if (h == 0 || m2 + 2 < 8) tmem_ld16(acc.taddr + 16u * (m + 1), v[h ^ 1]);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                double2 o = v2d(v[m & 1] + 4 * r);
-                mac(o, c[r], f[r]);
-                d2v(o, v[m & 1] + 4 * r);
+                for (int r = 0; r < 4; ++r) {
+                    double2 o = v2d(v[h] + 4 * r);
+                    mac(o, c[r], f[r]);
+                    d2v(o, v[h] + 4 * r);
+                }
+                tmem_st16(acc.taddr + 16u * m, v[h]);
             }
-            tmem_st16(acc.taddr + 16u * m, v[m & 1]);
+        };
+        if constexpr (ROLL) {
+#pragma unroll 1
+            for (int m2 = 0; m2 < 8; m2 += 2) pair(m2);
+        } else {
+#pragma unroll
+            for (int m2 = 0; m2 < 8; m2 += 2) pair(m2);
         }
     } else {
         double2* ap = acc.amp_s + threadIdx.x;
@@ -698,16 +769,15 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
 }
 
 // Any counter widths: one assignment's term value (0 when Z-marked).
+template <int NT>
 __device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const double2* crot, uint32_t J0, uint32_t J1,
-                                                    uint32_t J2, uint32_t Z, const uint32_t (&S)[kPlanes],
-                                                    const uint32_t (&A)[kPlanes], const uint32_t (&B)[kPlanes],
-                                                    uint32_t nS, uint32_t nA, uint32_t nB, int g) {
+                                                    uint32_t J2, uint32_t Z, KindCounters<NT>& K, int g) {
     if ((Z >> g) & 1u) return make_double2(0.0, 0.0);
     const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
     double2 v = crot[j];
-    const uint32_t s1 = slice_decode(S, nS, g);
-    const uint32_t a = slice_decode(A, nA, g);
-    const uint32_t b = slice_decode(B, nB, g);
+    const uint32_t s1 = K.s_of(g);
+    const uint32_t a = K.a_of(g);
+    const uint32_t b = K.b_of(g);
     double rr = L.u[s1];
     if (a | b) {
         const uint32_t mn = a < b ? a : b;
@@ -722,12 +792,10 @@ __device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const doub
     return v;
 }
 
-template <int NT, bool TM>
+template <int NT, bool TM, bool ROLL = false>
 __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
                                                     SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
-                                                    uint32_t& J2, uint32_t& Z, uint32_t (&S)[kPlanes],
-                                                    uint32_t (&A)[kPlanes], uint32_t (&B)[kPlanes],
-                                                    uint32_t& nS, uint32_t& nA, uint32_t& nB) {
+                                                    uint32_t& J2, uint32_t& Z, KindCounters<NT>& K) {
     const uint32_t lane = threadIdx.x & 31u;
     const double2 C = termc_take(tc, src);
     if (lane < uint32_t(kCrot)) {
@@ -739,17 +807,17 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
         crot[lane] = v;
     }
     __syncwarp();
-    if (nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
-        const uint32_t w1 = S[0], w2 = S[0] ^ S[1];
+    if (K.nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
+        const uint32_t w1 = K.S[0], w2 = K.S[0] ^ K.S[1];
         const uint32_t c1 = J1 & w1;
         J1 ^= w1;
         J2 ^= w2 ^ c1;
     }
-    const bool kinds = (nS | nA | nB) != 0;
+    const bool kinds = K.any();
     if (!kinds) {
-        slice_epilogue_fast<NT, TM, false>(L, crot, acc, J0, J1, J2, Z, S, A, B);
-    } else if (nS < 8 && nA < 4 && nB < 4) {
-        slice_epilogue_fast<NT, TM, true>(L, crot, acc, J0, J1, J2, Z, S, A, B);
+        slice_epilogue_fast<NT, TM, false, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
+    } else if (K.fits_fast()) {
+        slice_epilogue_fast<NT, TM, true, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
     } else if constexpr (TM) {
         tmem_wait_st();
 #pragma unroll 1
@@ -759,7 +827,7 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const double2 d = slice_value_slow(L, crot, J0, J1, J2, Z, S, A, B, nS, nA, nB, 8 * ch + q);
+                const double2 d = slice_value_slow<NT>(L, crot, J0, J1, J2, Z, K, 8 * ch + q);
                 double2 o = v2d(v + 4 * q);
                 o.x += d.x;
                 o.y += d.y;
@@ -772,7 +840,7 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
         while (alive) {
             const int g = __ffs(alive) - 1;
             alive &= alive - 1;
-            const double2 d = slice_value_slow(L, crot, J0, J1, J2, Z, S, A, B, nS, nA, nB, g);
+            const double2 d = slice_value_slow<NT>(L, crot, J0, J1, J2, Z, K, g);
             double2* ap = acc.amp_s + g * NT + threadIdx.x;
             double2 o = *ap;
             o.x += d.x;
@@ -781,11 +849,7 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
         }
     }
     J0 = J1 = J2 = Z = 0;
-    if (kinds) {
-#pragma unroll
-        for (int k = 0; k < kPlanes; ++k) S[k] = A[k] = B[k] = 0;
-        nS = nA = nB = 0;
-    }
+    if (kinds) K.reset();
 }
 
 // Random batches: the thread's 32 words are transposed into bit planes
@@ -794,7 +858,8 @@ template <bool P64, bool RAND, int NT, bool TM = false>
 size_t slice_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t planes = RAND ? size_t(P64 ? 64 : 32) * NT * 4 : 0;
-    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * NT * 16) + (NT / 32) * kWarpScratch * 16 + planes;
+    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * NT * 16) + (NT / 32) * kWarpScratch * 16 + planes +
+                     size_t(kHiPlanes) * NT * 4;
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
@@ -868,6 +933,8 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
     const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
     double2* crot = amp_s + (TM ? 0 : kSliceG * NT) + (threadIdx.x >> 5) * kWarpScratch;
+    uint32_t* hi_planes = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * NT) + (NT / 32) * kWarpScratch) +
+                          (RAND ? (P64 ? 64 : 32) * NT : 0);
     SliceAcc<NT, TM> acc{amp_s, 0u};
     if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
     acc.zero();
@@ -900,10 +967,8 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
     const uint32_t blo = uint32_t(base), bhi = uint32_t(base >> 32);
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
-    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
-#pragma unroll
-    for (int i = 0; i < kPlanes; ++i) S[i] = A[i] = B[i] = 0;
-    uint32_t nS = 0, nA = 0, nB = 0;
+    KindCounters<NT> K;
+    K.init(hi_planes + threadIdx.x);
 
     if (tb < te) {
         uint4* tiles = reinterpret_cast<uint4*>(smem);
@@ -932,46 +997,47 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
             // rows software-pipelined one ahead (the read past the last row
-            // stays inside the CTA's shared window and is never used)
+            // stays inside the CTA's shared window and is never used). Both
+            // parity vectors are formed before the jump, so nothing of the
+            // current row is live across it and the next row's loads need no
+            // register copies.
             uint4 na = lds128(a0), nb = lds128(a0 + 16);
             for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint4 ra = na;  // psi, phi, code, Walsh32(psi)
-                const uint4 rb = nb;  // Walsh32(phi), psi_hi, phi_hi, 0
+                const uint32_t code = na.z;  // op | kind flags | end
+                const uint32_t op = nb.w;    // jump-table index (the op again, own word: no masking)
+                uint32_t X, Y;
+                if constexpr (RAND) {
+                    X = planes_parity<NT>(na.x, planes_s);
+                    Y = na.y ? planes_parity<NT>(na.y, planes_s) : 0u;
+                    if constexpr (P64) {
+                        X ^= planes_parity<NT>(nb.y, planes_s + 32 * NT * 4);
+                        if (nb.z) Y ^= planes_parity<NT>(nb.z, planes_s + 32 * NT * 4);
+                    }
+                } else {
+                    uint32_t px, py;
+                    if constexpr (P64) {
+                        px = __popc((na.x & blo) ^ (nb.y & bhi));
+                        py = __popc((na.y & blo) ^ (nb.z & bhi));
+                    } else {
+                        px = __popc(na.x & blo);
+                        py = __popc(na.y & blo);
+                    }
+                    // Walsh32(psi) ^ -parity(psi & base); for P <= 32 the row
+                    // carries ~Walsh32 in its unused high-mask words
+                    X = (px & 1u) ? (P64 ? ~na.w : nb.y) : na.w;
+                    Y = (py & 1u) ? (P64 ? ~nb.x : nb.z) : nb.x;  // (== 0 for one-parity rows)
+                }
                 na = lds128(ad + 32);
                 nb = lds128(ad + 48);
-                const uint32_t op = __shfl_sync(0xFFFFFFFFu, ra.z, 0) & 0xFFu;  // provably warp-uniform -> BRXU
                 uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
-                if constexpr (RAND) {
-                    uint32_t X = planes_parity<NT>(ra.x, planes_s), Y = 0;
-                    if (ra.y) Y = planes_parity<NT>(ra.y, planes_s);
-                    if constexpr (P64) {
-                        X ^= planes_parity<NT>(rb.y, planes_s + 32 * NT * 4);
-                        if (rb.z) Y ^= planes_parity<NT>(rb.z, planes_s + 32 * NT * 4);
-                    }
-                    asm(PZX_SLICE_DISPATCH_ASM_XY
-                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
-                        : "r"(X), "r"(op), "r"(Y));
-                } else {
-                uint32_t pp;
-                if constexpr (P64) pp = __popc((ra.x & blo) ^ (rb.y & bhi)) & 1u;
-                else pp = __popc(ra.x & blo) & 1u;
-                const uint32_t X = ra.w ^ (0u - pp);
-                if constexpr (P64) {
-                    asm(PZX_SLICE_DISPATCH_ASM_P64
-                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
-                        : "r"(X), "r"(op), "r"(ra.y), "r"(rb.x), "r"(blo), "r"(rb.z), "r"(bhi));
-                } else {
-                    asm(PZX_SLICE_DISPATCH_ASM_P32
-                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
-                        : "r"(X), "r"(op), "r"(ra.y), "r"(rb.x), "r"(blo));
-                }
-                }
-                if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
-                    if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
-                    if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
-                    if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
-                    if (ra.z & kEndFlag)
-                        slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, S, A, B, nS, nA, nB);
+                asm(PZX_SLICE_DISPATCH_ASM_XY
+                    : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                    : "r"(X), "r"(op), "r"(Y));
+                if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (code & kSliceLamFlag) K.bump_s(vl);
+                    if (code & kSlicePiFlag) K.bump_a(vpi);
+                    if (code & kSlicePipFlag) K.bump_b(vpip);
+                    if (code & kEndFlag) slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }
             __syncthreads();  // every thread is done with buffer (i & 1)
@@ -1004,7 +1070,8 @@ template <bool TM = false>
 size_t sorted_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * kSliceThreads * 16) +
-                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(kSortedGroups) * 16 * kSortedTableStride;
+                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(kSortedGroups) * 16 * kSortedTableStride +
+                     size_t(kHiPlanes) * kSliceThreads * 4;
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
@@ -1024,6 +1091,7 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
     double2* crot = amp_s + (TM ? 0 : kSliceG * kSliceThreads) + (threadIdx.x >> 5) * kWarpScratch;
     uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * kSliceThreads) +
                                                 (kSliceThreads / 32) * kWarpScratch);
+    uint32_t* hi_planes = tab + kSortedGroups * 16 * (kSortedTableStride / 4);
     SliceAcc<kSliceThreads, TM> acc{amp_s, 0u};
     if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
     acc.zero();
@@ -1062,10 +1130,8 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
     };
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
-    uint32_t S[kPlanes], A[kPlanes], B[kPlanes];
-#pragma unroll
-    for (int i = 0; i < kPlanes; ++i) S[i] = A[i] = B[i] = 0;
-    uint32_t nS = 0, nA = 0, nB = 0;
+    KindCounters<kSliceThreads> K;
+    K.init(hi_planes + threadIdx.x);
     __syncwarp();
 
     if (tb < te) {
@@ -1108,12 +1174,11 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
                     : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
                     : "r"(X), "r"(op), "r"(Y));
                 if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
-                    if (ra.z & kSliceLamFlag) slice_bump(S, ++nS, vl);
-                    if (ra.z & kSlicePiFlag) slice_bump(A, ++nA, vpi);
-                    if (ra.z & kSlicePipFlag) slice_bump(B, ++nB, vpip);
+                    if (ra.z & kSliceLamFlag) K.bump_s(vl);
+                    if (ra.z & kSlicePiFlag) K.bump_a(vpi);
+                    if (ra.z & kSlicePipFlag) K.bump_b(vpip);
                     if (ra.z & kEndFlag)
-                        slice_term_epilogue<kSliceThreads, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, S, A,
-                                                               B, nS, nA, nB);
+                        slice_term_epilogue<kSliceThreads, TM, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }
             __syncthreads();
