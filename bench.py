@@ -252,7 +252,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     kflag = {"auto": 0, "general": P.KERNEL_GENERAL, "gray": P.KERNEL_GRAY, "slice": P.KERNEL_SLICE,
-             "slice_rand": P.KERNEL_SLICE_RAND, "sorted": P.KERNEL_SORTED}[args.kernel]
+             "slice_rand": P.KERNEL_SLICE_RAND, "sorted": P.KERNEL_SORTED, "slice2": P.KERNEL_SLICE2}[args.kernel]
 
     pflag = P.PROB_REAL if cfg.prob_real else P.PROB_ABS2
 
@@ -449,7 +449,7 @@ def main():
     ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand", "sorted"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand", "sorted", "slice2"],
                     help="force one evaluation kernel (default: the library's choice)")
     args = ap.parse_args()
     if args.impl == "reference":

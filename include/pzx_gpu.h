@@ -74,7 +74,8 @@ enum {
     PZX_KERNEL_GRAY = 1u << 9,    /* force the enumerated (low-bit Walsh) kernel   */
     PZX_KERNEL_SLICE = 1u << 10,  /* force the bit-sliced enumerated kernel        */
     PZX_KERNEL_SLICE_RAND = 1u << 11, /* force the plane-XOR bit-sliced kernel for any word list */
-    PZX_KERNEL_SORTED = 1u << 12  /* force sort + bit-sliced Four-Russians kernel (any word list) */
+    PZX_KERNEL_SORTED = 1u << 12, /* force sort + bit-sliced Four-Russians kernel (any word list) */
+    PZX_KERNEL_SLICE2 = 1u << 13  /* force the two-slice (64 assignments / thread) enumerated kernel */
 };
 
 typedef struct pzx_ctx pzx_ctx;

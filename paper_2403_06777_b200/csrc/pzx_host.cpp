@@ -233,10 +233,11 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
     if (h.want_srows) {
         h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
-        // P <= 32: the high-mask words carry ~Walsh32 instead, so the kernel
-        // selects X = parity ? ~W : W with one SEL
+        // P <= 32: the high-mask words carry -(bit 5) of psi / phi instead: the
+        // two-slice kernel's second slice (assignments + 32) has X' = X ^ that
+        auto m5 = [](uint64_t m) { return uint32_t(0) - uint32_t((m >> 5) & 1u); };
         if (h.n_params <= 32)
-            h.srows.push_back(make_uint4(walsh32(phi), ~walsh32(psi), ~walsh32(phi), op));
+            h.srows.push_back(make_uint4(walsh32(phi), m5(psi), m5(phi), op));
         else
             h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), op));
     }
@@ -611,11 +612,12 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
              : (flags & PZX_KERNEL_SLICE)   ? KC_SLICE
              : (flags & PZX_KERNEL_SLICE_RAND) ? KC_SLICER
              : (flags & PZX_KERNEL_SORTED)  ? KC_SORTED
+             : (flags & PZX_KERNEL_SLICE2)  ? KC_SLICE2
                                             : KC_AUTO;
     if (r.kernel != KC_AUTO && !kernel_supported(t->dev, r, r.kernel))
         return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "
                                            "(enumerated kernels need a contiguous batch starting at a multiple "
-                                           "of 16 (gray) or 32 (slice); slice needs terms of <= 127 rows)");
+                                           "of 16 (gray), 32 (slice) or 64 (slice2); slice needs terms of <= 127 rows)");
     KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;

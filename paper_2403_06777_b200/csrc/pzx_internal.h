@@ -64,7 +64,7 @@ struct DevTable {
     int p64 = 0;
     // bit-sliced kernel (only when every term has <= kSegRows rows):
     // rows as 2 x uint4 {psi, phi, op | kind flags | kEndFlag, Walsh32(psi)}, {Walsh32(phi), psi_hi, phi_hi, op}
-    // (n_params <= 32: {Walsh32(phi), ~Walsh32(psi), ~Walsh32(phi), op})
+    // (n_params <= 32: {Walsh32(phi), -(psi bit 5), -(phi bit 5), op})
     // (op = class * 2 + single, pzx_classes.h), constants C''_t * w^(sum of row jbase)
     const uint4* srows = nullptr;
     const double2* sterm_c = nullptr;
@@ -82,7 +82,7 @@ constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 
 constexpr int kSortedLowBits = 4 * kSortedGroups;
 constexpr uint32_t kSortedTableStride = 128 * 4;  // bytes between table rows (128 threads x 4 B)
 
-enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5 };
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5, KC_SLICE2 = 6 };
 
 struct LaunchReq {
     const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1

@@ -534,6 +534,15 @@ __host__ __device__ constexpr uint32_t slice_lut_offset() {
 constexpr uint32_t kTmemCols = 128;
 constexpr size_t kTmemCtaSmem = 51200;  // dynamic smem floor: at most 4 CTAs/SM (= 512 TMEM columns)
 
+// PZX_SLICE2=1 sends large enumerated batches to the two-slice kernel (default off)
+bool slice2_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PZX_SLICE2");
+        return e && std::string(e) == "1";  // measured slower than 16 warps x one slice
+    }();
+    return on;
+}
+
 // PZX_ACC=smem keeps the accumulators in shared memory (A/B comparisons)
 bool tmem_accumulators() {
     static const bool on = [] {
@@ -570,11 +579,12 @@ __device__ __forceinline__ void tmem_sync_fence() {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// warp 0 allocates kTmemCols columns; returns this thread's lane-quarter address
+// warp 0 allocates COLS columns; returns this thread's lane-quarter address
+template <uint32_t COLS = kTmemCols>
 __device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* base_s) {
     if ((threadIdx.x >> 5) == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(base_s)),
-                     "n"(kTmemCols)
+                     "n"(COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -582,10 +592,11 @@ __device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* base_s) {
     return *base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16);
 }
 __device__ __forceinline__ uint32_t tmem_base_of(uint32_t taddr) { return taddr & 0x0000FFFFu; }
+template <uint32_t COLS = kTmemCols>
 __device__ __forceinline__ void tmem_free_cta(uint32_t base) {
     tmem_sync_fence();
     if ((threadIdx.x >> 5) == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kTmemCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
 }
 __device__ __forceinline__ double2 v2d(const uint32_t* v) {
     return make_double2(__hiloint2double(int(v[1]), int(v[0])), __hiloint2double(int(v[3]), int(v[2])));
@@ -792,10 +803,10 @@ __device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const doub
     return v;
 }
 
-template <int NT, bool TM, bool ROLL = false>
-__device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
-                                                    SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
-                                                    uint32_t& J2, uint32_t& Z, KindCounters<NT>& K) {
+// Term epilogue, part 1 (once per warp and term): C from its cp.async slot,
+// the warp's C * w^j table (zeros for Z-marked assignments at 8..15).
+__device__ __forceinline__ void slice_epilogue_begin(TermC& tc, const double2* src, const SmemLut& L,
+                                                     double2* crot) {
     const uint32_t lane = threadIdx.x & 31u;
     const double2 C = termc_take(tc, src);
     if (lane < uint32_t(kCrot)) {
@@ -807,6 +818,14 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
         crot[lane] = v;
     }
     __syncwarp();
+}
+
+// Term epilogue, part 2 (per 32-assignment slice): fold 6*s1 into J, add
+// every live assignment's term value into its accumulator, reset the state.
+template <int NT, bool TM, bool ROLL = false>
+__device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
+                                                     uint32_t& J0, uint32_t& J1, uint32_t& J2, uint32_t& Z,
+                                                     KindCounters<NT>& K) {
     if (K.nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
         const uint32_t w1 = K.S[0], w2 = K.S[0] ^ K.S[1];
         const uint32_t c1 = J1 & w1;
@@ -852,6 +871,14 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
     if (kinds) K.reset();
 }
 
+template <int NT, bool TM, bool ROLL = false>
+__device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
+                                                    SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
+                                                    uint32_t& J2, uint32_t& Z, KindCounters<NT>& K) {
+    slice_epilogue_begin(tc, src, L, crot);
+    slice_epilogue_apply<NT, TM, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
+}
+
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
 template <bool P64, bool RAND, int NT, bool TM = false>
@@ -863,7 +890,7 @@ size_t slice_smem_bytes(const DevTable& t) {
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
-template <int NT, bool TM>
+template <int NT, bool TM, bool FREE = true>
 __device__ __forceinline__ void slice_store_results(const LaunchReq& r, uint64_t off, SliceAcc<NT, TM>& acc) {
     if constexpr (TM) {
         tmem_wait_st();
@@ -875,7 +902,7 @@ __device__ __forceinline__ void slice_store_results(const LaunchReq& r, uint64_t
 #pragma unroll
             for (int q = 0; q < 8; ++q) store_result(r, off + 8 * ch + q, v2d(v + 4 * q));
         }
-        tmem_free_cta(tmem_base_of(acc.taddr));
+        if constexpr (FREE) tmem_free_cta(tmem_base_of(acc.taddr));
     } else {
 #pragma unroll 4
         for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, acc.amp_s[g * NT + threadIdx.x]);
@@ -1022,10 +1049,8 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         px = __popc(na.x & blo);
                         py = __popc(na.y & blo);
                     }
-                    // Walsh32(psi) ^ -parity(psi & base); for P <= 32 the row
-                    // carries ~Walsh32 in its unused high-mask words
-                    X = (px & 1u) ? (P64 ? ~na.w : nb.y) : na.w;
-                    Y = (py & 1u) ? (P64 ? ~nb.x : nb.z) : nb.x;  // (== 0 for one-parity rows)
+                    X = na.w ^ (0u - (px & 1u));  // Walsh32(psi) ^ -parity(psi & base)
+                    Y = nb.x ^ (0u - (py & 1u));  // (== 0 for one-parity rows: phi == 0)
                 }
                 na = lds128(ad + 32);
                 nb = lds128(ad + 48);
@@ -1048,6 +1073,124 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
         }
     }
     slice_store_results<NT, TM>(r, off, acc);
+}
+
+// ---------------------------------------------------- two-slice kernel ----
+// Enumerated batches, 64 assignments per thread: slice a = base + g, slice b
+// = base + 32 + g (base % 64 == 0). Both slices share the row load, the
+// parity POPCs (X_b = X_a ^ -(psi bit 5)), the jump and the flag tests, and
+// the generated XY2 bodies run the two LOP3 chains interleaved (ILP 2), so the
+// per-row overhead is paid once per 64 assignments. Accumulators: 256 TMEM
+// columns per 128-thread CTA (2 CTAs = 8 warps per SM, each with twice the
+// independent work of the one-slice kernel).
+constexpr uint32_t kTmemCols2 = 256;
+constexpr size_t kTmemCtaSmem2 = 80 * 1024;  // dynamic smem floor: at most 2 CTAs/SM (= 512 TMEM columns)
+
+template <bool P64>
+size_t slice2_smem_bytes(const DevTable& t) {
+    const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    const size_t b = amp_off + (kSliceThreads / 32) * kWarpScratch * 16 + 2 * size_t(kHiPlanes) * kSliceThreads * 4;
+    return b > kTmemCtaSmem2 ? b : kTmemCtaSmem2;
+}
+
+template <bool P64>
+__global__ void __launch_bounds__(kSliceThreads, 2) k_eval_slice2(const DevTable t, const LaunchReq r) {
+    constexpr int NT = kSliceThreads;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t tmem_base_s;
+    const SmemLut L = kernel_prologue(t, smem, slice_lut_offset<P64>());
+    const uint32_t amp_off = (slice_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    double2* crot = reinterpret_cast<double2*>(smem + amp_off) + (threadIdx.x >> 5) * kWarpScratch;
+    uint32_t* hi_planes = reinterpret_cast<uint32_t*>(smem + amp_off + (NT / 32) * kWarpScratch * 16);
+    SliceAcc<NT, true> acc_a{nullptr, 0u}, acc_b{nullptr, 0u};
+    acc_a.taddr = tmem_alloc_cta<kTmemCols2>(&tmem_base_s);
+    acc_b.taddr = acc_a.taddr + kTmemCols;
+    acc_a.zero();
+    acc_b.zero();
+
+    uint64_t tb, te;
+    term_range(r, tb, te);
+    const uint64_t off = (uint64_t(blockIdx.x) * NT + threadIdx.x) * (2 * kSliceG);
+    const uint64_t base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    const uint32_t blo = uint32_t(base), bhi = uint32_t(base >> 32);
+
+    uint32_t Ja0 = 0, Ja1 = 0, Ja2 = 0, Za = 0, Jb0 = 0, Jb1 = 0, Jb2 = 0, Zb = 0;
+    KindCounters<NT> Ka, Kb;
+    Ka.init(hi_planes + threadIdx.x);
+    Kb.init(hi_planes + kHiPlanes * NT + threadIdx.x);
+
+    if (tb < te) {
+        uint4* tiles = reinterpret_cast<uint4*>(smem);
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSliceTile * 32);
+        const uint32_t tiles_s = smem_u32(tiles);
+        const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
+        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        auto issue = [&](uint32_t tile) {
+            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
+            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint32_t bytes = uint32_t(n) * 32u;
+            uint64_t* bar = &bars[tile & 1];
+            mbar_expect_tx(bar, bytes);
+            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.srows + rr * 2, bytes, bar);
+        };
+        if (threadIdx.x == 0) {
+            if (ntiles > 0) issue(0);
+            if (ntiles > 1) issue(1);
+        }
+        TermC tc;
+        termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
+        for (uint32_t i = 0; i < ntiles; ++i) {
+            mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
+            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
+            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint32_t aend = a0 + n * 32;
+            uint4 na = lds128(a0), nb = lds128(a0 + 16);
+            for (uint32_t ad = a0; ad < aend; ad += 32) {
+                const uint32_t code = na.z;
+                const uint32_t op = nb.w;
+                uint32_t px, py, m5x, m5y;
+                if constexpr (P64) {
+                    px = __popc((na.x & blo) ^ (nb.y & bhi));
+                    py = __popc((na.y & blo) ^ (nb.z & bhi));
+                    m5x = 0u - ((na.x >> 5) & 1u);
+                    m5y = 0u - ((na.y >> 5) & 1u);
+                } else {
+                    px = __popc(na.x & blo);
+                    py = __popc(na.y & blo);
+                    m5x = nb.y;  // host-precomputed -(psi bit 5), -(phi bit 5)
+                    m5y = nb.z;
+                }
+                const uint32_t Xa = na.w ^ (0u - (px & 1u)), Ya = nb.x ^ (0u - (py & 1u));
+                const uint32_t Xb = Xa ^ m5x, Yb = Ya ^ m5y;
+                na = lds128(ad + 32);
+                nb = lds128(ad + 48);
+                uint32_t vla, vpia, vpipa, vlb, vpib, vpipb;
+                asm(PZX_SLICE_DISPATCH_ASM_XY2
+                    : "+r"(Ja0), "+r"(Ja1), "+r"(Ja2), "+r"(Za), "+r"(Jb0), "+r"(Jb1), "+r"(Jb2), "+r"(Zb),
+                      "=r"(vla), "=r"(vpia), "=r"(vpipa), "=r"(vlb), "=r"(vpib), "=r"(vpipb)
+                    : "r"(Xa), "r"(Ya), "r"(Xb), "r"(Yb), "r"(op));
+                if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (code & kSliceLamFlag) { Ka.bump_s(vla); Kb.bump_s(vlb); }
+                    if (code & kSlicePiFlag) { Ka.bump_a(vpia); Kb.bump_a(vpib); }
+                    if (code & kSlicePipFlag) { Ka.bump_b(vpipa); Kb.bump_b(vpipb); }
+                    if (code & kEndFlag) {
+                        slice_epilogue_begin(tc, t.sterm_c, L, crot);
+                        slice_epilogue_apply<NT, true>(L, crot, acc_a, Ja0, Ja1, Ja2, Za, Ka);
+                        slice_epilogue_apply<NT, true>(L, crot, acc_b, Jb0, Jb1, Jb2, Zb, Kb);
+                    }
+                }
+            }
+            __syncthreads();  // every thread is done with buffer (i & 1)
+            if (threadIdx.x == 0 && i + 2 < ntiles) {
+                fence_proxy_async();
+                issue(i + 2);
+            }
+        }
+    }
+    slice_store_results<NT, true, false>(r, off, acc_a);
+    slice_store_results<NT, true, false>(r, off + kSliceG, acc_b);
+    tmem_free_cta<kTmemCols2>(tmem_base_of(acc_a.taddr));
 }
 
 // ------------------------------------------------------ sorted kernel ----
@@ -1309,6 +1452,13 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
         kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
+    if (kc == KC_SLICE2) {
+        const size_t sm = slice2_smem_bytes<P64>(t);
+        cudaError_t e = cudaFuncSetAttribute(k_eval_slice2<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        k_eval_slice2<P64><<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        return cudaGetLastError();
+    }
     if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         const bool small = slice_threads(r) == 32;
@@ -1337,6 +1487,9 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     if (r.kernel != KC_AUTO) return r.kernel;
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
+    if (enumerated && t.slice_ok && (r.first % (2 * kSliceG)) == 0 && slice_threads(r) == kSliceThreads &&
+        tmem_accumulators() && slice2_enabled())
+        return KC_SLICE2;
     if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
     // arbitrary word lists: sort, then the bit-sliced kernel with per-thread
@@ -1348,6 +1501,7 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
+    if (kc == KC_SLICE2) return enumerated && t.slice_ok && (r.first % (2 * kSliceG)) == 0;
     if (kc == KC_SLICER) return t.slice_ok != 0;
     if (kc == KC_SORTED) return t.sorted_ok != 0 && r.d_asg != nullptr;
     if (kc == KC_GRAY) return enumerated && (r.first % kGray) == 0;
@@ -1361,7 +1515,8 @@ int slice_threads(const LaunchReq& r) {
 }
 
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = kc == KC_SORTED                   ? uint64_t(kSliceThreads) * kSliceG
+    const uint64_t per = kc == KC_SLICE2                   ? uint64_t(kSliceThreads) * 2 * kSliceG
+                       : kc == KC_SORTED                   ? uint64_t(kSliceThreads) * kSliceG
                        : (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(slice_threads(r)) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
@@ -1376,7 +1531,12 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
     const bool tm = tmem_accumulators();
-    if (kc == KC_SORTED) {
+    if (kc == KC_SLICE2) {
+        sm = t.p64 ? slice2_smem_bytes<true>(t) : slice2_smem_bytes<false>(t);
+        auto kern = t.p64 ? k_eval_slice2<true> : k_eval_slice2<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+    } else if (kc == KC_SORTED) {
         sm = tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t);
         auto kern = tm ? k_eval_sorted<true> : k_eval_sorted<false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

@@ -216,25 +216,52 @@ def case_body(op, p64=False, y_in=False):
     return L
 
 
+def _rename(line, mp):
+    """Substitute operand / temp names (whole tokens) in one PTX line."""
+    import re
+    return re.sub(r"%\d+|\b(?:c0|c1|w1|yy)\b", lambda m: mp.get(m.group(0), m.group(0)), line)
+
+
+# two-slice variant: 64 assignments per thread, slices a and b share X/Y-free
+# row data and the jump; operands
+#   %0-%3 J0 J1 J2 Z (a), %4-%7 (b), %8-%10 vl vpi vpip (a), %11-%13 (b),
+#   %14 Xa, %15 Ya, %16 Xb, %17 Yb, %18 op
+_DUAL_A = {"%4": "%8", "%5": "%9", "%6": "%10", "%7": "%14", "%9": "%15"}
+_DUAL_B = {"%0": "%4", "%1": "%5", "%2": "%6", "%3": "%7", "%4": "%11", "%5": "%12", "%6": "%13",
+           "%7": "%16", "%9": "%17", "c0": "d0", "c1": "d1", "w1": "x1"}
+
+
+def case_body_dual(op):
+    a = [_rename(ln, _DUAL_A) for ln in case_body(op, False, True)]
+    b = [_rename(ln, _DUAL_B) for ln in case_body(op, False, True)]
+    out = []
+    for i in range(max(len(a), len(b))):  # interleave the two independent chains
+        if i < len(a):
+            out.append(a[i])
+        if i < len(b):
+            out.append(b[i])
+    return out
+
+
 def kind_flags(op):
     """Row code-word flag bits the C++ side reads: bit 8 lambda, 9 pi, 10 pi'."""
     _, _, _, lam, pi, pip, _ = slice_op(op)
     return (1 << 8 if lam else 0) | (1 << 9 if pi else 0) | (1 << 10 if pip else 0)
 
 
-def _asm_block(name, p64, y_in=False):
+def _asm_block(name, p64, y_in=False, dual=False):
     n = 129
     # identical case bodies share one label (smaller code, fewer I-cache misses)
     bodies, label_of = {}, []
     for i in range(n):
-        key = tuple(case_body(i, p64, y_in))
+        key = tuple(case_body_dual(i) if dual else case_body(i, p64, y_in))
         if key not in bodies:
             bodies[key] = len(bodies)
         label_of.append(bodies[key])
     lines = [f"#define {name} \\"]
-    body = ["{", ".reg .b32 c0, c1, w1, yy;",
+    body = ["{", ".reg .b32 c0, c1, w1, yy, d0, d1, x1;" if dual else ".reg .b32 c0, c1, w1, yy;",
             "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
-            "brx.idx.uni %8, ts%=;"]
+            f"brx.idx.uni {'%18' if dual else '%8'}, ts%=;"]
     for key, lab in sorted(bodies.items(), key=lambda kv: kv[1]):
         body.append(f"L{lab}_%=:")
         body.extend(key)
@@ -256,8 +283,11 @@ def generate() -> str:
     b32, n32 = _asm_block("PZX_SLICE_DISPATCH_ASM_P32", False)
     b64, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_P64", True)
     bxy, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_XY", False, True)
+    bxy2, _ = _asm_block("PZX_SLICE_DISPATCH_ASM_XY2", False, True, dual=True)
     lines += [f"// {n32} distinct case bodies",
-              "// _XY variant (random batches): operand %9 is Y itself"] + b32 + b64 + bxy
+              "// _XY variant: operand %9 is Y itself",
+              "// _XY2 variant (two slices): %0-%3 J0 J1 J2 Z (a), %4-%7 (b), %8-%10 vl vpi vpip (a),",
+              "//   %11-%13 (b), %14 Xa, %15 Ya, %16 Xb, %17 Yb, %18 op"] + b32 + b64 + bxy + bxy2
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")

@@ -299,6 +299,7 @@ KERNEL_GRAY = 1 << 9
 KERNEL_SLICE = 1 << 10
 KERNEL_SLICE_RAND = 1 << 11
 KERNEL_SORTED = 1 << 12
+KERNEL_SLICE2 = 1 << 13
 
 
 class DeviceTable:
@@ -494,6 +495,6 @@ __all__ = [
     "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
-    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "slice_op_table",
+    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
 ]
 _ = builtins

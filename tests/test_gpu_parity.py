@@ -94,9 +94,11 @@ def test_enumerated_range_kernels(ctx, path):
     a_gray = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GRAY)
     a_gen = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GENERAL)
     a_slice = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_SLICE)
+    a_slice2 = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_SLICE2)
     assert_close(a_gray, z["amp"])
     assert_close(a_gen, z["amp"])
     assert_close(a_slice, z["amp"])
+    assert_close(a_slice2, z["amp"])
     # explicit contiguous word list (what pzx_evaluate sees from a user sweep)
     assert_close(ctx.evaluate_batch(t, np.arange(n, dtype=np.uint64)), z["amp"])
     # unaligned start (general kernel) and ragged length
@@ -116,6 +118,24 @@ def test_slice_kernel_vs_oracle(ctx, P_):
     _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
     assert_close(amp[idx], want)
     assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
+
+
+@pytest.mark.parametrize("P_", [3, 6, 12, 20, 33, 64])
+def test_slice2_kernel_vs_oracle(ctx, P_):
+    """Two-slice (64 assignments / thread, TMEM accumulators) enumerated kernel."""
+    e = synth.generate(P_, 700, 1, 40, 900 + P_)
+    t = ctx.compile_bit_table(e)
+    n = 1 << min(P_, 13)
+    first = 0 if P_ <= 13 else 64 * 4321
+    amp = ctx.evaluate_range(t, first, n, flags=P.KERNEL_SLICE2)
+    words = np.arange(first, first + n, dtype=np.uint64)
+    idx = np.random.default_rng(P_).choice(n, min(n, 96), replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+    assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
+    # term-chunked grid (partials + fixed-order reduction) on a long batch
+    amp2 = ctx.evaluate_range(t, first, 1 << 16, flags=P.KERNEL_SLICE2)
+    assert_close(amp2[:n], amp, 1e-13)
 
 
 @pytest.mark.parametrize("P_", [7, 20, 32, 33, 64])

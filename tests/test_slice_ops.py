@@ -30,10 +30,10 @@ def test_generated_include_is_current():
     assert open(G.OUT).read() == G.generate()
 
 
-def _bodies(p64=False):
+def _bodies(p64=False, name=None):
     text = G.generate()
-    name = "PZX_SLICE_DISPATCH_ASM_P64" if p64 else "PZX_SLICE_DISPATCH_ASM_P32"
-    block = text[text.index(name):]
+    name = name or ("PZX_SLICE_DISPATCH_ASM_P64" if p64 else "PZX_SLICE_DISPATCH_ASM_P32")
+    block = text[text.index(name + " "):]
     block = block[:block.index("\n\n")]
     lines = re.findall(r'"(.*?)\\n"', block)
     table = next(ln for ln in lines if ".branchtargets" in ln)
@@ -124,3 +124,35 @@ def test_jbase_plus_w_is_the_exact_exponent():
             assert bool((lam >> v) & 1) == (kind == G.KLAMBDA)
             assert bool((pi >> v) & 1) == (kind == G.KPI)
             assert bool((pip >> v) & 1) == (kind == G.KPIP)
+
+
+def test_two_slice_chains_are_two_independent_mod8_adds():
+    """XY2 (two-slice kernel): slice a and slice b updated independently, each
+    exactly like the one-slice chain, from their own X / Y."""
+    bodies = _bodies(name="PZX_SLICE_DISPATCH_ASM_XY2")
+    assert len(bodies) == 129
+    for op in range(129):
+        jb, w, z, lam, pi, pip, _ = G.slice_op(op)
+        single = op < 128 and (op & 1)
+        for va in range(4):
+            for vb in range(4):
+                pa, qa, pb, qb = va & 1, va >> 1, vb & 1, vb >> 1
+                if single and (qa or qb):
+                    continue
+                for ja in (0, 5):
+                    for jbv in (3, 6):
+                        regs = {"%0": ja & 1, "%1": (ja >> 1) & 1, "%2": (ja >> 2) & 1, "%3": 0,
+                                "%4": jbv & 1, "%5": (jbv >> 1) & 1, "%6": (jbv >> 2) & 1, "%7": 1,
+                                "%8": 0, "%9": 0, "%10": 0, "%11": 0, "%12": 0, "%13": 0,
+                                "%14": pa, "%15": qa, "%16": pb, "%17": qb}
+                        out = _run(bodies[op], regs)
+                        for (v, j0, J, Zr, Zin, L, PI, PIP) in (
+                                (va, ja, ("%0", "%1", "%2"), "%3", 0, "%8", "%9", "%10"),
+                                (vb, jbv, ("%4", "%5", "%6"), "%7", 1, "%11", "%12", "%13")):
+                            jn = out[J[0]] | (out[J[1]] << 1) | (out[J[2]] << 2)
+                            if not (z >> v) & 1:
+                                assert jn == (j0 + w[v]) % 8, (op, v)
+                            assert out[Zr] == (Zin | ((z >> v) & 1))
+                            assert out[L] == (lam >> v) & 1
+                            assert out[PI] == (pi >> v) & 1
+                            assert out[PIP] == (pip >> v) & 1
