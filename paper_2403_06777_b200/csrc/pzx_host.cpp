@@ -630,9 +630,12 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         uint64_t spread = 0;
         void* tmp8 = static_cast<unsigned char*>(ctx->d_sort) + sort_scratch_bytes(r.n);
         if ((st = cuda_err(ctx, sorted_max_spread(r.d_sorted, r.n, tmp8, &spread, r.stream, &ctx->launches), "spread"))) return st;
-        if (spread >= (uint64_t(1) << kSortedLowBits)) {  // too sparse for two high parts per thread
+        // groups of 32 sorted words must span < 2^(4 G): 16 table bits for dense
+        // batches, 24 (wide tables) for sparse ones such as 2^16 random 32-bit words
+        r.sorted_groups = spread < (uint64_t(1) << (4 * kSortedGroups)) ? kSortedGroups : kSortedGroupsWide;
+        if (spread >= (uint64_t(1) << (4 * kSortedGroupsWide))) {  // too sparse for two high parts per thread
             if (r.kernel == KC_SORTED)
-                return set_err(ctx, PZX_E_INVALID, "sorted kernel: batch too sparse (32-word groups span >= 2^16)");
+                return set_err(ctx, PZX_E_INVALID, "sorted kernel: batch too sparse (32-word groups span >= 2^24)");
             kc = KC_GENERAL;
             r.d_sorted = nullptr;
             r.d_perm = nullptr;
@@ -645,7 +648,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
     constexpr int kWaves = 8;
-    const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc, slice_threads(r));
+    const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc, slice_threads(r), r.sorted_groups);
     const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;

@@ -78,7 +78,8 @@ struct DevTable {
     int sorted_ok = 0;
 };
 
-constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables
+constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables (dense batches)
+constexpr int kSortedGroupsWide = 6;          // parameters 0..23 via tables (sparse batches, e.g. 2^16 of 2^32)
 constexpr int kSortedLowBits = 4 * kSortedGroups;
 constexpr uint32_t kSortedTableStride = 128 * 4;  // bytes between table rows (128 threads x 4 B)
 
@@ -101,6 +102,7 @@ struct LaunchReq {
     int n_chunks = 1;
     // KC_SORTED: the batch sorted by (masked) word; results go to d_perm[i]
     const uint64_t* d_sorted = nullptr;
+    int sorted_groups = kSortedGroups;  // Four-Russians table groups of the sorted kernel (4 or 6)
     const uint32_t* d_perm = nullptr;
 };
 
@@ -117,7 +119,7 @@ cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, v
 // Grid policy helpers (host)
 int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
-int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt);
+int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_groups = kSortedGroups);
 int slice_threads(const LaunchReq& r);
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 

@@ -1209,11 +1209,11 @@ __host__ __device__ constexpr uint32_t sorted_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
-template <bool TM = false>
+template <bool TM = false, int G = kSortedGroups>
 size_t sorted_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * kSliceThreads * 16) +
-                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(kSortedGroups) * 16 * kSortedTableStride +
+                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(G) * 16 * kSortedTableStride +
                      size_t(kHiPlanes) * kSliceThreads * 4;
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
@@ -1224,8 +1224,10 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     return v;
 }
 
-template <bool TM = false>
-__global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const DevTable t, const LaunchReq r) {
+template <bool TM = false, int G = kSortedGroups>
+__global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eval_sorted(const DevTable t,
+                                                                                       const LaunchReq r) {
+    constexpr int kLow = 4 * G;  // parameters 0 .. kLow-1 through the per-thread tables
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint32_t tmem_base_s;
     const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset());
@@ -1234,7 +1236,7 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
     double2* crot = amp_s + (TM ? 0 : kSliceG * kSliceThreads) + (threadIdx.x >> 5) * kWarpScratch;
     uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * kSliceThreads) +
                                                 (kSliceThreads / 32) * kWarpScratch);
-    uint32_t* hi_planes = tab + kSortedGroups * 16 * (kSortedTableStride / 4);
+    uint32_t* hi_planes = tab + G * 16 * (kSortedTableStride / 4);
     SliceAcc<kSliceThreads, TM> acc{amp_s, 0u};
     if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
     acc.zero();
@@ -1249,14 +1251,14 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
         const uint64_t idx = off + g < r.n ? off + g : r.n - 1;  // pad with the last word (keeps order)
         w[g] = uint32_t(r.d_sorted[idx]);
     }
-    const uint32_t hmask = ~((1u << kSortedLowBits) - 1u);
-    const uint32_t H0 = w[0] & hmask, H1 = H0 + (1u << kSortedLowBits);
-    uint32_t M = 0;  // assignments whose high part is H1 (the host guarantees spread < 2^16)
+    const uint32_t hmask = ~((1u << kLow) - 1u);
+    const uint32_t H0 = w[0] & hmask, H1 = H0 + (1u << kLow);
+    uint32_t M = 0;  // assignments whose high part is H1 (the host guarantees spread < 2^kLow)
 #pragma unroll
     for (int g = 0; g < 32; ++g) M |= uint32_t((w[g] & hmask) != H0) << g;
     transpose32(w);  // w[i] = plane i (bit g = bit i of word g)
 #pragma unroll
-    for (int k = 0; k < kSortedGroups; ++k) {
+    for (int k = 0; k < G; ++k) {
         uint32_t e[16];
         e[0] = 0;
 #pragma unroll
@@ -1266,8 +1268,11 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? 4 : 1) k_eval_sorted(const
     }
     const uint32_t tab_s = smem_u32(tab) + threadIdx.x * 4;
     auto parity_vec = [&](uint32_t mask, uint32_t o01, uint32_t o23) -> uint32_t {
-        const uint32_t x = lds32(tab_s + (o01 & 0xFFFFu)) ^ lds32(tab_s + (o01 >> 16)) ^
-                           lds32(tab_s + (o23 & 0xFFFFu)) ^ lds32(tab_s + (o23 >> 16));
+        uint32_t x = lds32(tab_s + (o01 & 0xFFFFu)) ^ lds32(tab_s + (o01 >> 16)) ^
+                     lds32(tab_s + (o23 & 0xFFFFu)) ^ lds32(tab_s + (o23 >> 16));
+#pragma unroll
+        for (int k = 4; k < G; ++k)  // groups past the row record's 4 precomputed offsets
+            x ^= lds32(tab_s + (k * 16u + ((mask >> (4 * k)) & 15u)) * kSortedTableStride);
         const uint32_t p0 = __popc(mask & H0) & 1u, p1 = __popc(mask & H1) & 1u;
         return x ^ (0u - p0) ^ (M & (0u - (p0 ^ p1)));
     };
@@ -1445,8 +1450,12 @@ template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
     const bool tm = tmem_accumulators();
     if (kc == KC_SORTED) {
-        const size_t sm = tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t);
-        auto kern = tm ? k_eval_sorted<true> : k_eval_sorted<false>;
+        const bool wide = r.sorted_groups > kSortedGroups;
+        const size_t sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide>(t)
+                                     : sorted_smem_bytes<false, kSortedGroupsWide>(t))
+                               : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
+        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide> : k_eval_sorted<false, kSortedGroupsWide>)
+                         : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
@@ -1524,7 +1533,7 @@ int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
 }
 
 
-int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
+int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_groups) {
     const bool lng = t.max_rows > uint32_t(kSegRows);
     int nb = 0;
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
@@ -1537,8 +1546,11 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_SORTED) {
-        sm = tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t);
-        auto kern = tm ? k_eval_sorted<true> : k_eval_sorted<false>;
+        const bool wide = sorted_groups > kSortedGroups;
+        sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide>(t) : sorted_smem_bytes<false, kSortedGroupsWide>(t))
+                  : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
+        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide> : k_eval_sorted<false, kSortedGroupsWide>)
+                         : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_SLICE || kc == KC_SLICER) {

@@ -172,6 +172,22 @@ def test_sorted_kernel_vs_oracle(ctx, P_):
     assert_close(ctx.evaluate_batch(t, words), amp, 1e-13)
 
 
+@pytest.mark.parametrize("P_,n", [(28, 4096 + 5), (32, (1 << 16) + 33)])
+def test_sorted_kernel_wide_tables(ctx, P_, n):
+    """Sparse batches (C5-like: 2^16 random 32-bit words): 32-word groups span
+    2^16..2^24, so the sorted kernel uses 6 Four-Russians groups (24 bits)."""
+    e = synth.generate(P_, 300, 1, 40, 1100 + P_)
+    t = ctx.compile_bit_table(e)
+    rng = np.random.default_rng(P_)
+    words = rng.integers(0, 2**64, n, dtype=np.uint64)
+    amp = ctx.evaluate_batch(t, words, flags=P.KERNEL_SORTED)
+    idx = rng.choice(n, 48, replace=False)
+    _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
+    assert_close(amp, ctx.evaluate_batch(t, words, flags=P.KERNEL_GENERAL), 1e-13)
+    assert_close(ctx.evaluate_batch(t, words), amp, 1e-13)
+
+
 def test_sorted_kernel_rejects_sparse_batches(ctx):
     e = synth.generate(32, 64, 1, 20, 9)
     t = ctx.compile_bit_table(e)
