@@ -385,6 +385,16 @@ def run_ours(args):
                 cpu = {"value": v, "unit": "evals/s", "cores": thr, "kind": kind,
                        "sample": f"{n} assignments (evenly spaced) of the {cfg.n_assign}-assignment batch, "
                                  f"{note}, {el:.1f}s on {thr} threads"}
+                # SURVEY §8d baseline A asks for 1 core and all cores
+                v1, _, _, n1, el1, _ = cpu_reference_rate(expr, cfg, seconds=max(2.0, args.cpu_seconds / 4),
+                                                           threads=1)
+                cpu["single_core"] = {"value": v1, "unit": "evals/s", "cores": 1,
+                                      "sample": f"{n1} assignments, {el1:.1f}s on 1 thread"}
+                # baseline B (non-parametric per-assignment re-reduction) cannot run
+                cpu["baseline_b"] = {"value": None, "kind": "non-parametric re-reduction",
+                                     "reason": "not measurable: the reference ships no circuit reducer "
+                                               "(no clifford_simp / BSS decomposer; dense_semantics is declared "
+                                               "in dense.hpp without a definition), SURVEY §8d B"}
             except Exception as ex:  # the baseline must not kill the GPU number
                 cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                        "sample": f"failed: {ex}"}

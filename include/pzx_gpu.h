@@ -173,6 +173,12 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
                                uint32_t flags, void* stream);
+/* Marginal summing (sim-driver): out[i] = sum over b < 2^m of
+ * prob(fixed[i] | b), the don't-care outputs being the low m parameters
+ * (fixed[i] must have them clear); prob = |amp|^2, or Re(amp) with
+ * PZX_PROB_REAL. Deterministic (fixed-order reductions). Kernel flags apply. */
+pzx_status pzx_marginal_sum(pzx_ctx* ctx, const pzx_table* t, const uint64_t* fixed, uint64_t n_fixed,
+                            uint32_t m, uint32_t flags, double* out);
 /* prob from amplitudes on device (after a cross-GPU sum of partials). */
 pzx_status pzx_amp_to_prob_device(pzx_ctx* ctx, const double* d_amp, uint64_t n,
                                   double* d_prob, uint32_t flags, void* stream);

@@ -877,6 +877,72 @@ pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, 
     return eval_host(ctx, t, nullptr, first, n, amp, prob, flags);
 }
 
+// Marginal summing: out[i] = sum over b < 2^m of prob(fixed[i] | b),
+// prob = |amp|^2 (default) or Re(amp) (PZX_PROB_REAL). The don't-care outputs
+// are the low m parameters. Large groups run as enumerated ranges (bit-sliced
+// kernel); small groups are expanded into one word list per block of
+// patterns. Every reduction is fixed-order (deterministic).
+pzx_status pzx_marginal_sum(pzx_ctx* ctx, const pzx_table* t, const uint64_t* fixed, uint64_t n_fixed, uint32_t m,
+                            uint32_t flags, double* out) {
+    if (!ctx || !t || (n_fixed && (!fixed || !out))) return PZX_E_INVALID;
+    if (m > 40) return set_err(ctx, PZX_E_CAPACITY, "marginal_sum: more than 2^40 summed assignments per pattern");
+    if (n_fixed == 0) return PZX_OK;
+    const uint64_t G = uint64_t(1) << m, low = G - 1;
+    for (uint64_t i = 0; i < n_fixed; ++i)
+        if (fixed[i] & low) return set_err(ctx, PZX_E_INVALID, "marginal_sum: fixed words must have the low m bits clear");
+    if (flags & PZX_PROB_ABS2 && flags & PZX_PROB_REAL) return set_err(ctx, PZX_E_INVALID, "marginal_sum: one prob mode");
+    const uint32_t pf = (flags & PZX_PROB_REAL) ? PZX_PROB_REAL : PZX_PROB_ABS2;
+    const uint32_t kflags = (flags & ~(PZX_PROB_ABS2 | PZX_PROB_REAL)) | pf;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    constexpr uint64_t kBlock = uint64_t(1) << 22;  // assignments per evaluation launch
+    double* d_out = nullptr;
+    if ((st = cuda_err(ctx, cudaMalloc(reinterpret_cast<void**>(&d_out), n_fixed * 8), "alloc marginals"))) return st;
+    auto fail = [&](pzx_status s) { cudaFree(d_out); return s; };
+    if ((st = cuda_err(ctx, grow(&ctx->d_prob, &ctx->prob_cap, std::min(G, kBlock) * std::max<uint64_t>(1, kBlock / std::max(G, uint64_t(1))) * 8 + 8), "alloc prob"))) return fail(st);
+    double* d_prob = static_cast<double*>(ctx->d_prob);
+    LaunchReq r;
+    r.stream = ctx->stream;
+    r.term_begin = 0;
+    r.term_end = t->dev.n_terms;
+    r.prob_mode = prob_mode_of(pf);
+    r.d_prob = d_prob;
+    if (G >= uint64_t(1) << 12) {
+        // per pattern: enumerated sub-ranges of <= kBlock words, partial sums accumulated in order
+        for (uint64_t i = 0; i < n_fixed; ++i) {
+            for (uint64_t b0 = 0; b0 < G; b0 += kBlock) {
+                r.first = fixed[i] + b0;
+                r.n = std::min(kBlock, G - b0);
+                r.d_asg = nullptr;
+                r.d_amp = nullptr;
+                if ((st = run_eval(ctx, t, r, kflags))) return fail(st);
+                if ((st = cuda_err(ctx, launch_segment_sum(d_prob, r.n, 1, d_out + i, b0 > 0, ctx->stream, &ctx->launches), "segment sum"))) return fail(st);
+            }
+        }
+    } else {
+        const uint64_t per = kBlock >> m;  // patterns per block
+        if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, (per << m) * 8 + per * 8), "alloc words"))) return fail(st);
+        uint64_t* d_words = static_cast<uint64_t*>(ctx->d_asg);
+        uint64_t* d_fix = d_words + (per << m);
+        for (uint64_t p0 = 0; p0 < n_fixed; p0 += per) {
+            const uint64_t np = std::min(per, n_fixed - p0);
+            if ((st = cuda_err(ctx, cudaMemcpyAsync(d_fix, fixed + p0, np * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D patterns"))) return fail(st);
+            if ((st = cuda_err(ctx, launch_expand_words(d_fix, np, m, d_words, ctx->stream, &ctx->launches), "expand"))) return fail(st);
+            r.first = 0;
+            r.n = np << m;
+            r.d_asg = d_words;
+            r.d_amp = nullptr;
+            r.words_contiguous = 0;
+            if ((st = run_eval(ctx, t, r, kflags))) return fail(st);
+            if ((st = cuda_err(ctx, launch_segment_sum(d_prob, G, np, d_out + p0, 0, ctx->stream, &ctx->launches), "segment sum"))) return fail(st);
+        }
+    }
+    st = cuda_err(ctx, cudaMemcpyAsync(out, d_out, n_fixed * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H marginals");
+    if (!st) st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "marginal_sum");
+    cudaFree(d_out);
+    return st;
+}
+
 pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,

@@ -131,6 +131,10 @@ cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int
                                cudaStream_t s, uint64_t* launches);
 cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_t n,
                                uint8_t* d_out, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_expand_words(const uint64_t* d_fixed, uint64_t n_fixed, uint32_t m, uint64_t* d_words,
+                                cudaStream_t s, uint64_t* launches);
+cudaError_t launch_segment_sum(const double* d_in, uint64_t len, uint64_t n_seg, double* d_out, int accumulate,
+                               cudaStream_t s, uint64_t* launches);
 cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_t n,
                                uint32_t* d_out5, cudaStream_t s, uint64_t* launches);
 

@@ -1661,6 +1661,50 @@ cudaError_t launch_amp_to_prob(const double2* amp, uint64_t n, double* prob, int
     return cudaGetLastError();
 }
 
+// ---- marginal summing (sim-driver epilogue) ----------------
+// words[p * G + b] = fixed[p] | b, b < G = 2^m
+__global__ void k_expand_words(const uint64_t* __restrict__ fixed, uint64_t n_fixed, uint32_t m, uint64_t* words) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= (n_fixed << m)) return;
+    words[i] = fixed[i >> m] | (i & ((uint64_t(1) << m) - 1));
+}
+
+// out[s] (+)= sum of in[s * len .. s * len + len - 1]: one CTA per segment,
+// strided per-thread sums then a fixed-order tree -- deterministic
+__global__ void k_segment_sum(const double* __restrict__ in, uint64_t len, uint64_t n_seg, double* out,
+                              int accumulate) {
+    __shared__ double red[256];
+    const uint64_t s = blockIdx.x;
+    if (s >= n_seg) return;
+    const double* p = in + s * len;
+    double acc = 0.0;
+    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) acc += p[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[s] = accumulate ? out[s] + red[0] : red[0];
+}
+
+cudaError_t launch_expand_words(const uint64_t* d_fixed, uint64_t n_fixed, uint32_t m, uint64_t* d_words,
+                                cudaStream_t s, uint64_t* launches) {
+    const uint64_t n = n_fixed << m;
+    if (n == 0) return cudaSuccess;
+    k_expand_words<<<int((n + 255) / 256), 256, 0, s>>>(d_fixed, n_fixed, m, d_words);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_segment_sum(const double* d_in, uint64_t len, uint64_t n_seg, double* d_out, int accumulate,
+                               cudaStream_t s, uint64_t* launches) {
+    if (n_seg == 0) return cudaSuccess;
+    k_segment_sum<<<int(n_seg), 256, 0, s>>>(d_in, len, n_seg, d_out, accumulate);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_t n, uint8_t* d_out,
                                cudaStream_t s, uint64_t* launches) {
     const uint64_t total = t.n_rows * n;

@@ -423,6 +423,19 @@ class Context:
     def synchronize(self) -> None:
         _check(N.lib().pzx_synchronize(self.handle), self.handle)
 
+    def marginal_sum(self, table: DeviceTable, fixed, m: int, prob_real: bool = False,
+                     flags: int = 0) -> np.ndarray:
+        """Marginal summing (sim-driver): for every fixed word,
+        the sum over the 2^m settings of the low m parameters (the don't-care
+        outputs) of |amp|^2 -- or of Re(amp) for doubled diagrams."""
+        f = np.ascontiguousarray(np.asarray(fixed, dtype=np.uint64))
+        out = np.empty(f.size, np.float64)
+        if f.size:
+            flags = (flags & ~(PROB_ABS2 | PROB_REAL)) | (PROB_REAL if prob_real else PROB_ABS2)
+            _check(N.lib().pzx_marginal_sum(self.handle, table.handle, N.ptr(f, C.c_uint64), f.size, m, flags,
+                                            N.ptr(out, C.c_double)), self.handle)
+        return out
+
     # -- debug / parity hooks -------------------------------------------------
     def debug_phase_indices(self, table: DeviceTable, assignments) -> np.ndarray:
         a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))

@@ -260,6 +260,34 @@ def test_long_terms_segment_path(ctx):
     assert_close(ctx.evaluate_batch(t, z["words"], flags=P.KERNEL_GENERAL), z["amp"])
 
 
+@pytest.mark.parametrize("m", [0, 3, 11, 13])
+def test_marginal_sum(ctx, m):
+    """Marginal summing: sum of |amp|^2 (or Re amp) over the
+    2^m settings of the low m parameters, against per-assignment evaluation."""
+    P_ = 18
+    e = synth.generate(P_, 400, 1, 30, 1300 + m)
+    t = ctx.compile_bit_table(e)
+    rng = np.random.default_rng(m)
+    fixed = (rng.integers(0, 1 << (P_ - m), 5, dtype=np.uint64) << np.uint64(m)).astype(np.uint64)
+    got = ctx.marginal_sum(t, fixed, m)
+    for i, f in enumerate(fixed):
+        amp = ctx.evaluate_range(t, int(f), 1 << m)
+        want = float(np.sum(np.abs(amp) ** 2))
+        assert abs(got[i] - want) <= 1e-12 * max(want, 1e-300), (i, got[i], want)
+    got_re = ctx.marginal_sum(t, fixed[:2], m, prob_real=True)
+    for i, f in enumerate(fixed[:2]):
+        want = float(np.sum(ctx.evaluate_range(t, int(f), 1 << m).real))
+        assert abs(got_re[i] - want) <= 1e-12 * max(abs(want), np.sqrt(np.sum(np.abs(want) ** 2)), 1e-300) + 1e-12
+    # deterministic, and the oracle agrees on a small case
+    assert np.array_equal(ctx.marginal_sum(t, fixed, m), got)
+    if m <= 3:
+        words = (fixed[0] | np.arange(1 << m, dtype=np.uint64)).astype(np.uint64)
+        _, want = O.eval_batch(e, words, 8, impl="ref" if O.have_ref() else "port")
+        assert abs(got[0] - np.sum(np.abs(want) ** 2)) <= 1e-12 * np.sum(np.abs(want) ** 2)
+    with pytest.raises(P.Error):
+        ctx.marginal_sum(t, fixed | np.uint64(1), max(m, 1))
+
+
 def test_device_pointer_api_and_term_split(ctx):
     torch = pytest.importorskip("torch")
     e = synth.generate(10, 3000, 16, 40, 21)
