@@ -179,6 +179,13 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
  * PZX_PROB_REAL. Deterministic (fixed-order reductions). Kernel flags apply. */
 pzx_status pzx_marginal_sum(pzx_ctx* ctx, const pzx_table* t, const uint64_t* fixed, uint64_t n_fixed,
                             uint32_t m, uint32_t flags, double* out);
+/* Repeated weak simulation (PAPER App. F Alg. 2): tables[k]
+ * is the compiled doubled marginal P(a_1..a_{k+1}) (parameter j = bit j of
+ * the sample word); out[i] receives n_bits sampled bits per sample. prob =
+ * Re(value) by default (doubled diagrams), |value|^2 with PZX_PROB_ABS2.
+ * Draws use a counter-based RNG of (seed, bit, sample): reproducible. */
+pzx_status pzx_weak_sample(pzx_ctx* ctx, const pzx_table* const* tables, uint32_t n_bits, uint64_t n_samples,
+                           uint64_t seed, uint32_t flags, uint64_t* out);
 /* prob from amplitudes on device (after a cross-GPU sum of partials). */
 pzx_status pzx_amp_to_prob_device(pzx_ctx* ctx, const double* d_amp, uint64_t n,
                                   double* d_prob, uint32_t flags, void* stream);

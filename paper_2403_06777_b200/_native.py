@@ -18,7 +18,7 @@ EXPORTS = (
     "pzx_table_shape", "pzx_table_term_info", "pzx_evaluate", "pzx_evaluate_range",
     "pzx_evaluate_device", "pzx_amp_to_prob_device", "pzx_synchronize",
     "pzx_debug_phase_indices", "pzx_debug_term_codes", "pzx_table_compile_host", "pzx_class_table",
-    "pzx_slice_op_table", "pzx_marginal_sum",
+    "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -84,6 +84,7 @@ def lib() -> C.CDLL:
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     L.pzx_synchronize.argtypes = [vp]
     L.pzx_marginal_sum.argtypes = [vp, vp, u64p, C.c_uint64, C.c_uint32, C.c_uint32, dblp]
+    L.pzx_weak_sample.argtypes = [vp, C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32, u64p]
     L.pzx_debug_phase_indices.argtypes = [vp, vp, u64p, C.c_uint64, u8p]
     L.pzx_debug_term_codes.argtypes = [vp, vp, u64p, C.c_uint64, C.POINTER(TermCode)]
     L.pzx_table_compile_host.argtypes = [C.POINTER(ExprView), C.POINTER(vp)]

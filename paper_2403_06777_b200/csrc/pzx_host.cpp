@@ -943,6 +943,59 @@ pzx_status pzx_marginal_sum(pzx_ctx* ctx, const pzx_table* t, const uint64_t* fi
     return st;
 }
 
+// Repeated weak simulation (PAPER App. F Alg. 2): tables[k] is
+// the compiled doubled marginal P(a_1 .. a_{k+1}) (parameter j = bit j of the
+// sample word). Round k evaluates P(B_i || 0) for every sample on the device
+// and draws bit k from P(B_i || 0) / P(B_i); the samples never leave the GPU
+// until the end. n_bits tables -> n_bits compilations for any n_samples.
+pzx_status pzx_weak_sample(pzx_ctx* ctx, const pzx_table* const* tables, uint32_t n_bits, uint64_t n_samples,
+                           uint64_t seed, uint32_t flags, uint64_t* out) {
+    if (!ctx || (n_bits && !tables) || (n_samples && !out)) return PZX_E_INVALID;
+    if (n_bits > 64) return set_err(ctx, PZX_E_DOMAIN, "weak_sample: more than 64 output bits");
+    for (uint32_t k = 0; k < n_bits; ++k) {
+        if (!tables[k]) return set_err(ctx, PZX_E_INVALID, "weak_sample: null table");
+        if (tables[k]->dev.n_params < k + 1)
+            return set_err(ctx, PZX_E_MISSING_PARAM, "weak_sample: table k must take parameters a_1 .. a_{k+1}");
+    }
+    if (n_samples == 0) return PZX_OK;
+    if (flags & PZX_PROB_ABS2 && flags & PZX_PROB_REAL) return set_err(ctx, PZX_E_INVALID, "weak_sample: one prob mode");
+    const uint32_t pf = (flags & PZX_PROB_ABS2) ? PZX_PROB_ABS2 : PZX_PROB_REAL;  // doubled diagrams: Re
+    const uint32_t kflags = (flags & ~(PZX_PROB_ABS2 | PZX_PROB_REAL)) | pf;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    const uint64_t n = n_samples;
+    void* buf = nullptr;
+    const size_t bytes = n * 8 * 3 + 256;
+    if ((st = cuda_err(ctx, cudaMalloc(&buf, bytes), "alloc samples"))) return st;
+    uint64_t* d_words = static_cast<uint64_t*>(buf);
+    double* d_pprev = reinterpret_cast<double*>(d_words + n);
+    double* d_p0 = d_pprev + n;
+    unsigned int* d_err = reinterpret_cast<unsigned int*>(d_p0 + n);
+    auto done = [&](pzx_status s) { cudaFree(buf); return s; };
+    std::vector<double> ones(n, 1.0);  // P(empty prefix) = 1
+    if ((st = cuda_err(ctx, cudaMemsetAsync(d_words, 0, n * 8, ctx->stream), "init words"))) return done(st);
+    if ((st = cuda_err(ctx, cudaMemsetAsync(d_err, 0, 4, ctx->stream), "init err"))) return done(st);
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(d_pprev, ones.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream), "init P"))) return done(st);
+    for (uint32_t k = 0; k < n_bits; ++k) {
+        LaunchReq r;
+        r.stream = ctx->stream;
+        r.d_asg = d_words;
+        r.n = n;
+        r.term_begin = 0;
+        r.term_end = tables[k]->dev.n_terms;
+        r.prob_mode = prob_mode_of(pf);
+        r.d_prob = d_p0;
+        if ((st = run_eval(ctx, tables[k], r, kflags))) return done(st);
+        if ((st = cuda_err(ctx, launch_sample_step(d_words, d_pprev, d_p0, n, k, seed, d_err, ctx->stream, &ctx->launches), "sample step"))) return done(st);
+    }
+    unsigned int err = 0;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(out, d_words, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H samples"))) return done(st);
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H err"))) return done(st);
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "weak_sample"))) return done(st);
+    if (err) return done(set_err(ctx, PZX_E_DOMAIN, "weak_sample: zero-probability prefix encountered"));
+    return done(PZX_OK);
+}
+
 pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,

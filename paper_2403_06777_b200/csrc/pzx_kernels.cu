@@ -1688,6 +1688,46 @@ __global__ void k_segment_sum(const double* __restrict__ in, uint64_t len, uint6
     if (threadIdx.x == 0) out[s] = accumulate ? out[s] + red[0] : red[0];
 }
 
+// ---- repeated weak simulation (PAPER App. F Alg. 2) --------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// one chain-rule step for every sample i: p0 = P(B_i || 0), pp = P(B_i);
+// bit k of word i := 0 with probability p0 / pp, else 1 (counter-based RNG:
+// the draw depends only on (seed, k, i), so runs are reproducible)
+__global__ void k_sample_step(uint64_t* words, double* pprev, const double* __restrict__ p0, uint64_t n, uint32_t k,
+                              uint64_t seed, unsigned int* err) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double pp = pprev[i], q = p0[i];
+    if (!(pp > 0.0)) {
+        atomicOr(err, 1u);
+        return;
+    }
+    double ratio = q / pp;
+    ratio = ratio < 0.0 ? 0.0 : (ratio > 1.0 ? 1.0 : ratio);
+    const uint64_t h = splitmix64(seed ^ splitmix64((uint64_t(k) << 48) ^ i));
+    const double u = double(h >> 11) * 0x1.0p-53;
+    if (u < ratio) {
+        pprev[i] = q;
+    } else {
+        words[i] |= uint64_t(1) << k;
+        pprev[i] = pp - q;
+    }
+}
+
+cudaError_t launch_sample_step(uint64_t* d_words, double* d_pprev, const double* d_p0, uint64_t n, uint32_t k,
+                               uint64_t seed, unsigned int* d_err, cudaStream_t s, uint64_t* launches) {
+    if (n == 0) return cudaSuccess;
+    k_sample_step<<<int((n + 255) / 256), 256, 0, s>>>(d_words, d_pprev, d_p0, n, k, seed, d_err);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_expand_words(const uint64_t* d_fixed, uint64_t n_fixed, uint32_t m, uint64_t* d_words,
                                 cudaStream_t s, uint64_t* launches) {
     const uint64_t n = n_fixed << m;

@@ -423,6 +423,18 @@ class Context:
     def synchronize(self) -> None:
         _check(N.lib().pzx_synchronize(self.handle), self.handle)
 
+    def weak_sample(self, tables, n_samples: int, seed: int = 0, abs2: bool = False, flags: int = 0) -> np.ndarray:
+        """Repeated weak simulation (PAPER App. F Alg. 2): tables[k] is the
+        doubled marginal over parameters a_1..a_{k+1}; returns n_samples
+        words whose bit k is the sampled output bit k."""
+        hs = (C.c_void_p * max(1, len(tables)))(*[t.handle for t in tables])
+        out = np.zeros(n_samples, np.uint64)
+        flags = (flags & ~(PROB_ABS2 | PROB_REAL)) | (PROB_ABS2 if abs2 else PROB_REAL)
+        if n_samples:
+            _check(N.lib().pzx_weak_sample(self.handle, hs, len(tables), n_samples, seed & (2**64 - 1), flags,
+                                           N.ptr(out, C.c_uint64)), self.handle)
+        return out
+
     def marginal_sum(self, table: DeviceTable, fixed, m: int, prob_real: bool = False,
                      flags: int = 0) -> np.ndarray:
         """Marginal summing (sim-driver): for every fixed word,

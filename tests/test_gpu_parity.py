@@ -330,3 +330,60 @@ def test_full_size_c2_properties(ctx):
     pick = idx[:16]
     _, want = O.eval_batch(e, pick, os.cpu_count() or 8, impl="ref" if O.have_ref() else "port")
     assert_close(amp[pick.astype(np.int64)], want)
+
+
+def product_marginal_tables(s):
+    """Doubled-marginal tables of a product distribution over len(s) bits,
+    p_j(0) = (1 + s_j) / 2 with dyadic s_j: P_k(a) = prod_{j<k} p_j(a_j)
+    = sum over subsets S of [k] of prod_{j in S} s_j / 2^k * (-1)^{parity(S & a)};
+    (-1)^parity as the pair row V(4 parity, 4) / 2 = PhasePair((0, S), (4, {}))/2."""
+    exprs = []
+    for k in range(1, len(s) + 1):
+        terms = []
+        for S in range(1 << k):
+            sign, den = 1, k
+            for j in range(k):
+                if S >> j & 1:
+                    num, d = s[j]
+                    sign *= num
+                    den += d
+            if S == 0:
+                terms.append((P.RingQuad.make(1, 0, 0, 0, k), []))
+            else:
+                pp = P.Subterm.phase_pair(P.ParamPhase(0, S), P.ParamPhase(4, 0))
+                terms.append((P.RingQuad.make(sign, 0, 0, 0, den + 1), [pp]))
+        exprs.append(P.ScalarExpression.from_terms(k, terms))
+    return exprs
+
+
+def test_weak_sample_product_distribution(ctx):
+    """Repeated weak simulation (PAPER App. F Alg. 2) on tables whose marginals
+    are known in closed form: bit frequencies and a joint frequency within
+    6 sigma of the product distribution, reproducible per seed."""
+    s = [(1, 1), (-1, 1), (1, 1), (1, 2), (-1, 2), (0, 0)]   # s_j = num / 2^d: 1/2, -1/2, 1/2, 1/4, -1/4, 0
+    exprs = product_marginal_tables(s)
+    # the tables are the marginals (oracle check of the construction)
+    for k, e in enumerate(exprs[:3], 1):
+        words = np.arange(1 << k, dtype=np.uint64)
+        _, v = O.eval_batch(e, words, 4)
+        p0 = [(1 + (n / 2 ** d)) / 2 for n, d in s]
+        want = [np.prod([p0[j] if not (w >> j) & 1 else 1 - p0[j] for j in range(k)]) for w in range(1 << k)]
+        assert np.allclose(v.real, want, rtol=0, atol=1e-15) and np.allclose(v.imag, 0, atol=1e-15)
+    tables = [ctx.compile_bit_table(e) for e in exprs]
+    N = 1 << 16
+    w = ctx.weak_sample(tables, N, seed=7)
+    assert w.dtype == np.uint64 and np.all(w < (1 << len(s)))
+    p0 = np.array([(1 + (n / 2 ** d)) / 2 for n, d in s])
+    f0 = np.array([np.mean(((w >> np.uint64(j)) & np.uint64(1)) == 0) for j in range(len(s))])
+    sig = np.sqrt(p0 * (1 - p0) / N)
+    assert np.all(np.abs(f0 - p0) <= 6 * sig + 1e-12), (f0, p0)
+    both = np.mean((w & np.uint64(3)) == 0)
+    pj = p0[0] * p0[1]
+    assert abs(both - pj) <= 6 * np.sqrt(pj * (1 - pj) / N)
+    assert np.array_equal(ctx.weak_sample(tables, N, seed=7), w)
+    assert not np.array_equal(ctx.weak_sample(tables, N, seed=8), w)
+    # deterministic distribution: s = +1 -> always 0, s = -1 -> always 1
+    det = [ctx.compile_bit_table(e) for e in product_marginal_tables([(1, 0), (-1, 0), (1, 0)])]
+    assert np.all(ctx.weak_sample(det, 1000, seed=1) == 0b010)
+    with pytest.raises(P.Error):   # table k must take k + 1 parameters
+        ctx.weak_sample([tables[1], tables[0]], 10)
