@@ -173,6 +173,21 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
                                uint32_t flags, void* stream);
+/* PZX1 binary table codec (SPEC "External Interfaces"): the
+ * normalised table as header {"PZX1", u32 n_params, u64 m, u64 n_max, u64 R =
+ * m*n_max}, i64 constants[m][5], then field-major padded rows u8 flags[R] (1 =
+ * dummy), u8 k_alpha[R], u64 psi[R], u8 k_beta[R], u64 phi[R], little-endian.
+ * Encoders with buf == NULL report the size in *len; decode errors are
+ * PZX_E_PARSE (bad magic, truncation, inconsistent shape) and never leave a
+ * partial value. decode(encode(x)) == x and encode(decode(b)) == b byte for byte. */
+pzx_status pzx_pzx1_encode(const pzx_table_view* view, uint8_t* buf, uint64_t cap, uint64_t* len);
+pzx_status pzx_pzx1_encode_expr(const pzx_expr_view* expr, uint8_t* buf, uint64_t cap, uint64_t* len);
+pzx_status pzx_pzx1_info(const uint8_t* buf, uint64_t len, uint32_t* n_params, uint64_t* n_terms,
+                         uint64_t* n_rows);
+pzx_status pzx_pzx1_decode(const uint8_t* buf, uint64_t len, uint64_t* term_row_offset, int64_t* term_coef,
+                           uint64_t* psi_mask, uint64_t* phi_mask, uint8_t* k_alpha, uint8_t* k_beta);
+pzx_status pzx_table_upload_pzx1(pzx_ctx* ctx, const uint8_t* buf, uint64_t len, pzx_table** out);
+
 /* Marginal summing (sim-driver): out[i] = sum over b < 2^m of
  * prob(fixed[i] | b), the don't-care outputs being the low m parameters
  * (fixed[i] must have them clear); prob = |amp|^2, or Re(amp) with

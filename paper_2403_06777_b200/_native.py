@@ -18,7 +18,8 @@ EXPORTS = (
     "pzx_table_shape", "pzx_table_term_info", "pzx_evaluate", "pzx_evaluate_range",
     "pzx_evaluate_device", "pzx_amp_to_prob_device", "pzx_synchronize",
     "pzx_debug_phase_indices", "pzx_debug_term_codes", "pzx_table_compile_host", "pzx_class_table",
-    "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample",
+    "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample", "pzx_pzx1_encode", "pzx_pzx1_encode_expr",
+    "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -83,6 +84,11 @@ def lib() -> C.CDLL:
                                       vp, vp, C.c_uint32, vp]
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     L.pzx_synchronize.argtypes = [vp]
+    L.pzx_pzx1_encode.argtypes = [C.POINTER(TableView), u8p, C.c_uint64, u64p]
+    L.pzx_pzx1_encode_expr.argtypes = [C.POINTER(ExprView), u8p, C.c_uint64, u64p]
+    L.pzx_pzx1_info.argtypes = [u8p, C.c_uint64, C.POINTER(C.c_uint32), u64p, u64p]
+    L.pzx_pzx1_decode.argtypes = [u8p, C.c_uint64, u64p, i64p, u64p, u64p, u8p, u8p]
+    L.pzx_table_upload_pzx1.argtypes = [vp, u8p, C.c_uint64, C.POINTER(vp)]
     L.pzx_marginal_sum.argtypes = [vp, vp, u64p, C.c_uint64, C.c_uint32, C.c_uint32, dblp]
     L.pzx_weak_sample.argtypes = [vp, C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32, u64p]
     L.pzx_debug_phase_indices.argtypes = [vp, vp, u64p, C.c_uint64, u8p]

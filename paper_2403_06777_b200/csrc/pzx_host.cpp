@@ -775,6 +775,224 @@ pzx_status pzx_table_compile_host(const pzx_expr_view* expr, pzx_table** out) {
     return PZX_OK;
 }
 
+// ---------------------------------------------------------------- PZX1 ----
+// Binary table codec (SPEC "External Interfaces": header {magic "PZX1", n,
+// m, n_max, R}, constants as 5 x i64, field-major padded table). Layout,
+// little-endian:
+//   char magic[4] = "PZX1"; u32 n_params; u64 m; u64 n_max; u64 R = m * n_max
+//   i64 constants[m][5]                      RingQuad a, b, c, d, exp (canonical)
+//   u8 flags[R] (1 = dummy padding row), u8 k_alpha[R], u64 psi[R], u8 k_beta[R], u64 phi[R]
+// Row r = t * n_max + i is row i of term t (real rows first, dummies all-zero).
+extern "C++" {
+namespace {
+
+constexpr uint64_t kPzx1Header = 4 + 4 + 8 + 8 + 8;
+
+struct Rows {  // normalised table (CSR, no padding)
+    uint32_t n_params = 0;
+    std::vector<uint64_t> off{0};
+    std::vector<int64_t> coef;
+    std::vector<uint64_t> psi, phi;
+    std::vector<uint8_t> ka, kb;
+};
+
+// normalize_subterm (subterm.cpp:51-96) over a raw expression, constants folded
+// into C_t exactly as the compiler does (constant-first, diagram.cpp:158-161)
+int normalize_rows(const pzx_expr_view* v, Rows& out, std::string& err) {
+    if (v->n_params > 64) { err = "parameter capacity (64) exceeded"; return PZX_E_DOMAIN; }
+    out.n_params = v->n_params;
+    const uint64_t allowed = param_mask(v->n_params);
+    for (uint64_t t = 0; t < v->n_terms; ++t) {
+        Quad c;
+        if (!canon_input(v->term_scalar + 5 * t, c)) { err = "term scalar out of range"; return PZX_E_OVERFLOW; }
+        for (uint64_t j = v->term_offset[t]; j < v->term_offset[t + 1]; ++j) {
+            const uint8_t kind = v->kind[j];
+            const int psik = v->psi_k[j], phik = v->phi_k ? v->phi_k[j] : 0;
+            const uint64_t psim = v->psi_mask[j];
+            uint64_t phim = v->phi_mask ? v->phi_mask[j] : 0;
+            if (kind > PZX_PI_PAIR || psik > 7 || phik > 7) { err = "subterm kind or phase out of range"; return PZX_E_DOMAIN; }
+            if (kind == PZX_NODE || kind == PZX_HALF_PI) phim = 0;
+            if ((psim | phim) & ~allowed) { err = "subterm mask uses a parameter >= n_params"; return PZX_E_MISSING_PARAM; }
+            Quad k, nc;
+            bool has = false;
+            PairRow pr{};
+            if (normalize(kind, psik, psim, phik, phim, k, has, pr)) { err = "normalize_subterm: kind invariant violated"; return PZX_E_DOMAIN; }
+            if (!quad_mul(c, k, nc)) { err = "term constant overflow"; return PZX_E_OVERFLOW; }
+            c = nc;
+            if (has) {
+                out.ka.push_back(pr.ka);
+                out.kb.push_back(pr.kb);
+                out.psi.push_back(pr.psi);
+                out.phi.push_back(pr.phi);
+            }
+        }
+        const int64_t q[5] = {c.a, c.b, c.c, c.d, c.e};
+        out.coef.insert(out.coef.end(), q, q + 5);
+        out.off.push_back(out.ka.size());
+    }
+    return PZX_OK;
+}
+
+template <typename T>
+void put(uint8_t*& p, T v) {
+    std::memcpy(p, &v, sizeof(T));  // little-endian host (x86-64 / aarch64)
+    p += sizeof(T);
+}
+template <typename T>
+T get(const uint8_t*& p) {
+    T v;
+    std::memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    return v;
+}
+
+pzx_status encode_view(const pzx_table_view* v, uint8_t* buf, uint64_t cap, uint64_t* len) {
+    if (!v || !len || (v->n_terms && (!v->term_row_offset || !v->term_coef))) return PZX_E_INVALID;
+    const uint64_t m = v->n_terms;
+    uint64_t n_max = 0;
+    for (uint64_t t = 0; t < m; ++t) n_max = std::max(n_max, v->term_row_offset[t + 1] - v->term_row_offset[t]);
+    const uint64_t R = m * n_max;
+    const uint64_t need = kPzx1Header + 40 * m + 19 * R;
+    *len = need;
+    if (!buf) return PZX_OK;
+    if (cap < need) return PZX_E_CAPACITY;
+    uint8_t* p = buf;
+    std::memcpy(p, "PZX1", 4);
+    p += 4;
+    put<uint32_t>(p, v->n_params);
+    put<uint64_t>(p, m);
+    put<uint64_t>(p, n_max);
+    put<uint64_t>(p, R);
+    for (uint64_t i = 0; i < 5 * m; ++i) put<int64_t>(p, v->term_coef[i]);
+    uint8_t* f_flag = p;
+    uint8_t* f_ka = f_flag + R;
+    uint8_t* f_psi = f_ka + R;
+    uint8_t* f_kb = f_psi + 8 * R;
+    uint8_t* f_phi = f_kb + R;
+    std::memset(f_flag, 0, 19 * R);
+    for (uint64_t t = 0; t < m; ++t) {
+        const uint64_t r0 = v->term_row_offset[t], n = v->term_row_offset[t + 1] - r0;
+        for (uint64_t i = 0; i < n_max; ++i) {
+            const uint64_t r = t * n_max + i;
+            if (i >= n) { f_flag[r] = 1; continue; }
+            f_ka[r] = v->k_alpha[r0 + i];
+            f_kb[r] = v->k_beta[r0 + i];
+            std::memcpy(f_psi + 8 * r, &v->psi_mask[r0 + i], 8);
+            std::memcpy(f_phi + 8 * r, &v->phi_mask[r0 + i], 8);
+        }
+    }
+    return PZX_OK;
+}
+
+pzx_status decode_rows(const uint8_t* buf, uint64_t len, Rows& out, std::string& err) {
+    if (!buf || len < kPzx1Header) { err = "PZX1: truncated header"; return PZX_E_PARSE; }
+    const uint8_t* p = buf;
+    if (std::memcmp(p, "PZX1", 4) != 0) { err = "PZX1: bad magic / version"; return PZX_E_PARSE; }
+    p += 4;
+    out.n_params = get<uint32_t>(p);
+    const uint64_t m = get<uint64_t>(p), n_max = get<uint64_t>(p), R = get<uint64_t>(p);
+    if (out.n_params > 64) { err = "PZX1: n_params > 64"; return PZX_E_PARSE; }
+    if (n_max > (uint64_t(1) << 32) || m > (uint64_t(1) << 40) || R != m * n_max) { err = "PZX1: inconsistent shape"; return PZX_E_PARSE; }
+    const uint64_t need = kPzx1Header + 40 * m + 19 * R;
+    if (len != need) { err = len < need ? "PZX1: truncated body" : "PZX1: trailing bytes"; return PZX_E_PARSE; }
+    out.coef.resize(5 * m);
+    for (uint64_t i = 0; i < 5 * m; ++i) out.coef[i] = get<int64_t>(p);
+    const uint8_t* f_flag = p;
+    const uint8_t* f_ka = f_flag + R;
+    const uint8_t* f_psi = f_ka + R;
+    const uint8_t* f_kb = f_psi + 8 * R;
+    const uint8_t* f_phi = f_kb + R;
+    out.off.assign(1, 0);
+    for (uint64_t t = 0; t < m; ++t) {
+        bool dummy = false;
+        for (uint64_t i = 0; i < n_max; ++i) {
+            const uint64_t r = t * n_max + i;
+            if (f_flag[r] > 1) { err = "PZX1: bad row flag"; return PZX_E_PARSE; }
+            if (f_flag[r]) { dummy = true; continue; }
+            if (dummy) { err = "PZX1: real row after padding"; return PZX_E_PARSE; }
+            uint64_t a, b;
+            std::memcpy(&a, f_psi + 8 * r, 8);
+            std::memcpy(&b, f_phi + 8 * r, 8);
+            out.ka.push_back(f_ka[r]);
+            out.kb.push_back(f_kb[r]);
+            out.psi.push_back(a);
+            out.phi.push_back(b);
+        }
+        out.off.push_back(out.ka.size());
+    }
+    return PZX_OK;
+}
+
+pzx_table_view view_of(const Rows& r) {
+    pzx_table_view v{};
+    v.n_params = r.n_params;
+    v.n_terms = r.off.size() - 1;
+    v.term_row_offset = r.off.data();
+    v.term_coef = r.coef.data();
+    v.psi_mask = r.psi.data();
+    v.phi_mask = r.phi.data();
+    v.k_alpha = r.ka.data();
+    v.k_beta = r.kb.data();
+    return v;
+}
+
+}  // namespace
+}  // extern "C++"
+
+pzx_status pzx_pzx1_encode(const pzx_table_view* view, uint8_t* buf, uint64_t cap, uint64_t* len) {
+    return encode_view(view, buf, cap, len);
+}
+
+pzx_status pzx_pzx1_encode_expr(const pzx_expr_view* expr, uint8_t* buf, uint64_t cap, uint64_t* len) {
+    if (!expr || !len || (expr->n_terms && (!expr->term_offset || !expr->term_scalar))) return PZX_E_INVALID;
+    Rows r;
+    std::string err;
+    const int st = normalize_rows(expr, r, err);
+    if (st) return pzx_status(st);
+    const pzx_table_view v = view_of(r);
+    return encode_view(&v, buf, cap, len);
+}
+
+pzx_status pzx_pzx1_info(const uint8_t* buf, uint64_t len, uint32_t* n_params, uint64_t* n_terms, uint64_t* n_rows) {
+    Rows r;
+    std::string err;
+    const pzx_status st = decode_rows(buf, len, r, err);
+    if (st) return st;
+    if (n_params) *n_params = r.n_params;
+    if (n_terms) *n_terms = r.off.size() - 1;
+    if (n_rows) *n_rows = r.ka.size();
+    return PZX_OK;
+}
+
+pzx_status pzx_pzx1_decode(const uint8_t* buf, uint64_t len, uint64_t* term_row_offset, int64_t* term_coef,
+                           uint64_t* psi_mask, uint64_t* phi_mask, uint8_t* k_alpha, uint8_t* k_beta) {
+    Rows r;
+    std::string err;
+    const pzx_status st = decode_rows(buf, len, r, err);
+    if (st) return st;
+    if (!term_row_offset || !term_coef || (!r.ka.empty() && (!psi_mask || !phi_mask || !k_alpha || !k_beta)))
+        return PZX_E_INVALID;
+    std::memcpy(term_row_offset, r.off.data(), r.off.size() * 8);
+    std::memcpy(term_coef, r.coef.data(), r.coef.size() * 8);
+    if (!r.ka.empty()) {
+        std::memcpy(psi_mask, r.psi.data(), r.psi.size() * 8);
+        std::memcpy(phi_mask, r.phi.data(), r.phi.size() * 8);
+        std::memcpy(k_alpha, r.ka.data(), r.ka.size());
+        std::memcpy(k_beta, r.kb.data(), r.kb.size());
+    }
+    return PZX_OK;
+}
+
+pzx_status pzx_table_upload_pzx1(pzx_ctx* ctx, const uint8_t* buf, uint64_t len, pzx_table** out) {
+    if (!ctx || !out) return PZX_E_INVALID;
+    Rows r;
+    std::string err;
+    const pzx_status st = decode_rows(buf, len, r, err);
+    if (st) return set_err(ctx, st, err);
+    const pzx_table_view v = view_of(r);
+    return pzx_table_upload(ctx, &v, out);
+}
+
 pzx_status pzx_slice_op_table(int32_t out[129 * 10]) {
     if (!out) return PZX_E_INVALID;
     for (int op = 0; op < kSliceOps; ++op) {

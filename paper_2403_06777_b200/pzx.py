@@ -382,6 +382,14 @@ class Context:
         _check(N.lib().pzx_table_upload(self.handle, C.byref(v), C.byref(h)), self.handle)
         return DeviceTable(self, h)
 
+    def upload_pzx1(self, data: bytes) -> DeviceTable:
+        """Upload a PZX1-encoded table (see encode_pzx1)."""
+        buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+        h = C.c_void_p()
+        _check(N.lib().pzx_table_upload_pzx1(self.handle, N.ptr(buf, C.c_uint8), len(data), C.byref(h)),
+               self.handle)
+        return DeviceTable(self, h)
+
     # -- evaluation -----------------------------------------------------------
     def evaluate_batch(self, table: DeviceTable, assignments, *, prob: bool = False,
                        prob_real: bool = False, flags: int = 0):
@@ -501,6 +509,119 @@ def slice_op_table() -> np.ndarray:
     return out.reshape(129, 10)
 
 
+# ---------------------------------------------------------------- PZX1 ----
+@dataclass
+class PhaseTable:
+    """A normalised table (SPEC ScalarExpression after Eq. 4): term t is
+    C_t * prod of pair rows term_row_offset[t] .. term_row_offset[t+1]-1."""
+
+    n_params: int
+    term_row_offset: np.ndarray
+    term_coef: np.ndarray      # [m, 5] RingQuad a, b, c, d, exp
+    psi_mask: np.ndarray
+    phi_mask: np.ndarray
+    k_alpha: np.ndarray
+    k_beta: np.ndarray
+
+    @property
+    def n_terms(self) -> int:
+        return len(self.term_row_offset) - 1
+
+    def view(self):
+        arrs = [np.ascontiguousarray(self.term_row_offset, np.uint64),
+                np.ascontiguousarray(self.term_coef, np.int64).reshape(-1),
+                np.ascontiguousarray(self.psi_mask, np.uint64), np.ascontiguousarray(self.phi_mask, np.uint64),
+                np.ascontiguousarray(self.k_alpha, np.uint8), np.ascontiguousarray(self.k_beta, np.uint8)]
+        arrs = [x if x.size else np.zeros(1, x.dtype) for x in arrs]
+        v = N.TableView(self.n_params, self.n_terms, N.ptr(arrs[0], C.c_uint64), N.ptr(arrs[1], C.c_int64),
+                        N.ptr(arrs[2], C.c_uint64), N.ptr(arrs[3], C.c_uint64), N.ptr(arrs[4], C.c_uint8),
+                        N.ptr(arrs[5], C.c_uint8))
+        return v, arrs
+
+
+def _encode(fn, view) -> bytes:
+    n = C.c_uint64()
+    _check(fn(C.byref(view), None, 0, C.byref(n)))
+    buf = np.empty(max(1, n.value), np.uint8)
+    _check(fn(C.byref(view), N.ptr(buf, C.c_uint8), n.value, C.byref(n)))
+    return buf[:n.value].tobytes()
+
+
+def encode_pzx1(obj) -> bytes:
+    """PZX1 binary codec (SPEC "External Interfaces"): a ScalarExpression is
+    normalised first (normalize_subterm, constants folded); a PhaseTable is
+    written as is."""
+    L = N.lib()
+    if isinstance(obj, ScalarExpression):
+        v, keep = obj.view()
+        out = _encode(L.pzx_pzx1_encode_expr, v)
+        del keep
+        return out
+    v, keep = obj.view()
+    out = _encode(L.pzx_pzx1_encode, v)
+    del keep
+    return out
+
+
+def decode_pzx1(data: bytes) -> PhaseTable:
+    L = N.lib()
+    buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+    p, m, r = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    _check(L.pzx_pzx1_info(N.ptr(buf, C.c_uint8), len(data), C.byref(p), C.byref(m), C.byref(r)))
+    off = np.empty(m.value + 1, np.uint64)
+    coef = np.empty(max(1, 5 * m.value), np.int64)
+    R = max(1, r.value)
+    psi, phi = np.empty(R, np.uint64), np.empty(R, np.uint64)
+    ka, kb = np.empty(R, np.uint8), np.empty(R, np.uint8)
+    _check(L.pzx_pzx1_decode(N.ptr(buf, C.c_uint8), len(data), N.ptr(off, C.c_uint64), N.ptr(coef, C.c_int64),
+                             N.ptr(psi, C.c_uint64), N.ptr(phi, C.c_uint64), N.ptr(ka, C.c_uint8),
+                             N.ptr(kb, C.c_uint8)))
+    n = r.value
+    return PhaseTable(p.value, off, coef[:5 * m.value].reshape(-1, 5), psi[:n], phi[:n], ka[:n], kb[:n])
+
+
+def pzx1_to_json(data: bytes) -> str:
+    """JSON mirror of a PZX1 blob (same fields, padded rows included)."""
+    import json
+    import struct
+    if len(data) < 32 or data[:4] != b"PZX1":
+        raise ParseError("PZX1: bad magic / truncated header")
+    n, m, n_max, R = struct.unpack_from("<IQQQ", data, 4)
+    t = decode_pzx1(data)
+    flags, ka, kb, psi, phi = [], [], [], [], []
+    for i in range(m):
+        a, b = int(t.term_row_offset[i]), int(t.term_row_offset[i + 1])
+        for j in range(n_max):
+            real = a + j < b
+            flags.append(0 if real else 1)
+            ka.append(int(t.k_alpha[a + j]) if real else 0)
+            kb.append(int(t.k_beta[a + j]) if real else 0)
+            psi.append(int(t.psi_mask[a + j]) if real else 0)
+            phi.append(int(t.phi_mask[a + j]) if real else 0)
+    return json.dumps({"magic": "PZX1", "n_params": n, "m": m, "n_max": n_max, "R": R,
+                       "constants": t.term_coef.tolist(), "flags": flags, "k_alpha": ka, "psi": psi,
+                       "k_beta": kb, "phi": phi}, separators=(",", ":"))
+
+
+def pzx1_from_json(text: str) -> bytes:
+    import json
+    import struct
+    d = json.loads(text)
+    if d.get("magic") != "PZX1":
+        raise ParseError("PZX1 JSON: bad magic")
+    m, n_max, R = d["m"], d["n_max"], d["R"]
+    if R != m * n_max or any(len(d[k]) != R for k in ("flags", "k_alpha", "psi", "k_beta", "phi")) \
+            or len(d["constants"]) != m:
+        raise ParseError("PZX1 JSON: inconsistent shape")
+    out = bytearray(b"PZX1" + struct.pack("<IQQQ", d["n_params"], m, n_max, R))
+    out += np.asarray(d["constants"], np.int64).reshape(-1).astype("<i8").tobytes()
+    out += np.asarray(d["flags"], np.uint8).tobytes() + np.asarray(d["k_alpha"], np.uint8).tobytes()
+    out += np.asarray(d["psi"], np.uint64).astype("<u8").tobytes()
+    out += np.asarray(d["k_beta"], np.uint8).tobytes() + np.asarray(d["phi"], np.uint64).astype("<u8").tobytes()
+    decode_pzx1(bytes(out))  # validate
+    return bytes(out)
+
+
 def compile_bit_table(expr: ScalarExpression, ctx: Context) -> DeviceTable:
     """SPEC compile_bit_table: normalise, classify, upload."""
     return ctx.compile_bit_table(expr)
@@ -520,6 +641,7 @@ __all__ = [
     "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
+    "PhaseTable", "encode_pzx1", "decode_pzx1", "pzx1_to_json", "pzx1_from_json",
     "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
 ]
 _ = builtins
