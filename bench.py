@@ -21,9 +21,12 @@ ours (default):
   * cpu_baseline -- the reference's own CPU evaluator (oracle/_ref, built from
               /root/reference) on all host threads, bounded sample of the same
               workload (rank 0, N = 1 only).
-  Multi-GPU (torchrun): one process per GPU, each rank evaluates its own 2^20
-  assignment batch against a replicated table ("weak": per-GPU work fixed), no
-  collective on the data path.
+  Multi-GPU (torchrun): one process per GPU. Default --split assign: the
+  config's batch (C2: all 2^20 amplitudes; C3: the 2^24 samples) is cut into
+  contiguous per-rank slices against a replicated table ("strong", no
+  collective on the data path); --split weak gives every rank a full batch;
+  --split terms splits the table and sums partial amplitudes with one NCCL
+  all-reduce.
 
 reference: rank 0 times the reference's CPU implementation of the path
   (oracle/_ref) on the same config, bounded sample per step; other ranks exit.
@@ -236,12 +239,22 @@ def run_ours(args):
     table = ctx.compile_bit_table(expr)
     log(f"[bench] rank {rank}: table compiled+uploaded in {time.time() - t0:.1f}s "
         f"({table.n_rows} rows, max {table.max_term_rows}/term)")
-    N = args.assign or cfg.n_assign         # per-rank batch (weak scaling) / whole batch (term split)
-    first = 0 if split_terms else rank * N
+    # multi-GPU modes: "assign" (default) shards the config's batch into
+    # contiguous slices (strong scaling, no collective); "weak" gives every rank
+    # its own full batch; "terms" splits the table (every rank the whole batch)
+    weak = args.split == "weak"
+    N_total = args.assign or cfg.n_assign
+    if args.split == "assign":
+        lo, hi = rank * N_total // world, (rank + 1) * N_total // world
+    else:
+        lo, hi = 0, N_total
+    N = hi - lo                             # this rank's batch
+    first = rank * N_total if weak else lo
+    evals_per_step = world * N_total if weak else N_total
     words_host = None
     if not cfg.enumerated:
         from paper_2403_06777_b200 import synth
-        words_host = synth.assignments(cfg, N, seed_offset=0 if split_terms else rank)
+        words_host = synth.assignments(cfg, N_total, seed_offset=rank if weak else 0)[lo:hi]
     R, m = table.n_rows, table.n_terms
 
     stream = torch.cuda.current_stream(dev)
@@ -294,7 +307,7 @@ def run_ours(args):
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    value = (1 if split_terms else world) * N * args.steps / (tot_ms / 1e3)
+    value = evals_per_step * args.steps / (tot_ms / 1e3)
 
     # ---- end to end through the public API (host buffers) -------------------
     e2e_value, same = None, None
@@ -326,7 +339,7 @@ def run_ours(args):
             t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
-        e2e_value = N * len(e2e_times) / e2e_tot
+        e2e_value = evals_per_step * len(e2e_times) / e2e_tot
         same = True
     elif not args.no_e2e:
         if words_host is None:
@@ -363,7 +376,7 @@ def run_ours(args):
             t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
-        e2e_value = world * N * len(e2e_times) / e2e_tot
+        e2e_value = evals_per_step * len(e2e_times) / e2e_tot
         # sanity: e2e results equal the device-resident ones (same kernel, same words)
         same = np.allclose(pinned_amp.numpy(), d_amp.cpu().numpy(), rtol=0, atol=0)
 
@@ -412,14 +425,16 @@ def run_ours(args):
         line = {
             "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
             "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong" if split_terms else "weak",
+            "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "int32 exact exponent codes + fp64 term sum", "data": "synthetic",
             "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": m, "n_rows": R,
-                       "assignments_per_gpu": N, "batch": "enumerated" if cfg.enumerated else "random",
+                       "assignments_per_gpu": N, "assignments_total": evals_per_step, "batch": "enumerated" if cfg.enumerated else "random",
                        "l2": "flushed between timed steps (256 MiB memset outside the events)",
                        "parallelism": (f"term split x{world} + NCCL all-reduce" if split_terms
-                                       else f"assignment shards x{world}"), "kernel": args.kernel},
+                                       else f"full batch per rank x{world}" if weak
+                                       else f"assignment shards x{world} (contiguous slices, no collective)"),
+                       "kernel": args.kernel},
             "e2e": None if e2e_value is None else {
                 "value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
                 "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
@@ -454,8 +469,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
-    ap.add_argument("--split", default="assign", choices=["assign", "terms"],
-                    help="multi-GPU: assignment shards (weak) or term split + all-reduce (strong)")
+    ap.add_argument("--split", default="assign", choices=["assign", "weak", "terms"],
+                    help="multi-GPU: shard the batch (strong), a full batch per rank (weak), or split the "
+                         "terms + NCCL all-reduce (strong)")
     ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)
