@@ -233,11 +233,10 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
     if (h.want_srows) {
         h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
-        // P <= 32: the high-mask words carry -(bit 5) of psi / phi instead: the
-        // two-slice kernel's second slice (assignments + 32) has X' = X ^ that
-        auto m5 = [](uint64_t m) { return uint32_t(0) - uint32_t((m >> 5) & 1u); };
+        // P <= 32: the high-mask words carry ~Walsh32 instead, so the kernel
+        // forms X = parity ? ~W : W with one predicate + one SEL
         if (h.n_params <= 32)
-            h.srows.push_back(make_uint4(walsh32(phi), m5(psi), m5(phi), op));
+            h.srows.push_back(make_uint4(walsh32(phi), ~walsh32(psi), ~walsh32(phi), op));
         else
             h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), op));
     }

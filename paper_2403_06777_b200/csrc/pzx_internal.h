@@ -64,7 +64,7 @@ struct DevTable {
     int p64 = 0;
     // bit-sliced kernel (only when every term has <= kSegRows rows):
     // rows as 2 x uint4 {psi, phi, op | kind flags | kEndFlag, Walsh32(psi)}, {Walsh32(phi), psi_hi, phi_hi, op}
-    // (n_params <= 32: {Walsh32(phi), -(psi bit 5), -(phi bit 5), op})
+    // (n_params <= 32: {Walsh32(phi), ~Walsh32(psi), ~Walsh32(phi), op})
     // (op = class * 2 + single, pzx_classes.h), constants C''_t * w^(sum of row jbase)
     const uint4* srows = nullptr;
     const double2* sterm_c = nullptr;

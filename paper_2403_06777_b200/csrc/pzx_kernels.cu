@@ -879,6 +879,15 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
     slice_epilogue_apply<NT, TM, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
 }
 
+// odd(p) ? a : b as one predicate-setting LOP3 + SEL
+__device__ __forceinline__ uint32_t sel_parity(uint32_t p, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("{\n .reg .pred q;\n .reg .b32 t;\n and.b32 t, %1, 1;\n setp.ne.b32 q, t, 0;\n selp.b32 %0, %2, %3, q;\n}"
+        : "=r"(r)
+        : "r"(p), "r"(a), "r"(b));
+    return r;
+}
+
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
 template <bool P64, bool RAND, int NT, bool TM = false>
@@ -1049,8 +1058,15 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         px = __popc(na.x & blo);
                         py = __popc(na.y & blo);
                     }
-                    X = na.w ^ (0u - (px & 1u));  // Walsh32(psi) ^ -parity(psi & base)
-                    Y = nb.x ^ (0u - (py & 1u));  // (== 0 for one-parity rows: phi == 0)
+                    // Walsh32(psi) ^ -parity(psi & base), Y likewise (== 0 for one-parity
+                    // rows: phi == 0); for P <= 32 the row carries ~Walsh32 (one SEL)
+                    if constexpr (P64) {
+                        X = na.w ^ (0u - (px & 1u));
+                        Y = nb.x ^ (0u - (py & 1u));
+                    } else {
+                        X = sel_parity(px, nb.y, na.w);
+                        Y = sel_parity(py, nb.z, nb.x);
+                    }
                 }
                 na = lds128(ad + 32);
                 nb = lds128(ad + 48);
@@ -1149,18 +1165,15 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_eval_slice2(const DevTable
             for (uint32_t ad = a0; ad < aend; ad += 32) {
                 const uint32_t code = na.z;
                 const uint32_t op = nb.w;
-                uint32_t px, py, m5x, m5y;
+                uint32_t px, py;
                 if constexpr (P64) {
                     px = __popc((na.x & blo) ^ (nb.y & bhi));
                     py = __popc((na.y & blo) ^ (nb.z & bhi));
-                    m5x = 0u - ((na.x >> 5) & 1u);
-                    m5y = 0u - ((na.y >> 5) & 1u);
                 } else {
                     px = __popc(na.x & blo);
                     py = __popc(na.y & blo);
-                    m5x = nb.y;  // host-precomputed -(psi bit 5), -(phi bit 5)
-                    m5y = nb.z;
                 }
+                const uint32_t m5x = 0u - ((na.x >> 5) & 1u), m5y = 0u - ((na.y >> 5) & 1u);
                 const uint32_t Xa = na.w ^ (0u - (px & 1u)), Ya = nb.x ^ (0u - (py & 1u));
                 const uint32_t Xb = Xa ^ m5x, Yb = Ya ^ m5y;
                 na = lds128(ad + 32);
