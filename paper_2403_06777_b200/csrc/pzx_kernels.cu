@@ -1032,53 +1032,66 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
             const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
+            if constexpr (!RAND) {
+                // fused row loop (generated PTX, pzx_slice_dispatch.inc): plain rows
+                // never leave it; it returns after a flagged row or at the tile end.
+                // Rows are prefetched one ahead into r[] (the read past the last
+                // row stays inside the CTA's shared window and is never used).
+                uint4 ra = lds128(a0), rb = lds128(a0 + 16);
+                uint32_t ad = a0;
+                while (ad < aend) {
+                    uint32_t vl, vpi, vpip, code;
+                    if constexpr (P64) {
+                        asm volatile(PZX_SLICE_ROWLOOP_P64
+                                     : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi),
+                                       "=r"(vpip), "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w),
+                                       "+r"(rb.x), "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                     : "r"(aend), "r"(blo), "r"(bhi)
+                                     : "memory");
+                    } else {
+                        asm volatile(PZX_SLICE_ROWLOOP_P32
+                                     : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi),
+                                       "=r"(vpip), "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w),
+                                       "+r"(rb.x), "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                     : "r"(aend), "r"(blo), "r"(bhi)
+                                     : "memory");
+                    }
+                    if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                        if (code & kSliceLamFlag) K.bump_s(vl);
+                        if (code & kSlicePiFlag) K.bump_a(vpi);
+                        if (code & kSlicePipFlag) K.bump_b(vpip);
+                        if (code & kEndFlag)
+                            slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                    }
+                }
+            } else {
             // rows software-pipelined one ahead (the read past the last row
-            // stays inside the CTA's shared window and is never used). Both
-            // parity vectors are formed before the jump, so nothing of the
-            // current row is live across it and the next row's loads need no
-            // register copies.
-            uint4 na = lds128(a0), nb = lds128(a0 + 16);
-            for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint32_t code = na.z;  // op | kind flags | end
-                const uint32_t op = nb.w;    // jump-table index (the op again, own word: no masking)
-                uint32_t X, Y;
-                if constexpr (RAND) {
-                    X = planes_parity<NT>(na.x, planes_s);
-                    Y = na.y ? planes_parity<NT>(na.y, planes_s) : 0u;
+                // stays inside the CTA's shared window and is never used). Both
+                // parity vectors are formed before the jump, so nothing of the
+                // current row is live across it and the next row's loads need no
+                // register copies.
+                uint4 na = lds128(a0), nb = lds128(a0 + 16);
+                for (uint32_t ad = a0; ad < aend; ad += 32) {
+                    const uint32_t code = na.z;  // op | kind flags | end
+                    const uint32_t op = nb.w;    // jump-table index (the op again, own word: no masking)
+                    uint32_t X = planes_parity<NT>(na.x, planes_s);
+                    uint32_t Y = na.y ? planes_parity<NT>(na.y, planes_s) : 0u;
                     if constexpr (P64) {
                         X ^= planes_parity<NT>(nb.y, planes_s + 32 * NT * 4);
                         if (nb.z) Y ^= planes_parity<NT>(nb.z, planes_s + 32 * NT * 4);
                     }
-                } else {
-                    uint32_t px, py;
-                    if constexpr (P64) {
-                        px = __popc((na.x & blo) ^ (nb.y & bhi));
-                        py = __popc((na.y & blo) ^ (nb.z & bhi));
-                    } else {
-                        px = __popc(na.x & blo);
-                        py = __popc(na.y & blo);
+                    na = lds128(ad + 32);
+                    nb = lds128(ad + 48);
+                    uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
+                    asm(PZX_SLICE_DISPATCH_ASM_XY
+                        : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                        : "r"(X), "r"(op), "r"(Y));
+                    if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                        if (code & kSliceLamFlag) K.bump_s(vl);
+                        if (code & kSlicePiFlag) K.bump_a(vpi);
+                        if (code & kSlicePipFlag) K.bump_b(vpip);
+                        if (code & kEndFlag) slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                     }
-                    // Walsh32(psi) ^ -parity(psi & base), Y likewise (== 0 for one-parity
-                    // rows: phi == 0); for P <= 32 the row carries ~Walsh32 (one SEL)
-                    if constexpr (P64) {
-                        X = na.w ^ (0u - (px & 1u));
-                        Y = nb.x ^ (0u - (py & 1u));
-                    } else {
-                        X = sel_parity(px, nb.y, na.w);
-                        Y = sel_parity(py, nb.z, nb.x);
-                    }
-                }
-                na = lds128(ad + 32);
-                nb = lds128(ad + 48);
-                uint32_t vl, vpi, vpip;  // written only by rows whose kind flags are set
-                asm(PZX_SLICE_DISPATCH_ASM_XY
-                    : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
-                    : "r"(X), "r"(op), "r"(Y));
-                if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
-                    if (code & kSliceLamFlag) K.bump_s(vl);
-                    if (code & kSlicePiFlag) K.bump_a(vpi);
-                    if (code & kSlicePipFlag) K.bump_b(vpip);
-                    if (code & kEndFlag) slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }
             __syncthreads();  // every thread is done with buffer (i & 1)

@@ -243,6 +243,59 @@ def case_body_dual(op):
     return out
 
 
+# ------------------------------------------------------- fused row loop ----
+# The whole plain-row loop of the enumerated bit-sliced kernel as one inline
+# PTX block: per row, the head forms X / Y (AND + POPC + predicate + SEL on
+# the row's Walsh / ~Walsh words; P64: XOR form), tests the row's kind / end
+# flags, advances, prefetches the next row into the same registers and jumps
+# (BRX) into the class body, which ends with ONE branch straight back to the
+# head -- two taken branches per row instead of four. The block returns to
+# C++ after a flagged row (bumps / epilogue) or at the tile end.
+# operands (outputs first, as inline asm numbers them):
+#   %0 ad (in/out), %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip (out), %8 code of the
+#   last row (out), %9-%16 row registers r0..r7 (in/out: current row in, next
+#   row out), %17 aend, %18 blo, %19 bhi
+_LOOP_MAP = {"%0": "%1", "%1": "%2", "%2": "%3", "%3": "%4", "%4": "%5", "%5": "%6", "%6": "%7",
+             "%7": "xx", "%9": "yv"}
+ROW_FLAG_MASK = (1 << 8) | (1 << 9) | (1 << 10) | (1 << 31)
+
+
+def _loop_block(name, p64):
+    n = 129
+    bodies, label_of = {}, []
+    for i in range(n):
+        key = tuple(_rename(ln, _LOOP_MAP) for ln in case_body(i, False, True))
+        if key not in bodies:
+            bodies[key] = len(bodies)
+        label_of.append(bodies[key])
+    b = ["{", ".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi;", ".reg .pred q1, q2, pl, mo, cont;",
+         "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
+         "H%=:"]
+    if p64:  # rows {psi, phi, code, W(psi)}, {W(phi), psi_hi, phi_hi, op}
+        b += ["and.b32 tq, %9, %18;", "and.b32 c0, %14, %19;", "xor.b32 tq, tq, c0;", "popc.b32 tq, tq;",
+              "and.b32 tq, tq, 1;", "neg.s32 tq, tq;", "xor.b32 xx, %12, tq;",
+              "and.b32 tq, %10, %18;", "and.b32 c0, %15, %19;", "xor.b32 tq, tq, c0;", "popc.b32 tq, tq;",
+              "and.b32 tq, tq, 1;", "neg.s32 tq, tq;", "xor.b32 yv, %13, tq;"]
+    else:    # rows {psi, phi, code, W(psi)}, {W(phi), ~W(psi), ~W(phi), op}
+        b += ["and.b32 tq, %9, %18;", "popc.b32 tq, tq;", "and.b32 tq, tq, 1;", "setp.ne.b32 q1, tq, 0;",
+              "selp.b32 xx, %14, %12, q1;",
+              "and.b32 tq, %10, %18;", "popc.b32 tq, tq;", "and.b32 tq, tq, 1;", "setp.ne.b32 q2, tq, 0;",
+              "selp.b32 yv, %15, %13, q2;"]
+    b += ["mov.b32 opi, %16;", "mov.b32 %8, %11;",
+          f"and.b32 tq, %11, {ROW_FLAG_MASK:#x};", "setp.eq.b32 pl, tq, 0;",
+          "add.u32 %0, %0, 32;", "setp.lt.u32 mo, %0, %17;", "and.pred cont, pl, mo;",
+          "ld.shared.v4.u32 {%9, %10, %11, %12}, [%0];", "ld.shared.v4.u32 {%13, %14, %15, %16}, [%0+16];",
+          "brx.idx.uni opi, ts%=;"]
+    for key, lab in sorted(bodies.items(), key=lambda kv: kv[1]):
+        b.append(f"L{lab}_%=:")
+        b.extend(key)
+        b.append("@cont bra.uni H%=;")
+        b.append("bra.uni X%=;")
+    b += ["X%=:", "}"]
+    lines = [f"#define {name} \\"] + [f'    "{x}\\n" \\' for x in b] + [""]
+    return lines
+
+
 def kind_flags(op):
     """Row code-word flag bits the C++ side reads: bit 8 lambda, 9 pi, 10 pi'."""
     _, _, _, lam, pi, pip, _ = slice_op(op)
@@ -288,6 +341,9 @@ def generate() -> str:
               "// _XY variant: operand %9 is Y itself",
               "// _XY2 variant (two slices): %0-%3 J0 J1 J2 Z (a), %4-%7 (b), %8-%10 vl vpi vpip (a),",
               "//   %11-%13 (b), %14 Xa, %15 Ya, %16 Xb, %17 Yb, %18 op"] + b32 + b64 + bxy + bxy2
+    lines += ["// fused plain-row loop (enumerated kernel): %0 ad, %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip,",
+              "//   %8 code (out), %9-%16 row registers, %17 aend, %18 blo, %19 bhi"]
+    lines += _loop_block("PZX_SLICE_ROWLOOP_P32", False) + _loop_block("PZX_SLICE_ROWLOOP_P64", True)
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")

@@ -156,3 +156,45 @@ def test_two_slice_chains_are_two_independent_mod8_adds():
                             assert out[L] == (lam >> v) & 1
                             assert out[PI] == (pi >> v) & 1
                             assert out[PIP] == (pip >> v) & 1
+
+
+@pytest.mark.parametrize("name", ["PZX_SLICE_ROWLOOP_P32", "PZX_SLICE_ROWLOOP_P64"])
+def test_fused_row_loop_bodies(name):
+    """The fused row loop's class bodies (operands renumbered: %1-%4 J0 J1 J2 Z,
+    %5-%7 vl vpi vpip, X / Y in xx / yv) are the same mod-8 chains, and every
+    body ends by looping back to the head or leaving the block."""
+    text = G.generate()
+    block = text[text.index("#define " + name + " "):]
+    block = block[:block.index("\n\n")]
+    lines = re.findall(r'"(.*?)\\n"', block)
+    table = next(ln for ln in lines if ".branchtargets" in ln)
+    targets = [int(x.strip().split("_")[0][1:]) for x in table.split(".branchtargets")[1].rstrip(";").split(",")]
+    bodies, cur = {}, None
+    for ln in lines:
+        m = re.match(r"L(\d+)_%=:", ln)
+        if m:
+            cur = int(m.group(1))
+            bodies[cur] = []
+        elif cur is not None and ln.startswith("@cont bra.uni H%="):
+            cur = None
+        elif cur is not None:
+            bodies[cur].append(ln)
+    assert len(targets) == 129 and set(targets) <= set(bodies)
+    assert block.count("@cont bra.uni H%=;") == len(bodies) and block.count("bra.uni X%=;") == len(bodies)
+    for op in range(129):
+        jb, w, z, lam, pi, pip, _ = G.slice_op(op)
+        single = op < 128 and (op & 1)
+        body = [ln.replace("xx", "%14").replace("yv", "%15") for ln in bodies[targets[op]]]
+        for v in range(4):
+            p, q = v & 1, v >> 1
+            if single and q:
+                continue
+            for j0 in range(8):
+                regs = {"%1": j0 & 1, "%2": (j0 >> 1) & 1, "%3": (j0 >> 2) & 1, "%4": 0,
+                        "%5": 0, "%6": 0, "%7": 0, "%14": p, "%15": q}
+                out = _run(body, regs)
+                jn = out["%1"] | (out["%2"] << 1) | (out["%3"] << 2)
+                if not (z >> v) & 1:
+                    assert jn == (j0 + w[v]) % 8, (op, v, j0)
+                assert out["%4"] == ((z >> v) & 1)
+                assert out["%5"] == (lam >> v) & 1 and out["%6"] == (pi >> v) & 1 and out["%7"] == (pip >> v) & 1
