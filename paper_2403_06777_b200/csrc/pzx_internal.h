@@ -70,7 +70,7 @@ struct DevTable {
     const double2* sterm_c = nullptr;
     int slice_ok = 0;
     // sorted-batch bit-sliced kernel (arbitrary word lists, n_params <= 32):
-    // rows as 2 x uint4 {psi, phi, op | flags, 0}, {psi offsets 0|1, psi offsets 2|3,
+    // rows as 2 x uint4 {psi, phi, op | flags, op}, {psi offsets 0|1, psi offsets 2|3,
     // phi offsets 0|1, phi offsets 2|3}; offset k = (k * 16 + nibble_k(mask)) *
     // kSortedTableStride (16-bit byte offsets into the per-thread Four-Russians
     // tables of the low 16 parameter bits)

@@ -1293,15 +1293,8 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
         for (int v = 0; v < 16; ++v) tab[(k * 16 + v) * kSliceThreads + threadIdx.x] = e[v];
     }
     const uint32_t tab_s = smem_u32(tab) + threadIdx.x * 4;
-    auto parity_vec = [&](uint32_t mask, uint32_t o01, uint32_t o23) -> uint32_t {
-        uint32_t x = lds32(tab_s + (o01 & 0xFFFFu)) ^ lds32(tab_s + (o01 >> 16)) ^
-                     lds32(tab_s + (o23 & 0xFFFFu)) ^ lds32(tab_s + (o23 >> 16));
-#pragma unroll
-        for (int k = 4; k < G; ++k)  // groups past the row record's 4 precomputed offsets
-            x ^= lds32(tab_s + (k * 16u + ((mask >> (4 * k)) & 15u)) * kSortedTableStride);
-        const uint32_t p0 = __popc(mask & H0) & 1u, p1 = __popc(mask & H1) & 1u;
-        return x ^ (0u - p0) ^ (M & (0u - (p0 ^ p1)));
-    };
+    // per row (PZX_SORTED_ROWLOOP_G*): X = XOR_k T_k[nibble_k(psi)] ^ hx with
+    // p0 / p1 = parity(psi & H0 / H1): hx = p1 ? (p0 ? ~0 : M) : (p0 ? ~M : 0)
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
     KindCounters<kSliceThreads> K;
@@ -1334,24 +1327,31 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
             const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
             const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
             const uint32_t aend = a0 + n * 32;
-            uint4 na = lds128(a0), nb = lds128(a0 + 16);
-            for (uint32_t ad = a0; ad < aend; ad += 32) {
-                const uint4 ra = na;  // psi, phi, code, 0
-                const uint4 rb = nb;  // psi offsets 0|1, 2|3, phi offsets 0|1, 2|3
-                na = lds128(ad + 32);
-                nb = lds128(ad + 48);
-                const uint32_t X = parity_vec(ra.x, rb.x, rb.y);
-                const uint32_t Y = ra.y ? parity_vec(ra.y, rb.z, rb.w) : 0u;
-                const uint32_t op = ra.z & 0xFFu;
-                uint32_t vl, vpi, vpip;
-                asm(PZX_SLICE_DISPATCH_ASM_XY
-                    : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
-                    : "r"(X), "r"(op), "r"(Y));
-                if (ra.z & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
-                    if (ra.z & kSliceLamFlag) K.bump_s(vl);
-                    if (ra.z & kSlicePiFlag) K.bump_a(vpi);
-                    if (ra.z & kSlicePipFlag) K.bump_b(vpip);
-                    if (ra.z & kEndFlag)
+            // fused row loop (generated PTX): rows prefetched one ahead in ra / rb
+            uint4 ra = lds128(a0), rb = lds128(a0 + 16);
+            uint32_t ad = a0;
+            while (ad < aend) {
+                uint32_t vl, vpi, vpip, code;
+                if constexpr (G > 4) {
+                    asm volatile(PZX_SORTED_ROWLOOP_G6
+                                 : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
+                                   "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
+                                   "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                 : "r"(aend), "r"(tab_s), "r"(H0), "r"(H1), "r"(M), "r"(~M)
+                                 : "memory");
+                } else {
+                    asm volatile(PZX_SORTED_ROWLOOP_G4
+                                 : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
+                                   "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
+                                   "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                 : "r"(aend), "r"(tab_s), "r"(H0), "r"(H1), "r"(M), "r"(~M)
+                                 : "memory");
+                }
+                if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (code & kSliceLamFlag) K.bump_s(vl);
+                    if (code & kSlicePiFlag) K.bump_a(vpi);
+                    if (code & kSlicePipFlag) K.bump_b(vpip);
+                    if (code & kEndFlag)
                         slice_term_epilogue<kSliceThreads, TM, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }

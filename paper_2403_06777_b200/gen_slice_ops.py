@@ -296,6 +296,77 @@ def _loop_block(name, p64):
     return lines
 
 
+# sorted-batch kernel's fused loop. Rows {psi, phi, code, op}, {psi offsets
+# 0|1, 2|3, phi offsets 0|1, 2|3} (16-bit byte offsets into the thread's
+# Four-Russians tables); X = XOR of G table words (groups 4.. computed from
+# the mask) ^ the high-part term: with p0 / p1 the parities of psi & H0 / H1,
+# hx = p1 ? (p0 ? ~0 : M) : (p0 ? ~M : 0). Y likewise, its loads predicated
+# off for one-parity rows (phi == 0 -> Y = 0).
+# operands: %0 ad, %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip, %8 code (out),
+#   %9-%16 row registers, %17 aend, %18 tab (this thread's table address),
+#   %19 H0, %20 H1, %21 M, %22 ~M
+def _sorted_par(out, mask, o01, o23, G, pred=None):
+    pp = f"@{pred} " if pred else ""
+    L = []
+    for i, (src, sh) in enumerate(((o01, False), (o01, True), (o23, False), (o23, True))):
+        L.append(f"{'shr.b32' if sh else 'and.b32'} ta, {src}, {'16' if sh else '0xFFFF'};")
+        L.append("add.u32 ta, ta, %18;")
+        L.append(f"{pp}ld.shared.u32 t{i}, [ta];")
+    for k in range(4, G):
+        L.append(f"shr.b32 ta, {mask}, {4 * k};")
+        L.append("and.b32 ta, ta, 15;")
+        L.append(f"mad.lo.u32 ta, ta, 512, %18;")
+        L.append(f"{pp}ld.shared.u32 t{k}, [ta+{k * 16 * 512}];")
+    L.append(f"and.b32 ta, {mask}, %19;")
+    L.append("popc.b32 ta, ta;")
+    L.append("and.b32 ta, ta, 1;")
+    L.append("setp.ne.b32 s0, ta, 0;")
+    L.append(f"and.b32 ta, {mask}, %20;")
+    L.append("popc.b32 ta, ta;")
+    L.append("and.b32 ta, ta, 1;")
+    L.append("setp.ne.b32 s1, ta, 0;")
+    L.append("selp.b32 tb, 0xFFFFFFFF, %21, s0;")
+    L.append("selp.b32 ta, %22, 0, s0;")
+    L.append("selp.b32 ta, tb, ta, s1;")
+    xs = " ".join(f"t{i}" for i in range(G))
+    L.append(f"xor.b32 ta, ta, t0;")
+    for i in range(1, G):
+        L.append(f"xor.b32 ta, ta, t{i};")
+    L.append(f"mov.b32 {out}, ta;" if not pred else f"selp.b32 {out}, ta, 0, {pred};")
+    _ = xs
+    return L
+
+
+def _sorted_loop_block(name, G):
+    n = 129
+    bodies, label_of = {}, []
+    for i in range(n):
+        key = tuple(_rename(ln, _LOOP_MAP) for ln in case_body(i, False, True))
+        if key not in bodies:
+            bodies[key] = len(bodies)
+        label_of.append(bodies[key])
+    regs = ", ".join(f"t{i}" for i in range(G))
+    b = ["{", f".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi, ta, tb, {regs};",
+         ".reg .pred pl, mo, cont, s0, s1, hp;",
+         "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
+         "H%=:"]
+    b += _sorted_par("xx", "%9", "%13", "%14", G)
+    b += ["setp.ne.b32 hp, %10, 0;"]
+    b += _sorted_par("yv", "%10", "%15", "%16", G, pred="hp")
+    b += ["mov.b32 opi, %12;", "mov.b32 %8, %11;",
+          f"and.b32 tq, %11, {ROW_FLAG_MASK:#x};", "setp.eq.b32 pl, tq, 0;",
+          "add.u32 %0, %0, 32;", "setp.lt.u32 mo, %0, %17;", "and.pred cont, pl, mo;",
+          "ld.shared.v4.u32 {%9, %10, %11, %12}, [%0];", "ld.shared.v4.u32 {%13, %14, %15, %16}, [%0+16];",
+          "brx.idx.uni opi, ts%=;"]
+    for key, lab in sorted(bodies.items(), key=lambda kv: kv[1]):
+        b.append(f"L{lab}_%=:")
+        b.extend(key)
+        b.append("@cont bra.uni H%=;")
+        b.append("bra.uni X%=;")
+    b += ["X%=:", "}"]
+    return [f"#define {name} \\"] + [f'    "{x}\\n" \\' for x in b] + [""]
+
+
 def kind_flags(op):
     """Row code-word flag bits the C++ side reads: bit 8 lambda, 9 pi, 10 pi'."""
     _, _, _, lam, pi, pip, _ = slice_op(op)
@@ -344,6 +415,10 @@ def generate() -> str:
     lines += ["// fused plain-row loop (enumerated kernel): %0 ad, %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip,",
               "//   %8 code (out), %9-%16 row registers, %17 aend, %18 blo, %19 bhi"]
     lines += _loop_block("PZX_SLICE_ROWLOOP_P32", False) + _loop_block("PZX_SLICE_ROWLOOP_P64", True)
+    lines += ["// fused loop of the sorted-batch kernel (G = 4 / 6 table groups): %0 ad, %1-%4 J0 J1 J2 Z,",
+              "//   %5-%7 vl vpi vpip, %8 code, %9-%16 row registers, %17 aend, %18 table, %19 H0, %20 H1,",
+              "//   %21 M, %22 ~M"]
+    lines += _sorted_loop_block("PZX_SORTED_ROWLOOP_G4", 4) + _sorted_loop_block("PZX_SORTED_ROWLOOP_G6", 6)
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")
