@@ -433,7 +433,7 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
     L.p3_off = align16(L.u_off + 8 * (M + 1));
     L.pd_off = align16(L.p3_off + 8 * (M / 2 + 1));
     L.sab_off = align16(L.pd_off + 16 * (2 * M + 1));
-    L.bytes = align16(L.sab_off + 16 * 128);
+    L.bytes = align16(L.sab_off + 16 * 256);
     std::vector<unsigned char> blob(L.bytes, 0);
     uint32_t* codes = reinterpret_cast<uint32_t*>(blob.data() + L.codes_off);
     for (int c = 0; c < 64; ++c)
@@ -460,17 +460,17 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
         a = cmul(a, pi);
         b = cmul(b, pip);
     }
-    // (sqrt2-1)^s pi^a pi'^b for s < 8, a, b < 4 (slice-kernel fast path),
-    // index s | a << 3 | b << 5, each rounded once from f128
+    // (sqrt2-1)^s pi^a pi'^b for s < 16, a, b < 4 (slice-kernel fast path),
+    // index s | a << 4 | b << 6, each rounded once from f128
     double* sab = reinterpret_cast<double*>(blob.data() + L.sab_off);
-    for (int is = 0; is < 8; ++is)
+    for (int is = 0; is < 16; ++is)
         for (int ia = 0; ia < 4; ++ia)
             for (int ib = 0; ib < 4; ++ib) {
                 C128 v{1, 0};
                 for (int k = 0; k < ia; ++k) v = cmul(v, pi);
                 for (int k = 0; k < ib; ++k) v = cmul(v, pip);
                 for (int k = 0; k < is; ++k) v = cmul(v, C128{f128_sqrt2() - 1, 0});
-                const int i = is | (ia << 3) | (ib << 5);
+                const int i = is | (ia << 4) | (ib << 6);
                 sab[2 * i] = double(v.re);
                 sab[2 * i + 1] = double(v.im);
             }

@@ -39,7 +39,7 @@ struct LutLayout {
     uint32_t u_off;      // double (sqrt2 - 1)^s, s = 0..max_rows
     uint32_t p3_off;     // double 3^m, m = 0..max_rows/2
     uint32_t pd_off;     // double2 pi^d (d > 0) / pi'^-d (d < 0), d = -max_rows..max_rows
-    uint32_t sab_off;    // double2 (sqrt2-1)^s pi^a pi'^b, s < 8, a, b < 4, index s | a << 3 | b << 5
+    uint32_t sab_off;    // double2 (sqrt2-1)^s pi^a pi'^b, s < 16, a, b < 4, index s | a << 4 | b << 6
                          // (bit-sliced kernels' epilogue fast path)
     uint32_t bytes;
     int32_t max_rows;

@@ -87,7 +87,7 @@ struct SmemLut {
     const double* u;
     const double* p3;
     const double2* pd;  // centred: pd[d], d in [-max_rows, max_rows]
-    const double2* sab;  // (sqrt2-1)^s pi^a pi'^b, s < 8, a, b < 4, index s | a << 3 | b << 5
+    const double2* sab;  // (sqrt2-1)^s pi^a pi'^b, s < 16, a, b < 4, index s | a << 4 | b << 6
 };
 
 __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* dst_bytes) {
@@ -441,9 +441,9 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 // Bit-sliced lambda / pi / pi' counters (one bit per assignment per plane,
 // up to kPlanes planes = counts < 128). The planes the epilogue fast path reads
-// (s1 < 8, a, b < 4) stay in registers; the rarely reached high planes live
+// (s1 < 16, a, b < 4) stay in registers; the rarely reached high planes live
 // in shared memory ([plane][NT], conflict-free) so they cost no registers.
-constexpr int kLoS = 3, kLoAB = 2;
+constexpr int kLoS = 4, kLoAB = 2;
 constexpr int kHiPlanes = (kPlanes - kLoS) + 2 * (kPlanes - kLoAB);  // 14 shared planes per thread
 
 template <int NT>
@@ -506,7 +506,8 @@ struct KindCounters {
     __device__ __forceinline__ uint32_t b_of(int g) { return decode<kLoAB>(B, nB, g, [&](int i) { return hb(i); }); }
 
     __device__ __forceinline__ bool any() const { return (nS | nA | nB) != 0; }
-    __device__ __forceinline__ bool fits_fast() const { return nS < 8 && nA < 4 && nB < 4; }
+    __device__ __forceinline__ bool fits_fast() const { return nS < 16 && nA < 4 && nB < 4; }
+    __device__ __forceinline__ bool has_pi() const { return (nA | nB) != 0; }
     __device__ __forceinline__ void reset() {
         for (int i = kLoS; i < kPlanes && (nS >> i); ++i) *hs(i) = 0;
         for (int i = kLoAB; i < kPlanes && (nA >> i); ++i) *ha(i) = 0;
@@ -687,11 +688,13 @@ __device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
 // Term epilogue shared by the bit-sliced kernels: fold 6*s1 into J, build
 // the warp's C * w^j table, and add every live assignment's term value into its
 // fp64 accumulator; resets the per-term state. Fast path (every counter fits
-// its field: s1 < 8, a, b < 4): per group of 4 assignments two byte-keys
-// words are built by nib_spread -- (j | Z << 3) and (s1 | a << 3 | b << 5) --
+// its field: s1 < 16, a, b < 4): per group of 4 assignments two byte-keys
+// words are built by nib_spread -- (j | Z << 3) and (s1 | a << 4 | b << 6) --
 // then each assignment is 2 table loads + 4 DFMA into its accumulator, no
 // branches (Z-marked assignments read a zero entry).
-template <int NT, bool TM, bool KINDS, bool ROLL>
+// KINDS: some lambda / pi / pi' rows (the (sqrt2-1)^s pi^a pi'^b table is
+// read); AB: some pi / pi' rows (else their planes are known zero and skipped)
+template <int NT, bool TM, bool KINDS, bool ROLL, bool AB = true>
 __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
                                                     uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
                                                     const KindCounters<NT>& K) {
@@ -699,11 +702,13 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
     const uint32_t(&A)[kLoAB] = K.A;
     const uint32_t(&B)[kLoAB] = K.B;
     const Nib j0 = nib_split(J0), j1 = nib_split(J1), j2 = nib_split(J2), z = nib_split(Z);
-    Nib s0{}, s1{}, s2{}, a0{}, a1{}, b0{}, b1{};
+    Nib s0{}, s1{}, s2{}, s3{}, a0{}, a1{}, b0{}, b1{};
     if constexpr (KINDS) {
-        s0 = nib_split(S[0]); s1 = nib_split(S[1]); s2 = nib_split(S[2]);
-        a0 = nib_split(A[0]); a1 = nib_split(A[1]);
-        b0 = nib_split(B[0]); b1 = nib_split(B[1]);
+        s0 = nib_split(S[0]); s1 = nib_split(S[1]); s2 = nib_split(S[2]); s3 = nib_split(S[3]);
+        if constexpr (AB) {
+            a0 = nib_split(A[0]); a1 = nib_split(A[1]);
+            b0 = nib_split(B[0]); b1 = nib_split(B[1]);
+        }
     }
     auto mac = [&](double2& o, const double2 c, const double2 f) {
         if constexpr (KINDS) {
@@ -719,10 +724,12 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
     // the term values of group m (4 assignments): c[r] * f[r]
     auto group = [&](int m, double2 (&c)[4], double2 (&f)[4]) {
         const uint32_t kj = nib_spread(j0, m, 0) | nib_spread(j1, m, 1) | nib_spread(j2, m, 2) | nib_spread(z, m, 3);
-        uint32_t ks = 0;
-        if constexpr (KINDS)
-            ks = nib_spread(s0, m, 0) | nib_spread(s1, m, 1) | nib_spread(s2, m, 2) | nib_spread(a0, m, 3) |
-                 nib_spread(a1, m, 4) | nib_spread(b0, m, 5) | nib_spread(b1, m, 6);
+        uint32_t ks = 0;  // s | a << 4 | b << 6
+        if constexpr (KINDS) {
+            ks = nib_spread(s0, m, 0) | nib_spread(s1, m, 1) | nib_spread(s2, m, 2) | nib_spread(s3, m, 3);
+            if constexpr (AB)
+                ks |= nib_spread(a0, m, 4) | nib_spread(a1, m, 5) | nib_spread(b0, m, 6) | nib_spread(b1, m, 7);
+        }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             c[r] = crot[__byte_perm(kj, 0u, 0x4440u | uint32_t(r))];
@@ -836,7 +843,8 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
     if (!kinds) {
         slice_epilogue_fast<NT, TM, false, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
     } else if (K.fits_fast()) {
-        slice_epilogue_fast<NT, TM, true, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
+        if (K.has_pi()) slice_epilogue_fast<NT, TM, true, ROLL, true>(L, crot, acc, J0, J1, J2, Z, K);
+        else slice_epilogue_fast<NT, TM, true, ROLL, false>(L, crot, acc, J0, J1, J2, Z, K);
     } else if constexpr (TM) {
         tmem_wait_st();
 #pragma unroll 1
