@@ -1553,8 +1553,11 @@ bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
 
 // bit-sliced kernels: 32-thread CTAs when the batch cannot give every SM a
 // 128-thread block (small enumerated batches with huge tables, e.g. C4)
+// 32-thread CTAs only when a 128-thread CTA would leave warps idle (batches
+// of a few thousand assignments, C4); otherwise 128 threads with TMEM
+// accumulators -- term chunking supplies the CTAs a small batch lacks
 int slice_threads(const LaunchReq& r) {
-    return r.n < uint64_t(kSliceThreads) * kSliceG * 148 ? 32 : kSliceThreads;
+    return r.n < uint64_t(4) * kSliceThreads * kSliceG ? 32 : kSliceThreads;
 }
 
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
