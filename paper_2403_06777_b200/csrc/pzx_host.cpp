@@ -651,7 +651,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;
-        c = std::min<uint64_t>(c, nterms);
+        c = std::min<uint64_t>(c, kc == KC_SLICEWC ? std::max<uint64_t>(1, nterms / kWarpChunksHost) : nterms);
         c = std::min<uint64_t>(c, std::max<uint64_t>(1, (uint64_t(1) << 30) / (r.n * 16 + 1)));
         chunks = int(std::min<uint64_t>(c, 65535));
         // round the grid up to whole waves when that does not need more chunks than terms
@@ -662,6 +662,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
             if (c2 <= nterms && c2 <= 65535 && c2 * (r.n * 16) <= (uint64_t(1) << 30)) chunks = int(c2);
         }
     }
+    if (kc == KC_SLICEWC) chunks *= kWarpChunksHost;  // 4 warp chunks per CTA row, always partials
     r.n_chunks = chunks;
     if (chunks > 1) {
         std::vector<uint64_t> b;

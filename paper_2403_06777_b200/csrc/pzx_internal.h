@@ -83,7 +83,9 @@ constexpr int kSortedGroupsWide = 6;          // parameters 0..23 via tables (sp
 constexpr int kSortedLowBits = 4 * kSortedGroups;
 constexpr uint32_t kSortedTableStride = 128 * 4;  // bytes between table rows (128 threads x 4 B)
 
-enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5, KC_SLICE2 = 6 };
+enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5, KC_SLICE2 = 6,
+                    KC_SLICEWC = 7 /* small enumerated batches: 4 warps x 4 term chunks per CTA (auto only) */ };
+constexpr int kWarpChunksHost = 4;  // term chunks per CTA of the warp-chunk kernel
 
 struct LaunchReq {
     const uint64_t* d_asg = nullptr;  // nullptr: enumerated first .. first + n - 1

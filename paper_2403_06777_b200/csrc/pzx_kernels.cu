@@ -1112,6 +1112,137 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
     slice_store_results<NT, TM>(r, off, acc);
 }
 
+// ------------------------------------------------- warp-chunk kernel ----
+// Small enumerated batches (a few thousand assignments, e.g. C4's 2^10
+// marginal parameters against 2e8 rows): all 4 warps of a CTA own the SAME
+// 32 x 32 assignments and walk 4 different term chunks (chunk = 4 blockIdx.y
+// + warp), each with its own TMA row pipeline, so the CTA keeps 128 threads
+// with TMEM accumulators (16 warps / SM) instead of 1-warp CTAs with shared-
+// memory accumulators. Every warp's partial amplitudes go to its own chunk
+// slot; the fixed-order chunk reduction sums them.
+constexpr int kWarpChunks = kSliceThreads / 32;
+static_assert(kWarpChunks == kWarpChunksHost, "warp-chunk count shared with the host");
+
+template <bool P64>
+__host__ __device__ constexpr uint32_t slicewc_lut_offset() {
+    return kWarpChunks * 2 * kSliceTile * 32 + kWarpChunks * 16 + 16;
+}
+
+template <bool P64>
+size_t slicewc_smem_bytes(const DevTable& t) {
+    const uint32_t amp_off = (slicewc_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    const size_t b = amp_off + (kSliceThreads / 32) * kWarpScratch * 16 + size_t(kHiPlanes) * kSliceThreads * 4;
+    return b > kTmemCtaSmem ? b : kTmemCtaSmem;
+}
+
+template <bool P64>
+__global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTable t, const LaunchReq r) {
+    constexpr int NT = kSliceThreads;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t tmem_base_s;
+    // the warp index through a lane-0 shuffle: provably warp-uniform, so the
+    // row loop's branches stay uniform (no divergence bookkeeping)
+    const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31u;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpChunks * 2 * kSliceTile * 32) + 2 * warp;
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    const SmemLut L = stage_lut(t, smem + slicewc_lut_offset<P64>());
+    __syncthreads();
+    const uint32_t amp_off = (slicewc_lut_offset<P64>() + t.lut_layout.bytes + 127u) & ~127u;
+    double2* crot = reinterpret_cast<double2*>(smem + amp_off) + warp * kWarpScratch;
+    uint32_t* hi_planes = reinterpret_cast<uint32_t*>(smem + amp_off + (NT / 32) * kWarpScratch * 16);
+    SliceAcc<NT, true> acc{nullptr, 0u};
+    acc.taddr = tmem_alloc_cta(&tmem_base_s);
+    acc.zero();
+
+    const uint32_t chunk = blockIdx.y * kWarpChunks + warp;
+    const uint64_t tb = r.d_chunk_terms[chunk], te = r.d_chunk_terms[chunk + 1];
+    const uint64_t off = (uint64_t(blockIdx.x) * 32 + lane) * kSliceG;
+    const uint64_t base = r.d_asg ? (off < r.n ? r.d_asg[off] : 0) : r.first + off;
+    const uint32_t blo = uint32_t(base), bhi = uint32_t(base >> 32);
+
+    uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
+    KindCounters<NT> K;
+    K.init(hi_planes + threadIdx.x);
+
+    if (tb < te) {
+        uint4* tiles = reinterpret_cast<uint4*>(smem) + warp * (2 * kSliceTile * 2);
+        const uint32_t tiles_s = smem_u32(tiles);
+        const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
+        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        auto issue = [&](uint32_t tile) {
+            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
+            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint32_t bytes = uint32_t(n) * 32u;
+            uint64_t* bar = &bars[tile & 1];
+            mbar_expect_tx(bar, bytes);
+            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.srows + rr * 2, bytes, bar);
+        };
+        if (lane == 0) {
+            if (ntiles > 0) issue(0);
+            if (ntiles > 1) issue(1);
+        }
+        TermC tc;
+        termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
+        for (uint32_t i = 0; i < ntiles; ++i) {
+            mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
+            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
+            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint32_t aend = a0 + n * 32;
+            uint4 ra = lds128(a0), rb = lds128(a0 + 16);
+            uint32_t ad = a0;
+            while (ad < aend) {
+                uint32_t vl, vpi, vpip, code;
+                if constexpr (P64) {
+                    asm volatile(PZX_SLICE_ROWLOOP_P64
+                                 : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
+                                   "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
+                                   "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                 : "r"(aend), "r"(blo), "r"(bhi)
+                                 : "memory");
+                } else {
+                    asm volatile(PZX_SLICE_ROWLOOP_P32
+                                 : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
+                                   "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
+                                   "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                 : "r"(aend), "r"(blo), "r"(bhi)
+                                 : "memory");
+                }
+                if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
+                    if (code & kSliceLamFlag) K.bump_s(vl);
+                    if (code & kSlicePiFlag) K.bump_a(vpi);
+                    if (code & kSlicePipFlag) K.bump_b(vpip);
+                    if (code & kEndFlag)
+                        slice_term_epilogue<NT, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                }
+            }
+            __syncwarp();  // the warp is done with buffer (i & 1)
+            if (lane == 0 && i + 2 < ntiles) {
+                fence_proxy_async();
+                issue(i + 2);
+            }
+        }
+    }
+    // this warp's partial amplitudes -> chunk slot `chunk`
+    tmem_wait_st();
+#pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(acc.taddr + 32u * ch, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t idx = off + 8 * ch + q;
+            if (idx < r.n) r.d_partial[uint64_t(chunk) * r.n + idx] = v2d(v + 4 * q);
+        }
+    }
+    tmem_free_cta(tmem_base_of(acc.taddr));
+}
+
 // ---------------------------------------------------- two-slice kernel ----
 // Enumerated batches, 64 assignments per thread: slice a = base + g, slice b
 // = base + 32 + g (base % 64 == 0). Both slices share the row load, the
@@ -1495,6 +1626,13 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
         kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
+    if (kc == KC_SLICEWC) {
+        const size_t sm = slicewc_smem_bytes<P64>(t);
+        cudaError_t e = cudaFuncSetAttribute(k_eval_slice_wc<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        k_eval_slice_wc<P64><<<dim3(grid.x, grid.y / kWarpChunks), kSliceThreads, sm, r.stream>>>(t, r);
+        return cudaGetLastError();
+    }
     if (kc == KC_SLICE2) {
         const size_t sm = slice2_smem_bytes<P64>(t);
         cudaError_t e = cudaFuncSetAttribute(k_eval_slice2<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -1533,7 +1671,8 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     if (enumerated && t.slice_ok && (r.first % (2 * kSliceG)) == 0 && slice_threads(r) == kSliceThreads &&
         tmem_accumulators() && slice2_enabled())
         return KC_SLICE2;
-    if (enumerated && t.slice_ok && (r.first % kSliceG) == 0) return KC_SLICE;
+    if (enumerated && t.slice_ok && (r.first % kSliceG) == 0)
+        return (slice_threads(r) == 32 && tmem_accumulators()) ? KC_SLICEWC : KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
     // arbitrary word lists: sort, then the bit-sliced kernel with per-thread
     // Four-Russians tables (needs n_params <= 32 and terms <= 127 rows)
@@ -1561,7 +1700,8 @@ int slice_threads(const LaunchReq& r) {
 }
 
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
-    const uint64_t per = kc == KC_SLICE2                   ? uint64_t(kSliceThreads) * 2 * kSliceG
+    const uint64_t per = kc == KC_SLICEWC                  ? uint64_t(32) * kSliceG
+                       : kc == KC_SLICE2                   ? uint64_t(kSliceThreads) * 2 * kSliceG
                        : kc == KC_SORTED                   ? uint64_t(kSliceThreads) * kSliceG
                        : (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(slice_threads(r)) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
@@ -1577,7 +1717,12 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
     cudaError_t e;
 #define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
     const bool tm = tmem_accumulators();
-    if (kc == KC_SLICE2) {
+    if (kc == KC_SLICEWC) {
+        sm = t.p64 ? slicewc_smem_bytes<true>(t) : slicewc_smem_bytes<false>(t);
+        auto kern = t.p64 ? k_eval_slice_wc<true> : k_eval_slice_wc<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+    } else if (kc == KC_SLICE2) {
         sm = t.p64 ? slice2_smem_bytes<true>(t) : slice2_smem_bytes<false>(t);
         auto kern = t.p64 ? k_eval_slice2<true> : k_eval_slice2<false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
