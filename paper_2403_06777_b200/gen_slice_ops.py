@@ -268,9 +268,13 @@ def _loop_block(name, p64):
         if key not in bodies:
             bodies[key] = len(bodies)
         label_of.append(bodies[key])
-    b = ["{", ".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi;", ".reg .pred q1, q2, pl, mo, cont;",
+    b = ["{", ".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi, nc;", ".reg .pred q1, q2, pl, mo, cont;",
          "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
-         "H%=:"]
+         "H%=:",
+         # the next row's code word first: its consumer (the next head's flag
+         # test, which the compiler runs on the uniform datapath) then waits on
+         # a load issued a whole head earlier
+         "ld.shared.u32 nc, [%0+40];"]
     if p64:  # rows {psi, phi, code, W(psi)}, {W(phi), psi_hi, phi_hi, op}
         b += ["and.b32 tq, %9, %18;", "and.b32 c0, %14, %19;", "xor.b32 tq, tq, c0;", "popc.b32 tq, tq;",
               "and.b32 tq, tq, 1;", "neg.s32 tq, tq;", "xor.b32 xx, %12, tq;",
@@ -285,6 +289,7 @@ def _loop_block(name, p64):
           f"and.b32 tq, %11, {ROW_FLAG_MASK:#x};", "setp.eq.b32 pl, tq, 0;",
           "add.u32 %0, %0, 32;", "setp.lt.u32 mo, %0, %17;", "and.pred cont, pl, mo;",
           "ld.shared.v4.u32 {%9, %10, %11, %12}, [%0];", "ld.shared.v4.u32 {%13, %14, %15, %16}, [%0+16];",
+          "mov.b32 %11, nc;",
           "brx.idx.uni opi, ts%=;"]
     for key, lab in sorted(bodies.items(), key=lambda kv: kv[1]):
         b.append(f"L{lab}_%=:")
