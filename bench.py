@@ -472,7 +472,8 @@ def main():
     ap.add_argument("--split", default="assign", choices=["assign", "weak", "terms"],
                     help="multi-GPU: shard the batch (strong), a full batch per rank (weak), or split the "
                          "terms + NCCL all-reduce (strong)")
-    ap.add_argument("--assign", type=int, default=0, help="override the per-GPU batch size (0: config's)")
+    ap.add_argument("--assign", type=int, default=0,
+                    help="override the config's batch size (0: config's); sharded across ranks unless --split weak")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-per-thread", type=int, default=2)
     ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand", "sorted", "slice2"],
