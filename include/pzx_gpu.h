@@ -173,6 +173,19 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
                                uint32_t flags, void* stream);
+/* SPEC BackendContract: capability descriptor of this backend. */
+typedef struct {
+    uint32_t max_params;          /* 64 */
+    uint32_t max_rows_per_term;   /* of the bit-sliced kernels (longer terms use the POPC / gray kernels) */
+    uint64_t max_rows_in_flight;  /* table rows staged in shared memory per CTA (TMA tiles) */
+    uint64_t preferred_batch;     /* assignments per call that fill the GPU */
+    uint32_t exact;               /* 0: fp64 amplitudes (1e-12 relative); phase indices are exact */
+    uint32_t deterministic;       /* 1: fixed-order reductions, run-to-run identical */
+    uint32_t n_sm;
+    uint32_t tmem_accumulators;   /* 1 when the bit-sliced kernels keep accumulators in TMEM */
+} pzx_backend_contract;
+pzx_status pzx_backend_contract_get(pzx_ctx* ctx, pzx_backend_contract* out);
+
 /* PZX1 binary table codec (SPEC "External Interfaces"): the
  * normalised table as header {"PZX1", u32 n_params, u64 m, u64 n_max, u64 R =
  * m*n_max}, i64 constants[m][5], then field-major padded rows u8 flags[R] (1 =

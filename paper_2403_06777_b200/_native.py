@@ -19,7 +19,7 @@ EXPORTS = (
     "pzx_evaluate_device", "pzx_amp_to_prob_device", "pzx_synchronize",
     "pzx_debug_phase_indices", "pzx_debug_term_codes", "pzx_table_compile_host", "pzx_class_table",
     "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample", "pzx_pzx1_encode", "pzx_pzx1_encode_expr",
-    "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1",
+    "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -42,6 +42,13 @@ class TableView(C.Structure):
         ("term_row_offset", u64p), ("term_coef", i64p),
         ("psi_mask", u64p), ("phi_mask", u64p), ("k_alpha", u8p), ("k_beta", u8p),
     ]
+
+
+class BackendContract(C.Structure):
+    _fields_ = [("max_params", C.c_uint32), ("max_rows_per_term", C.c_uint32),
+                ("max_rows_in_flight", C.c_uint64), ("preferred_batch", C.c_uint64),
+                ("exact", C.c_uint32), ("deterministic", C.c_uint32), ("n_sm", C.c_uint32),
+                ("tmem_accumulators", C.c_uint32)]
 
 
 class TermCode(C.Structure):
@@ -84,6 +91,7 @@ def lib() -> C.CDLL:
                                       vp, vp, C.c_uint32, vp]
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     L.pzx_synchronize.argtypes = [vp]
+    L.pzx_backend_contract_get.argtypes = [vp, C.POINTER(BackendContract)]
     L.pzx_pzx1_encode.argtypes = [C.POINTER(TableView), u8p, C.c_uint64, u64p]
     L.pzx_pzx1_encode_expr.argtypes = [C.POINTER(ExprView), u8p, C.c_uint64, u64p]
     L.pzx_pzx1_info.argtypes = [u8p, C.c_uint64, C.POINTER(C.c_uint32), u64p, u64p]

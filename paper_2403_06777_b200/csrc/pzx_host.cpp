@@ -939,6 +939,19 @@ pzx_table_view view_of(const Rows& r) {
 }  // namespace
 }  // extern "C++"
 
+pzx_status pzx_backend_contract_get(pzx_ctx* ctx, pzx_backend_contract* out) {
+    if (!ctx || !out) return PZX_E_INVALID;
+    out->max_params = 64;
+    out->max_rows_per_term = uint32_t(kSegRows);
+    out->max_rows_in_flight = 2 * 64;  // two 64-row TMA tiles per CTA (per warp for small batches)
+    out->preferred_batch = uint64_t(ctx->n_sm) * 4 * 128 * 32;
+    out->exact = 0;
+    out->deterministic = 1;
+    out->n_sm = uint32_t(ctx->n_sm);
+    out->tmem_accumulators = tmem_accumulators() ? 1u : 0u;
+    return PZX_OK;
+}
+
 pzx_status pzx_pzx1_encode(const pzx_table_view* view, uint8_t* buf, uint64_t cap, uint64_t* len) {
     return encode_view(view, buf, cap, len);
 }

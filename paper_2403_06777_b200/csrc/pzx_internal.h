@@ -121,6 +121,7 @@ cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, v
 // Grid policy helpers (host)
 int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
+bool tmem_accumulators();
 int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_groups = kSortedGroups);
 int slice_threads(const LaunchReq& r);
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc);

@@ -33,6 +33,15 @@
 
 namespace pzxb {
 
+// PZX_ACC=smem keeps the accumulators in shared memory (A/B comparisons)
+bool tmem_accumulators() {
+    static const bool on = [] {
+        const char* e = std::getenv("PZX_ACC");
+        return !(e && std::string(e) == "smem");
+    }();
+    return on;
+}
+
 namespace {
 
 constexpr int kTileRows = 256;
@@ -544,14 +553,6 @@ bool slice2_enabled() {
     return on;
 }
 
-// PZX_ACC=smem keeps the accumulators in shared memory (A/B comparisons)
-bool tmem_accumulators() {
-    static const bool on = [] {
-        const char* e = std::getenv("PZX_ACC");
-        return !(e && std::string(e) == "smem");
-    }();
-    return on;
-}
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"

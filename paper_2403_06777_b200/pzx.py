@@ -382,6 +382,12 @@ class Context:
         _check(N.lib().pzx_table_upload(self.handle, C.byref(v), C.byref(h)), self.handle)
         return DeviceTable(self, h)
 
+    def backend_contract(self) -> dict:
+        """SPEC BackendContract: this backend's capabilities."""
+        c = N.BackendContract()
+        _check(N.lib().pzx_backend_contract_get(self.handle, C.byref(c)), self.handle)
+        return {k: getattr(c, k) for k, _ in N.BackendContract._fields_}
+
     def upload_pzx1(self, data: bytes) -> DeviceTable:
         """Upload a PZX1-encoded table (see encode_pzx1)."""
         buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)

@@ -387,3 +387,9 @@ def test_weak_sample_product_distribution(ctx):
     assert np.all(ctx.weak_sample(det, 1000, seed=1) == 0b010)
     with pytest.raises(P.Error):   # table k must take k + 1 parameters
         ctx.weak_sample([tables[1], tables[0]], 10)
+
+
+def test_backend_contract(ctx):
+    c = ctx.backend_contract()
+    assert c["max_params"] == 64 and c["deterministic"] == 1 and c["exact"] == 0
+    assert c["max_rows_per_term"] == 127 and c["n_sm"] > 0 and c["preferred_batch"] > 0
