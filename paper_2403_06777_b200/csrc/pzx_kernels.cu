@@ -743,23 +743,22 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
         // (ROLL: a rolled loop over pairs of groups keeps the epilogue's code
         // small -- pays off in the sorted kernel, not in the slice kernel)
         tmem_wait_st();  // the previous term's stores have landed
-        uint32_t v[2][16];
-        tmem_ld16(acc.taddr, v[0]);
         auto pair = [&](int m2) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int m = m2 + h;
                 double2 c[4], f[4];
+                uint32_t v[16];
+                tmem_ld16(acc.taddr + 16u * m, v);
                 group(m, c, f);
                 tmem_wait_ld();
-                if (h == 0 || m2 + 2 < 8) tmem_ld16(acc.taddr + 16u * (m + 1), v[h ^ 1]);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    double2 o = v2d(v[h] + 4 * r);
+                    double2 o = v2d(v + 4 * r);
                     mac(o, c[r], f[r]);
-                    d2v(o, v[h] + 4 * r);
+                    d2v(o, v + 4 * r);
                 }
-                tmem_st16(acc.taddr + 16u * m, v[h]);
+                tmem_st16(acc.taddr + 16u * m, v);
             }
         };
         if constexpr (ROLL) {
