@@ -70,6 +70,7 @@ enum { PZX_NODE = 0, PZX_PHASE_PAIR = 1, PZX_HALF_PI = 2, PZX_PI_PAIR = 3 };
 enum {
     PZX_PROB_ABS2 = 1u << 0,  /* prob[i] = |amp_i|^2 (Born rule)            */
     PZX_PROB_REAL = 1u << 1,  /* prob[i] = Re(amp_i) (doubled diagram)      */
+    PZX_ACCUMULATE = 1u << 2, /* pzx_evaluate_device: add into d_amp (term ranges)  */
     PZX_KERNEL_GENERAL = 1u << 8, /* force the per-assignment POPC kernel          */
     PZX_KERNEL_GRAY = 1u << 9,    /* force the enumerated (low-bit Walsh) kernel   */
     PZX_KERNEL_SLICE = 1u << 10,  /* force the bit-sliced enumerated kernel        */
@@ -168,7 +169,8 @@ pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, 
  * d_assignments may be NULL for the enumerated batch starting at `first`.
  * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)
  * gives partial amplitudes for the term split; d_amp receives 2n doubles,
- * d_prob n doubles (either may be NULL). accumulate != 0 adds into d_amp. */
+ * d_prob n doubles (either may be NULL). With PZX_ACCUMULATE the amplitudes are
+ * added into d_amp (and d_prob is computed from the sum). */
 pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,

@@ -1243,7 +1243,7 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
     r.d_amp = reinterpret_cast<double2*>(d_amp);
     r.d_prob = d_prob;
     r.prob_mode = prob_mode_of(flags);
-    r.accumulate = 0;
+    r.accumulate = (flags & PZX_ACCUMULATE) ? 1 : 0;
     if (!d_amp && !d_prob) return PZX_OK;
     return run_eval(ctx, t, r, flags);
 }

@@ -298,6 +298,7 @@ KERNEL_GENERAL = 1 << 8
 KERNEL_GRAY = 1 << 9
 KERNEL_SLICE = 1 << 10
 KERNEL_SLICE_RAND = 1 << 11
+ACCUMULATE = 1 << 2
 KERNEL_SORTED = 1 << 12
 KERNEL_SLICE2 = 1 << 13
 
@@ -648,6 +649,6 @@ __all__ = [
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
     "PhaseTable", "encode_pzx1", "decode_pzx1", "pzx1_to_json", "pzx1_from_json",
-    "PROB_ABS2", "PROB_REAL", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
+    "PROB_ABS2", "PROB_REAL", "ACCUMULATE", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
 ]
 _ = builtins

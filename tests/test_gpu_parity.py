@@ -303,6 +303,12 @@ def test_device_pointer_api_and_term_split(ctx):
     torch.cuda.synchronize()
     s = (amp + part).cpu().numpy().view(np.complex128)
     assert_close(s, full, 1e-13)
+    # PZX_ACCUMULATE: the second range adds into the first one's amplitudes
+    acc = torch.zeros(2 * n, dtype=torch.float64, device="cuda:0")
+    ctx.evaluate_device(t, n, first=0, term_begin=0, term_end=cut, d_amp=acc.data_ptr(), stream=st)
+    ctx.evaluate_device(t, n, first=0, term_begin=cut, d_amp=acc.data_ptr(), flags=P.ACCUMULATE, stream=st)
+    torch.cuda.synchronize()
+    assert_close(acc.cpu().numpy().view(np.complex128), full, 1e-13)
     prob = torch.empty(n, dtype=torch.float64, device="cuda:0")
     both = amp + part
     ctx.amp_to_prob_device(both.data_ptr(), n, prob.data_ptr(), stream=st)
