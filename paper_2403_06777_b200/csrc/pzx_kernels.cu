@@ -712,10 +712,13 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
         }
     }
     auto mac = [&](double2& o, const double2 c, const double2 f) {
-        if constexpr (KINDS) {
+        if constexpr (KINDS && AB) {
             o.x = fma(c.x, f.x, o.x);
             o.y = fma(c.x, f.y, o.y);
             o.x = fma(-c.y, f.y, o.x);
+            o.y = fma(c.y, f.x, o.y);
+        } else if constexpr (KINDS) {  // pi-free term: the table entry (sqrt2-1)^s is real
+            o.x = fma(c.x, f.x, o.x);
             o.y = fma(c.y, f.x, o.y);
         } else {
             o.x += c.x;
@@ -734,7 +737,12 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             c[r] = crot[__byte_perm(kj, 0u, 0x4440u | uint32_t(r))];
-            if constexpr (KINDS) f[r] = L.sab[__byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
+            if constexpr (KINDS && AB) {
+                f[r] = L.sab[__byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
+            } else if constexpr (KINDS) {
+                f[r].x = reinterpret_cast<const double*>(L.sab)[2 * __byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
+                f[r].y = 0.0;
+            }
         }
     };
     if constexpr (TM) {
