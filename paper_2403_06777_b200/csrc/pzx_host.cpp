@@ -626,18 +626,31 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         if ((st = cuda_err(ctx, grow(&ctx->d_sort, &ctx->sort_cap, sort_scratch_bytes(r.n) + 256), "alloc sort scratch"))) return st;
         if ((st = cuda_err(ctx, sort_words(r.d_asg, r.n, t->dev.n_params, ctx->d_sort, &r.d_sorted, &r.d_perm,
                                            r.stream, &ctx->launches), "sort words"))) return st;
-        uint64_t spread = 0;
-        void* tmp8 = static_cast<unsigned char*>(ctx->d_sort) + sort_scratch_bytes(r.n);
-        if ((st = cuda_err(ctx, sorted_max_spread(r.d_sorted, r.n, tmp8, &spread, r.stream, &ctx->launches), "spread"))) return st;
-        // groups of 32 sorted words must span < 2^(4 G): 16 table bits for dense
-        // batches, 24 (wide tables) for sparse ones such as 2^16 random 32-bit words
-        r.sorted_groups = spread < (uint64_t(1) << (4 * kSortedGroups)) ? kSortedGroups : kSortedGroupsWide;
-        if (spread >= (uint64_t(1) << (4 * kSortedGroupsWide))) {  // too sparse for two high parts per thread
+        // regroup: every thread's 32 words must share their high part (bits >= 4 G);
+        // 16 table bits for dense batches, 24 (wide tables) when 16 would pad by
+        // more than 25 % (sparse batches such as 2^16 random 32-bit words)
+        void* gs = static_cast<unsigned char*>(ctx->d_sort) + sort_base_bytes(r.n);
+        uint64_t slots = 0;
+        int groups = kSortedGroups;
+        if ((st = cuda_err(ctx, group_slots(r.d_sorted, r.n, 4 * kSortedGroups, gs, &slots, r.stream, &ctx->launches), "group"))) return st;
+        if (slots > r.n + r.n / 4 + 32) {
+            groups = kSortedGroupsWide;
+            if ((st = cuda_err(ctx, group_slots(r.d_sorted, r.n, 4 * kSortedGroupsWide, gs, &slots, r.stream, &ctx->launches), "group"))) return st;
+        }
+        if (slots > 2 * r.n + 32) {  // sparser than half-filled groups: the POPC kernel is faster
             if (r.kernel == KC_SORTED)
-                return set_err(ctx, PZX_E_INVALID, "sorted kernel: batch too sparse (32-word groups span >= 2^24)");
+                return set_err(ctx, PZX_E_INVALID, "sorted kernel: batch too sparse (high-part groups under half full)");
             kc = KC_GENERAL;
             r.d_sorted = nullptr;
             r.d_perm = nullptr;
+        } else {
+            const uint64_t* pw = nullptr;
+            const uint32_t* pp = nullptr;
+            if ((st = cuda_err(ctx, group_sorted(r.d_sorted, r.d_perm, r.n, 4 * groups, gs, &pw, &pp, &slots, r.stream, &ctx->launches), "group words"))) return st;
+            r.d_sorted = pw;
+            r.d_perm = pp;
+            r.n = slots;  // the kernel and the chunk reduction run over the padded slots
+            r.sorted_groups = groups;
         }
     }
     // grid policy: split the terms into chunks so that the grid is >= kWaves

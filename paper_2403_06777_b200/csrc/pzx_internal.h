@@ -112,8 +112,12 @@ struct LaunchReq {
 // scratch must hold sort_scratch_bytes(n) bytes; outputs live inside scratch.
 size_t sort_scratch_bytes(uint64_t n);
 // max over 32-word groups of (last - first) of the sorted batch (device -> host)
-cudaError_t sorted_max_spread(const uint64_t* d_sorted, uint64_t n, void* d_tmp8, uint64_t* h_out,
-                              cudaStream_t s, uint64_t* launches);
+cudaError_t group_sorted(const uint64_t* d_sorted, const uint32_t* d_perm, uint64_t n, uint32_t low, void* scratch,
+                         const uint64_t** d_pw, const uint32_t** d_pp, uint64_t* n_slots, cudaStream_t s,
+                         uint64_t* launches);
+cudaError_t group_slots(const uint64_t* d_sorted, uint64_t n, uint32_t low, void* scratch, uint64_t* n_slots,
+                        cudaStream_t s, uint64_t* launches);
+size_t sort_base_bytes(uint64_t n);
 cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, void* scratch,
                        const uint64_t** d_sorted, const uint32_t** d_perm, cudaStream_t s,
                        uint64_t* launches);

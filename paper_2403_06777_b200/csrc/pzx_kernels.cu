@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "pzx_classes.h"
 #include "pzx_internal.h"
@@ -276,7 +277,10 @@ __device__ __forceinline__ void store_result(const LaunchReq& r, uint64_t idx, d
         r.d_partial[uint64_t(blockIdx.y) * r.n + idx] = amp;
         return;
     }
-    if (r.d_perm) idx = r.d_perm[idx];  // sorted batch: back to the caller's order
+    if (r.d_perm) {  // sorted batch: back to the caller's order (~0: a padding slot)
+        idx = r.d_perm[idx];
+        if (idx == 0xFFFFFFFFu) return;
+    }
     if (r.accumulate) {
         const double2 o = r.d_amp[idx];
         amp.x += o.x;
@@ -1424,11 +1428,8 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
         const uint64_t idx = off + g < r.n ? off + g : r.n - 1;  // pad with the last word (keeps order)
         w[g] = uint32_t(r.d_sorted[idx]);
     }
-    const uint32_t hmask = ~((1u << kLow) - 1u);
-    const uint32_t H0 = w[0] & hmask, H1 = H0 + (1u << kLow);
-    uint32_t M = 0;  // assignments whose high part is H1 (the host guarantees spread < 2^kLow)
-#pragma unroll
-    for (int g = 0; g < 32; ++g) M |= uint32_t((w[g] & hmask) != H0) << g;
+    // the host padded the sorted words into groups of 32 sharing one high part
+    const uint32_t H0 = w[0] & ~((1u << kLow) - 1u);
     transpose32(w);  // w[i] = plane i (bit g = bit i of word g)
 #pragma unroll
     for (int k = 0; k < G; ++k) {
@@ -1440,8 +1441,7 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
         for (int v = 0; v < 16; ++v) tab[(k * 16 + v) * kSliceThreads + threadIdx.x] = e[v];
     }
     const uint32_t tab_s = smem_u32(tab) + threadIdx.x * 4;
-    // per row (PZX_SORTED_ROWLOOP_G*): X = XOR_k T_k[nibble_k(psi)] ^ hx with
-    // p0 / p1 = parity(psi & H0 / H1): hx = p1 ? (p0 ? ~0 : M) : (p0 ? ~M : 0)
+    // per row (PZX_SORTED_ROWLOOP_G*): X = XOR_k T_k[nibble_k(psi)] ^ -parity(psi & H0)
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
     KindCounters<kSliceThreads> K;
@@ -1484,14 +1484,14 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
                                  : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
                                    "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
                                    "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
-                                 : "r"(aend), "r"(tab_s), "r"(H0), "r"(H1), "r"(M), "r"(~M)
+                                 : "r"(aend), "r"(tab_s), "r"(H0)
                                  : "memory");
                 } else {
                     asm volatile(PZX_SORTED_ROWLOOP_G4
                                  : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
                                    "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
                                    "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
-                                 : "r"(aend), "r"(tab_s), "r"(H0), "r"(H1), "r"(M), "r"(~M)
+                                 : "r"(aend), "r"(tab_s), "r"(H0)
                                  : "memory");
                 }
                 if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag | kEndFlag)) {
@@ -1512,13 +1512,6 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
     slice_store_results<kSliceThreads, TM>(r, off, acc);
 }
 
-__global__ void k_max_spread(const uint64_t* __restrict__ sorted, uint64_t n, unsigned long long* out) {
-    const uint64_t grp = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t i0 = grp * kSliceG;
-    if (i0 >= n) return;
-    const uint64_t i1 = i0 + kSliceG - 1 < n ? i0 + kSliceG - 1 : n - 1;
-    atomicMax(out, (unsigned long long)(sorted[i1] - sorted[i0]));
-}
 
 __global__ void k_mask_iota(const uint64_t* __restrict__ in, uint64_t n, uint64_t mask, uint64_t* keys,
                             uint32_t* vals) {
@@ -1536,6 +1529,7 @@ __global__ void k_reduce_partials(const double2* __restrict__ partial, int n_chu
     const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint64_t i = perm ? perm[k] : k;
+    if (i == 0xFFFFFFFFu) return;  // padding slot of the sorted kernel
     double2 s = make_double2(0.0, 0.0);
     for (int c = 0; c < n_chunks; ++c) {
         const double2 v = partial[uint64_t(c) * n + k];
@@ -1802,20 +1796,142 @@ size_t cub_sort_temp(uint64_t n) {
 }
 }  // namespace
 
-cudaError_t sorted_max_spread(const uint64_t* d_sorted, uint64_t n, void* d_tmp8, uint64_t* h_out,
-                              cudaStream_t s, uint64_t* launches) {
-    cudaError_t e = cudaMemsetAsync(d_tmp8, 0, 8, s);
-    if (e != cudaSuccess) return e;
-    const uint64_t groups = (n + kSliceG - 1) / kSliceG;
-    k_max_spread<<<int((groups + 255) / 256), 256, 0, s>>>(d_sorted, n, static_cast<unsigned long long*>(d_tmp8));
-    ++*launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(h_out, d_tmp8, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    return cudaStreamSynchronize(s);
+
+// ---- padded high-part groups for the sorted kernel ------------------------
+// The sorted words are regrouped so that the 32 words of every thread share
+// their high part (bits >= low): each run of equal high part is padded to a
+// multiple of 32 slots (padding repeats the run's last word, perm = ~0 so
+// nothing is stored for it). A thread then needs one high-part parity per
+// row instead of two.
+__global__ void k_run_flags(const uint64_t* __restrict__ k, uint64_t n, uint32_t low, uint32_t* flag) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flag[i] = (i == 0 || (k[i] >> low) != (k[i - 1] >> low)) ? 1u : 0u;
+}
+__global__ void k_run_starts(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rid, uint64_t n,
+                             uint32_t* start) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) start[rid[i] - 1] = uint32_t(i);
+}
+__global__ void k_run_pads(const uint32_t* __restrict__ start, const uint32_t* __restrict__ n_runs_p, uint64_t n,
+                           uint32_t* pad) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t R = *n_runs_p;
+    if (r >= R) return;
+    const uint64_t len = (r + 1 < R ? start[r + 1] : n) - start[r];
+    pad[r] = uint32_t((32 - len % 32) % 32);
+}
+__global__ void k_group_scatter(const uint64_t* __restrict__ k, const uint32_t* __restrict__ perm,
+                                const uint32_t* __restrict__ rid, const uint32_t* __restrict__ pad_before,
+                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ pad,
+                                const uint32_t* __restrict__ n_runs_p, uint64_t n, uint64_t* pw, uint32_t* pp) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = rid[i] - 1;
+    const uint64_t s = i + pad_before[r];
+    pw[s] = k[i];
+    pp[s] = perm[i];
+    const uint32_t R = *n_runs_p;
+    const uint64_t last = (r + 1 < R ? start[r + 1] : n) - 1;
+    if (i == last)  // the run's padding slots follow its last word
+        for (uint32_t q = 1; q <= pad[r]; ++q) {
+            pw[s + q] = k[i];
+            pp[s + q] = 0xFFFFFFFFu;
+        }
 }
 
-size_t sort_scratch_bytes(uint64_t n) {
+size_t cub_scan_temp(uint64_t n) {
+    size_t t = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, t, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  int64_t(n));
+    size_t t2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  int64_t(n));
+    return t > t2 ? t : t2;
+}
+
+size_t group_scratch_bytes(uint64_t n) {
+    return 5 * align256(n * 4) + align256(2 * n * 8 + 64 * 8) + align256(2 * n * 4 + 64 * 4) + align256(cub_scan_temp(n)) + 256;
+}
+
+size_t sort_base_bytes(uint64_t n) {
     return 2 * align256(n * 8) + 2 * align256(n * 4) + align256(cub_sort_temp(n));
+}
+
+size_t sort_scratch_bytes(uint64_t n) { return sort_base_bytes(n) + group_scratch_bytes(n); }
+
+cudaError_t group_sorted(const uint64_t* d_sorted, const uint32_t* d_perm, uint64_t n, uint32_t low, void* scratch,
+                         const uint64_t** d_pw, const uint32_t** d_pp, uint64_t* n_slots, cudaStream_t s,
+                         uint64_t* launches) {
+    unsigned char* p = static_cast<unsigned char*>(scratch);
+    auto take = [&](size_t b) { unsigned char* q = p; p += align256(b); return q; };
+    uint32_t* flag = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* rid = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* start = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* pad = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* padb = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint64_t* pw = reinterpret_cast<uint64_t*>(take(2 * n * 8 + 64 * 8));
+    uint32_t* pp = reinterpret_cast<uint32_t*>(take(2 * n * 4 + 64 * 4));
+    size_t temp = cub_scan_temp(n);
+    void* tmp = take(temp);
+    uint32_t* nr = reinterpret_cast<uint32_t*>(take(16));
+    const int b = 256, g = int((n + b - 1) / b);
+    cudaError_t e;
+    k_run_flags<<<g, b, 0, s>>>(d_sorted, n, low, flag);
+    if ((e = cub::DeviceScan::InclusiveSum(tmp, temp, flag, rid, int64_t(n), s)) != cudaSuccess) return e;
+    k_run_starts<<<g, b, 0, s>>>(flag, rid, n, start);
+    if ((e = cudaMemcpyAsync(nr, rid + (n - 1), 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+    k_run_pads<<<g, b, 0, s>>>(start, nr, n, pad);
+    uint32_t R = 0;
+    if ((e = cudaMemcpyAsync(&R, nr, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, temp, pad, padb, int64_t(R), s)) != cudaSuccess) return e;
+    uint32_t tail[2] = {0, 0};
+    if ((e = cudaMemcpyAsync(&tail[0], padb + (R - 1), 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&tail[1], pad + (R - 1), 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    *n_slots = n + uint64_t(tail[0]) + tail[1];
+    if (*n_slots > 2 * n + 64) return cudaErrorInvalidValue;  // caller checks the ratio first
+    k_group_scatter<<<g, b, 0, s>>>(d_sorted, d_perm, rid, padb, start, pad, nr, n, pw, pp);
+    *launches += 6;
+    *d_pw = pw;
+    *d_pp = pp;
+    return cudaGetLastError();
+}
+
+// number of padded slots for a given low-bit count, without building them
+cudaError_t group_slots(const uint64_t* d_sorted, uint64_t n, uint32_t low, void* scratch, uint64_t* n_slots,
+                        cudaStream_t s, uint64_t* launches) {
+    unsigned char* p = static_cast<unsigned char*>(scratch);
+    auto take = [&](size_t b) { unsigned char* q = p; p += align256(b); return q; };
+    uint32_t* flag = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* rid = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* start = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* pad = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* padb = reinterpret_cast<uint32_t*>(take(n * 4));
+    take(2 * n * 8 + 64 * 8);
+    take(2 * n * 4 + 64 * 4);
+    size_t temp = cub_scan_temp(n);
+    void* tmp = take(temp);
+    uint32_t* nr = reinterpret_cast<uint32_t*>(take(16));
+    const int b = 256, g = int((n + b - 1) / b);
+    cudaError_t e;
+    k_run_flags<<<g, b, 0, s>>>(d_sorted, n, low, flag);
+    if ((e = cub::DeviceScan::InclusiveSum(tmp, temp, flag, rid, int64_t(n), s)) != cudaSuccess) return e;
+    k_run_starts<<<g, b, 0, s>>>(flag, rid, n, start);
+    if ((e = cudaMemcpyAsync(nr, rid + (n - 1), 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+    k_run_pads<<<g, b, 0, s>>>(start, nr, n, pad);
+    uint32_t R = 0;
+    if ((e = cudaMemcpyAsync(&R, nr, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, temp, pad, padb, int64_t(R), s)) != cudaSuccess) return e;
+    uint32_t tail[2] = {0, 0};
+    if ((e = cudaMemcpyAsync(&tail[0], padb + (R - 1), 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&tail[1], pad + (R - 1), 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    *n_slots = n + uint64_t(tail[0]) + tail[1];
+    *launches += 4;
+    return cudaSuccess;
 }
 
 cudaError_t sort_words(const uint64_t* d_words, uint64_t n, uint32_t n_params, void* scratch,

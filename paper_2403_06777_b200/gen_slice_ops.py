@@ -304,12 +304,11 @@ def _loop_block(name, p64):
 # sorted-batch kernel's fused loop. Rows {psi, phi, code, op}, {psi offsets
 # 0|1, 2|3, phi offsets 0|1, 2|3} (16-bit byte offsets into the thread's
 # Four-Russians tables); X = XOR of G table words (groups 4.. computed from
-# the mask) ^ the high-part term: with p0 / p1 the parities of psi & H0 / H1,
-# hx = p1 ? (p0 ? ~0 : M) : (p0 ? ~M : 0). Y likewise, its loads predicated
-# off for one-parity rows (phi == 0 -> Y = 0).
+# the mask) ^ -parity(psi & H0): the host regroups the sorted words so that a
+# thread's 32 words share their high part H0. Y likewise, its loads
+# predicated off for one-parity rows (phi == 0 -> Y = 0).
 # operands: %0 ad, %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip, %8 code (out),
-#   %9-%16 row registers, %17 aend, %18 tab (this thread's table address),
-#   %19 H0, %20 H1, %21 M, %22 ~M
+#   %9-%16 row registers, %17 aend, %18 tab (this thread's table address), %19 H0
 def _sorted_par(out, mask, o01, o23, G, pred=None):
     pp = f"@{pred} " if pred else ""
     L = []
@@ -320,25 +319,15 @@ def _sorted_par(out, mask, o01, o23, G, pred=None):
     for k in range(4, G):
         L.append(f"shr.b32 ta, {mask}, {4 * k};")
         L.append("and.b32 ta, ta, 15;")
-        L.append(f"mad.lo.u32 ta, ta, 512, %18;")
+        L.append("mad.lo.u32 ta, ta, 512, %18;")
         L.append(f"{pp}ld.shared.u32 t{k}, [ta+{k * 16 * 512}];")
     L.append(f"and.b32 ta, {mask}, %19;")
     L.append("popc.b32 ta, ta;")
     L.append("and.b32 ta, ta, 1;")
-    L.append("setp.ne.b32 s0, ta, 0;")
-    L.append(f"and.b32 ta, {mask}, %20;")
-    L.append("popc.b32 ta, ta;")
-    L.append("and.b32 ta, ta, 1;")
-    L.append("setp.ne.b32 s1, ta, 0;")
-    L.append("selp.b32 tb, 0xFFFFFFFF, %21, s0;")
-    L.append("selp.b32 ta, %22, 0, s0;")
-    L.append("selp.b32 ta, tb, ta, s1;")
-    xs = " ".join(f"t{i}" for i in range(G))
-    L.append(f"xor.b32 ta, ta, t0;")
-    for i in range(1, G):
+    L.append("neg.s32 ta, ta;")
+    for i in range(G):
         L.append(f"xor.b32 ta, ta, t{i};")
     L.append(f"mov.b32 {out}, ta;" if not pred else f"selp.b32 {out}, ta, 0, {pred};")
-    _ = xs
     return L
 
 
@@ -351,8 +340,8 @@ def _sorted_loop_block(name, G):
             bodies[key] = len(bodies)
         label_of.append(bodies[key])
     regs = ", ".join(f"t{i}" for i in range(G))
-    b = ["{", f".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi, ta, tb, {regs};",
-         ".reg .pred pl, mo, cont, s0, s1, hp;",
+    b = ["{", f".reg .b32 c0, c1, w1, yy, xx, yv, tq, opi, ta, {regs};",
+         ".reg .pred pl, mo, cont, hp;",
          "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
          "H%=:"]
     b += _sorted_par("xx", "%9", "%13", "%14", G)
@@ -421,8 +410,7 @@ def generate() -> str:
               "//   %8 code (out), %9-%16 row registers, %17 aend, %18 blo, %19 bhi"]
     lines += _loop_block("PZX_SLICE_ROWLOOP_P32", False) + _loop_block("PZX_SLICE_ROWLOOP_P64", True)
     lines += ["// fused loop of the sorted-batch kernel (G = 4 / 6 table groups): %0 ad, %1-%4 J0 J1 J2 Z,",
-              "//   %5-%7 vl vpi vpip, %8 code, %9-%16 row registers, %17 aend, %18 table, %19 H0, %20 H1,",
-              "//   %21 M, %22 ~M"]
+              "//   %5-%7 vl vpi vpip, %8 code, %9-%16 row registers, %17 aend, %18 table, %19 H0"]
     lines += _sorted_loop_block("PZX_SORTED_ROWLOOP_G4", 4) + _sorted_loop_block("PZX_SORTED_ROWLOOP_G6", 6)
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")

@@ -191,7 +191,7 @@ def test_sorted_kernel_wide_tables(ctx, P_, n):
 def test_sorted_kernel_rejects_sparse_batches(ctx):
     e = synth.generate(32, 64, 1, 20, 9)
     t = ctx.compile_bit_table(e)
-    words = np.random.default_rng(3).integers(0, 2**32, 4096, dtype=np.uint64)  # gaps ~2^20
+    words = np.random.default_rng(3).integers(0, 2**32, 1024, dtype=np.uint64)  # ~4 words per 2^24 window
     with pytest.raises(P.Error):
         ctx.evaluate_batch(t, words, flags=P.KERNEL_SORTED)
     # auto falls back to the POPC kernel
