@@ -175,6 +175,23 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
                                uint32_t flags, void* stream);
+/* Several GPUs from one host thread. REPLICATE: the table
+ * on every device, a batch cut into contiguous per-device slices evaluated
+ * concurrently (no inter-GPU traffic). SPLIT_TERMS: row-balanced term ranges
+ * per device, the whole batch everywhere, partial amplitudes copied peer to
+ * peer to the first device and summed in device order (deterministic). */
+enum { PZX_REPLICATE = 0, PZX_SPLIT_TERMS = 1 };
+typedef struct pzx_group pzx_group;
+typedef struct pzx_group_table pzx_group_table;
+pzx_status pzx_group_create(const int* devices, int n_devices, pzx_group** out);
+void pzx_group_destroy(pzx_group* g);
+const char* pzx_group_last_error(const pzx_group* g);
+pzx_status pzx_group_upload_expr(pzx_group* g, const pzx_expr_view* expr, uint32_t mode, pzx_group_table** out);
+void pzx_group_table_free(pzx_group_table* t);
+/* assignments == NULL: the enumerated batch first .. first+n-1 */
+pzx_status pzx_group_evaluate(pzx_group* g, const pzx_group_table* t, const uint64_t* assignments, uint64_t first,
+                              uint64_t n, double* amp, double* prob, uint32_t flags);
+
 /* SPEC BackendContract: capability descriptor of this backend. */
 typedef struct {
     uint32_t max_params;          /* 64 */

@@ -20,6 +20,8 @@ EXPORTS = (
     "pzx_debug_phase_indices", "pzx_debug_term_codes", "pzx_table_compile_host", "pzx_class_table",
     "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample", "pzx_pzx1_encode", "pzx_pzx1_encode_expr",
     "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
+    "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
+    "pzx_group_evaluate",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -92,6 +94,15 @@ def lib() -> C.CDLL:
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     L.pzx_synchronize.argtypes = [vp]
     L.pzx_backend_contract_get.argtypes = [vp, C.POINTER(BackendContract)]
+    L.pzx_group_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+    L.pzx_group_destroy.argtypes = [vp]
+    L.pzx_group_destroy.restype = None
+    L.pzx_group_last_error.argtypes = [vp]
+    L.pzx_group_last_error.restype = C.c_char_p
+    L.pzx_group_upload_expr.argtypes = [vp, C.POINTER(ExprView), C.c_uint32, C.POINTER(vp)]
+    L.pzx_group_table_free.argtypes = [vp]
+    L.pzx_group_table_free.restype = None
+    L.pzx_group_evaluate.argtypes = [vp, vp, u64p, C.c_uint64, C.c_uint64, dblp, dblp, C.c_uint32]
     L.pzx_pzx1_encode.argtypes = [C.POINTER(TableView), u8p, C.c_uint64, u64p]
     L.pzx_pzx1_encode_expr.argtypes = [C.POINTER(ExprView), u8p, C.c_uint64, u64p]
     L.pzx_pzx1_info.argtypes = [u8p, C.c_uint64, C.POINTER(C.c_uint32), u64p, u64p]

@@ -140,6 +140,9 @@ cudaError_t launch_debug_phase(const DevTable& t, const uint64_t* d_asg, uint64_
                                uint8_t* d_out, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_sample_step(uint64_t* d_words, double* d_pprev, const double* d_p0, uint64_t n, uint32_t k,
                                uint64_t seed, unsigned int* d_err, cudaStream_t s, uint64_t* launches);
+// sum of n_parts partial amplitude arrays [part][n] in part order (deterministic), then prob
+cudaError_t launch_sum_partials(const double2* parts, int n_parts, uint64_t n, double2* amp, double* prob,
+                                int prob_mode, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_expand_words(const uint64_t* d_fixed, uint64_t n_fixed, uint32_t m, uint64_t* d_words,
                                 cudaStream_t s, uint64_t* launches);
 cudaError_t launch_segment_sum(const double* d_in, uint64_t len, uint64_t n_seg, double* d_out, int accumulate,

@@ -2034,6 +2034,14 @@ cudaError_t launch_sample_step(uint64_t* d_words, double* d_pprev, const double*
     return cudaGetLastError();
 }
 
+cudaError_t launch_sum_partials(const double2* parts, int n_parts, uint64_t n, double2* amp, double* prob,
+                                int prob_mode, cudaStream_t s, uint64_t* launches) {
+    if (n == 0) return cudaSuccess;
+    k_reduce_partials<<<int((n + 255) / 256), 256, 0, s>>>(parts, n_parts, n, amp, prob, prob_mode, 0, nullptr);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_expand_words(const uint64_t* d_fixed, uint64_t n_fixed, uint32_t m, uint64_t* d_words,
                                 cudaStream_t s, uint64_t* launches) {
     const uint64_t n = n_fixed << m;

@@ -516,6 +516,79 @@ def slice_op_table() -> np.ndarray:
     return out.reshape(129, 10)
 
 
+# ------------------------------------------------------------ multi-GPU ----
+REPLICATE, SPLIT_TERMS = 0, 1
+
+
+class Group:
+    """Several GPUs driven from this thread through the C ABI (pzx_group_*):
+    REPLICATE shards batches across devices, SPLIT_TERMS splits the table and
+    sums partial amplitudes on the first device (peer copies, device order)."""
+
+    def __init__(self, devices: Sequence[int]):
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(N.lib().pzx_group_create(arr, len(devices), C.byref(h)))
+        self.handle = h
+        self.devices = list(devices)
+
+    def _check(self, st: int) -> None:
+        if st:
+            lib = N.lib()
+            raise _STATUS.get(st, Error)(f"{lib.pzx_status_string(st).decode()}: "
+                                         f"{lib.pzx_group_last_error(self.handle).decode()}")
+
+    def upload(self, expr: ScalarExpression, mode: int = REPLICATE) -> "GroupTable":
+        v, keep = expr.view()
+        h = C.c_void_p()
+        self._check(N.lib().pzx_group_upload_expr(self.handle, C.byref(v), mode, C.byref(h)))
+        del keep
+        return GroupTable(h)
+
+    def evaluate_batch(self, table: "GroupTable", assignments, prob_real: bool = False) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        amp = np.empty(a.size, np.complex128)
+        if a.size:
+            self._check(N.lib().pzx_group_evaluate(self.handle, table.handle, N.ptr(a, C.c_uint64), 0, a.size,
+                                                   N.ptr(amp.view(np.float64), C.c_double), None,
+                                                   PROB_REAL if prob_real else PROB_ABS2))
+        return amp
+
+    def evaluate_range(self, table: "GroupTable", first: int, n: int) -> np.ndarray:
+        amp = np.empty(n, np.complex128)
+        if n:
+            self._check(N.lib().pzx_group_evaluate(self.handle, table.handle, None, first, n,
+                                                   N.ptr(amp.view(np.float64), C.c_double), None, PROB_ABS2))
+        return amp
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib().pzx_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GroupTable:
+    def __init__(self, handle):
+        self.handle = handle
+
+    def free(self) -> None:
+        if self.handle:
+            N.lib().pzx_group_table_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 # ---------------------------------------------------------------- PZX1 ----
 @dataclass
 class PhaseTable:
@@ -648,7 +721,7 @@ __all__ = [
     "Error", "ParseError", "DomainError", "Lemma1Violation", "OverflowError", "MissingParameter", "CudaError",
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
-    "PhaseTable", "encode_pzx1", "decode_pzx1", "pzx1_to_json", "pzx1_from_json",
+    "Group", "GroupTable", "REPLICATE", "SPLIT_TERMS", "PhaseTable", "encode_pzx1", "decode_pzx1", "pzx1_to_json", "pzx1_from_json",
     "PROB_ABS2", "PROB_REAL", "ACCUMULATE", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
 ]
 _ = builtins

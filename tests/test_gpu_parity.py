@@ -399,3 +399,19 @@ def test_backend_contract(ctx):
     c = ctx.backend_contract()
     assert c["max_params"] == 64 and c["deterministic"] == 1 and c["exact"] == 0
     assert c["max_rows_per_term"] == 127 and c["n_sm"] > 0 and c["preferred_batch"] > 0
+
+
+@pytest.mark.parametrize("mode", ["replicate", "split_terms"])
+def test_group_api_two_contexts(ctx, mode):
+    """pzx_group_* with two contexts on the one GPU of the box: the sharding /
+    term-split logic and the ordered partial sum, against one context."""
+    e = synth.generate(16, 900, 4, 40, 1500)
+    t = ctx.compile_bit_table(e)
+    g = P.Group([0, 0])
+    gt = g.upload(e, P.REPLICATE if mode == "replicate" else P.SPLIT_TERMS)
+    n = 1 << 14
+    assert_close(g.evaluate_range(gt, 0, n), ctx.evaluate_range(t, 0, n), 1e-13)
+    words = np.random.default_rng(5).integers(0, 1 << 16, 3001, dtype=np.uint64)
+    assert_close(g.evaluate_batch(gt, words), ctx.evaluate_batch(t, words), 1e-13)
+    gt.free()
+    g.close()
