@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         if (code & kSlicePiFlag) K.bump_a(vpi);
                         if (code & kSlicePipFlag) K.bump_b(vpip);
                         if (code & kEndFlag)
-                            slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                            slice_term_epilogue<NT, TM, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                     }
                 }
             } else {
@@ -1229,7 +1229,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
                     if (code & kEndFlag)
-                        slice_term_epilogue<NT, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                        slice_term_epilogue<NT, true, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }
             __syncwarp();  // the warp is done with buffer (i & 1)
