@@ -415,3 +415,30 @@ def test_group_api_two_contexts(ctx, mode):
     assert_close(g.evaluate_batch(gt, words), ctx.evaluate_batch(t, words), 1e-13)
     gt.free()
     g.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_kernels_against_oracle(ctx, seed):
+    """Random shapes through every kernel the library can pick: random P, term
+    lengths up to 120 rows, both row mixes; the forced and automatic choices
+    agree with each other and with the reference oracle on a sample."""
+    rng = np.random.default_rng(7000 + seed)
+    P_ = int(rng.choice([5, 9, 14, 20, 27, 32, 40, 64]))
+    mix = "general" if seed % 2 else "clifford"
+    e = synth.generate(P_, int(rng.integers(50, 400)), 0, int(rng.integers(8, 121)), 7100 + seed, mix)
+    t = ctx.compile_bit_table(e)
+    n = int(rng.integers(40, 5000))
+    first = 0 if P_ <= 12 else int(rng.integers(0, 1 << min(P_, 40)) // 64 * 64)
+    ref = ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL)
+    for fl in (0, P.KERNEL_GRAY, P.KERNEL_SLICE, P.KERNEL_SLICE2):
+        assert_close(ctx.evaluate_range(t, first, n, flags=fl), ref, 1e-13)
+    words = rng.integers(0, 2**64, n, dtype=np.uint64)
+    gen = ctx.evaluate_batch(t, words, flags=P.KERNEL_GENERAL)
+    assert_close(ctx.evaluate_batch(t, words), gen, 1e-13)            # auto (sorted where it applies)
+    assert_close(ctx.evaluate_batch(t, words, flags=P.KERNEL_SLICE_RAND), gen, 1e-13)
+    idx = rng.choice(n, 24, replace=False)
+    try:
+        _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+    except O.OracleError:  # the reference's int64 RingQuad overflows on long random terms (ring.cpp:61-63)
+        return
+    assert_close(gen[idx], want)
