@@ -345,8 +345,10 @@ def _sorted_loop_block(name, G):
          "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
          "H%=:"]
     b += _sorted_par("xx", "%9", "%13", "%14", G)
-    b += ["setp.ne.b32 hp, %10, 0;"]
-    b += _sorted_par("yv", "%10", "%15", "%16", G, pred="hp")
+    # one-parity rows (phi == 0, ~40 %) jump over the Y lookups (a uniform branch)
+    b += ["setp.eq.b32 hp, %10, 0;", "mov.b32 yv, 0;", "@hp bra.uni NY%=;"]
+    b += _sorted_par("yv", "%10", "%15", "%16", G)
+    b += ["NY%=:"]
     b += ["mov.b32 opi, %12;", "mov.b32 %8, %11;",
           f"and.b32 tq, %11, {ROW_FLAG_MASK:#x};", "setp.eq.b32 pl, tq, 0;",
           "add.u32 %0, %0, 32;", "setp.lt.u32 mo, %0, %17;", "and.pred cont, pl, mo;",
