@@ -698,8 +698,9 @@ __device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
 // then each assignment is 2 table loads + 4 DFMA into its accumulator, no
 // branches (Z-marked assignments read a zero entry).
 // KINDS: some lambda / pi / pi' rows (the (sqrt2-1)^s pi^a pi'^b table is
-// read); AB: some pi / pi' rows (else their planes are known zero and skipped)
-template <int NT, bool TM, bool KINDS, bool ROLL, bool AB = true>
+// read); AB: planes of the pi / pi' counters to decode (0: pi-free term, 1: a,
+// b < 2, 2: a, b < 4) -- known-zero planes are skipped
+template <int NT, bool TM, bool KINDS, bool ROLL, int AB = 2>
 __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
                                                     uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
                                                     const KindCounters<NT>& K) {
@@ -710,13 +711,17 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
     Nib s0{}, s1{}, s2{}, s3{}, a0{}, a1{}, b0{}, b1{};
     if constexpr (KINDS) {
         s0 = nib_split(S[0]); s1 = nib_split(S[1]); s2 = nib_split(S[2]); s3 = nib_split(S[3]);
-        if constexpr (AB) {
-            a0 = nib_split(A[0]); a1 = nib_split(A[1]);
-            b0 = nib_split(B[0]); b1 = nib_split(B[1]);
+        if constexpr (AB >= 1) {
+            a0 = nib_split(A[0]);
+            b0 = nib_split(B[0]);
+        }
+        if constexpr (AB >= 2) {
+            a1 = nib_split(A[1]);
+            b1 = nib_split(B[1]);
         }
     }
     auto mac = [&](double2& o, const double2 c, const double2 f) {
-        if constexpr (KINDS && AB) {
+        if constexpr (KINDS && AB > 0) {
             o.x = fma(c.x, f.x, o.x);
             o.y = fma(c.x, f.y, o.y);
             o.x = fma(-c.y, f.y, o.x);
@@ -735,13 +740,13 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
         uint32_t ks = 0;  // s | a << 4 | b << 6
         if constexpr (KINDS) {
             ks = nib_spread(s0, m, 0) | nib_spread(s1, m, 1) | nib_spread(s2, m, 2) | nib_spread(s3, m, 3);
-            if constexpr (AB)
-                ks |= nib_spread(a0, m, 4) | nib_spread(a1, m, 5) | nib_spread(b0, m, 6) | nib_spread(b1, m, 7);
+            if constexpr (AB >= 1) ks |= nib_spread(a0, m, 4) | nib_spread(b0, m, 6);
+            if constexpr (AB >= 2) ks |= nib_spread(a1, m, 5) | nib_spread(b1, m, 7);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             c[r] = crot[__byte_perm(kj, 0u, 0x4440u | uint32_t(r))];
-            if constexpr (KINDS && AB) {
+            if constexpr (KINDS && AB > 0) {
                 f[r] = L.sab[__byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
             } else if constexpr (KINDS) {
                 f[r].x = reinterpret_cast<const double*>(L.sab)[2 * __byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
@@ -753,7 +758,7 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
         // 8 groups of 4 assignments = 16 TMEM columns each; the load of group
         // m + 1 is in flight while group m is computed (wait::ld waits for all)
         // (ROLL: a rolled loop over pairs of groups keeps the epilogue's code
-        // small -- pays off in the sorted kernel, not in the slice kernel)
+        // small -- the row loop and its jump targets stay in the I-cache)
         tmem_wait_st();  // the previous term's stores have landed
         auto pair = [&](int m2) {
 #pragma unroll
@@ -855,8 +860,9 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
     if (!kinds) {
         slice_epilogue_fast<NT, TM, false, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
     } else if (K.fits_fast()) {
-        if (K.has_pi()) slice_epilogue_fast<NT, TM, true, ROLL, true>(L, crot, acc, J0, J1, J2, Z, K);
-        else slice_epilogue_fast<NT, TM, true, ROLL, false>(L, crot, acc, J0, J1, J2, Z, K);
+        if (!K.has_pi()) slice_epilogue_fast<NT, TM, true, ROLL, 0>(L, crot, acc, J0, J1, J2, Z, K);
+        else if (K.nA < 2 && K.nB < 2) slice_epilogue_fast<NT, TM, true, ROLL, 1>(L, crot, acc, J0, J1, J2, Z, K);
+        else slice_epilogue_fast<NT, TM, true, ROLL, 2>(L, crot, acc, J0, J1, J2, Z, K);
     } else if constexpr (TM) {
         tmem_wait_st();
 #pragma unroll 1
