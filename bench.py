@@ -386,6 +386,14 @@ def run_ours(args):
     work = N * (w_row * R + 16 * m)                    # algorithmic int ops per launch
     f_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tops = N_SM * INT_LANES_PER_SM * f_mhz * 1e6 / 1e12
+    mb_path = os.path.join(ROOT, "profiles", "r01", "microbench.json")
+    mb_lop3 = None
+    try:  # the int32 LOP3 rate measured on this pool's B200s (pzx_microbench)
+        with open(mb_path) as f:
+            mb_lop3 = json.load(f)["per_sm_per_clk"]["lop3_int32"]
+        peak_tops = N_SM * mb_lop3 * f_mhz * 1e6 / 1e12
+    except Exception:
+        pass
     achieved = work / (mean_ms / 1e3) / 1e12
     row_evals = N * R / (mean_ms / 1e3)
     table_bytes = R * 16 + m * 24
@@ -441,8 +449,11 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
                          "frac": achieved / peak_tops, "traffic": traffic,
-                         "peak_source": f"148 SM x 64 int32 lanes/clk x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
-                                        "MEASURED_PEAKS.json clock; lane rate from the CUDA throughput table)",
+                         "peak_source": (f"148 SM x {mb_lop3:.1f} int32 LOP3/clk/SM measured on this pool "
+                                         f"(profiles/r01/microbench.json) x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
+                                         "MEASURED_PEAKS.json clock)" if mb_lop3 else
+                                         f"148 SM x 64 int32 lanes/clk x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
+                                         "MEASURED_PEAKS.json clock; lane rate from the CUDA throughput table)"),
                          "work_per_launch": work, "row_evals_per_s": row_evals,
                          "hbm_gbs_if_table_streamed_once": table_bytes / (mean_ms / 1e3) / 1e9,
                          "ncu": None if ncu_info is None else {

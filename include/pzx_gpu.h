@@ -192,6 +192,10 @@ void pzx_group_table_free(pzx_group_table* t);
 pzx_status pzx_group_evaluate(pzx_group* g, const pzx_group_table* t, const uint64_t* assignments, uint64_t first,
                               uint64_t n, double* amp, double* prob, uint32_t flags);
 
+/* Pipe-rate microbenchmark behind the roofline denominators:
+ * which = 0 int32 LOP3, 1 POPC, 2 fp64 FMA, 3 LDS.32; thread-instructions/s. */
+pzx_status pzx_microbench(int device, int which, double* ops_per_s);
+
 /* SPEC BackendContract: capability descriptor of this backend. */
 typedef struct {
     uint32_t max_params;          /* 64 */

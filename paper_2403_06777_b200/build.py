@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libpzx_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["pzx_kernels.cu"]
+SOURCES_CU = ["pzx_kernels.cu", "pzx_microbench.cu"]
 SOURCES_CPP = ["pzx_host.cpp", "pzx_group.cpp"]
 HEADERS = ["pzx_internal.h", "pzx_math.hpp", "pzx_classes.h", "pzx_slice_dispatch.inc"]
 
