@@ -905,14 +905,6 @@ __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* sr
     slice_epilogue_apply<NT, TM, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
 }
 
-// odd(p) ? a : b as one predicate-setting LOP3 + SEL
-__device__ __forceinline__ uint32_t sel_parity(uint32_t p, uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("{\n .reg .pred q;\n .reg .b32 t;\n and.b32 t, %1, 1;\n setp.ne.b32 q, t, 0;\n selp.b32 %0, %2, %3, q;\n}"
-        : "=r"(r)
-        : "r"(p), "r"(a), "r"(b));
-    return r;
-}
 
 // Random batches: the thread's 32 words are transposed into bit planes
 // (plane i, bit g = bit i of word g) kept in shared memory [i][thread].
@@ -1401,11 +1393,6 @@ size_t sorted_smem_bytes(const DevTable& t) {
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 
 template <bool TM = false, int G = kSortedGroups>
 __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eval_sorted(const DevTable t,
