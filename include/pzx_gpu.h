@@ -175,6 +175,16 @@ pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t*
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
                                uint32_t flags, void* stream);
+/* Upload with compile options. PZX_COMPILE_SIMPLIFY: post-reduction table
+ * simplification (PAPER "Conclusions") -- rows of a term with
+ * identical masks whose product is assignment-independent are folded into the
+ * term constant (pairwise node cancellation; a zero product drops the term's
+ * rows and zeroes it). Values are unchanged; row order / counts then differ
+ * from the plain normalisation (the debug hooks index the compiled rows). */
+enum { PZX_COMPILE_SIMPLIFY = 1u << 0 };
+pzx_status pzx_table_upload_expr_ex(pzx_ctx* ctx, const pzx_expr_view* expr, uint32_t compile_flags,
+                                    pzx_table** out);
+
 /* Several GPUs from one host thread. REPLICATE: the table
  * on every device, a batch cut into contiguous per-device slices evaluated
  * concurrently (no inter-GPU traffic). SPLIT_TERMS: row-balanced term ranges

@@ -21,7 +21,7 @@ EXPORTS = (
     "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample", "pzx_pzx1_encode", "pzx_pzx1_encode_expr",
     "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
     "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
-    "pzx_group_evaluate", "pzx_microbench",
+    "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     L.pzx_synchronize.argtypes = [vp]
     L.pzx_backend_contract_get.argtypes = [vp, C.POINTER(BackendContract)]
+    L.pzx_table_upload_expr_ex.argtypes = [vp, C.POINTER(ExprView), C.c_uint32, C.POINTER(vp)]
     L.pzx_microbench.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     L.pzx_group_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
     L.pzx_group_destroy.argtypes = [vp]

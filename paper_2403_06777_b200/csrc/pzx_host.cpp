@@ -162,6 +162,7 @@ struct HostTable {
     int jb_term = 0;                        // running sum of slice jbase in the open term
     bool want_srows = true;                 // build the bit-sliced layout (enumerated batches)
     bool want_qrows = true;                 // build the sorted-batch layout (word lists, n_params <= 32)
+    bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
     uint32_t max_rows = 0;
@@ -311,10 +312,87 @@ bool canon_input(const int64_t* q, Quad& out) {
     return quad_canon(q[0], q[1], q[2], q[3], q[4], out);
 }
 
+// Post-reduction table simplification (PAPER "Conclusions": pairwise node
+// cancellation). Rows of one term that share their (psi, phi)
+// masks see the same parities, so a set of them whose product takes the same
+// value at every reachable (p, q) is a constant: it is folded into C_t
+// exactly, and a zero constant zeroes the whole term. The paper's example
+// (1 + w^(k + 4x))(1 + w^(k + 4 + 4x)) = 1 - w^(2k) is the two-row case; k = 0
+// with k = 4 gives 0. Greedy: the whole group first, then pairs.
+void simplify_term(std::vector<PairRow>& rows, Quad& c, bool& zero_term) {
+    zero_term = false;
+    if (rows.size() < 2) return;
+    auto canon = [](PairRow r) {  // lone parity in psi (V(x,y) = V(y,x))
+        if (r.psi == 0 && r.phi != 0) { std::swap(r.ka, r.kb); std::swap(r.psi, r.phi); }
+        return r;
+    };
+    for (auto& r : rows) r = canon(r);
+    // value of a row set at (p, q); false on int64 growth (large groups are left alone)
+    auto product = [&](const std::vector<size_t>& idx, int p, int q, Zw& out) {
+        Zw v = zw(1, 0, 0, 0);
+        for (size_t i : idx) {
+            v = zw_mul(v, zw_pair_value(rows[i].ka + 4 * p, rows[i].kb + 4 * q));
+            for (int k = 0; k < 4; ++k)
+                if (v.c[k] > (int64_t(1) << 40) || v.c[k] < -(int64_t(1) << 40)) return false;
+        }
+        out = v;
+        return true;
+    };
+    auto constant_of = [&](const std::vector<size_t>& idx, Zw& k) {
+        const PairRow& r = rows[idx[0]];
+        const int np = r.psi ? 2 : 1, nq = r.phi ? 2 : 1;
+        if (!product(idx, 0, 0, k)) return false;
+        for (int p = 0; p < np; ++p)
+            for (int q = 0; q < nq; ++q) {
+                Zw v;
+                if (!product(idx, p, q, v) || !(v == k)) return false;
+            }
+        return true;
+    };
+    std::vector<char> gone(rows.size(), 0);
+    auto fold = [&](const std::vector<size_t>& idx, const Zw& k) {
+        if (k.zero()) { zero_term = true; return; }
+        Quad kq, nc;
+        if (!zw_to_quad(k, kq) || !quad_mul(c, kq, nc)) return;  // leave it unfolded on overflow
+        c = nc;
+        for (size_t i : idx) gone[i] = 1;
+    };
+    std::vector<size_t> order(rows.size());
+    for (size_t i = 0; i < rows.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        return rows[a].psi != rows[b].psi ? rows[a].psi < rows[b].psi : rows[a].phi < rows[b].phi;
+    });
+    for (size_t s = 0; s < order.size() && !zero_term;) {
+        size_t e = s + 1;
+        while (e < order.size() && rows[order[e]].psi == rows[order[s]].psi && rows[order[e]].phi == rows[order[s]].phi) ++e;
+        if (e - s >= 2 && e - s <= 24) {
+            std::vector<size_t> grp(order.begin() + long(s), order.begin() + long(e));
+            Zw k;
+            if (constant_of(grp, k)) {
+                fold(grp, k);
+            } else {
+                for (size_t a = 0; a < grp.size() && !zero_term; ++a)
+                    for (size_t b = a + 1; b < grp.size() && !gone[grp[a]]; ++b) {
+                        if (gone[grp[b]]) continue;
+                        const std::vector<size_t> pr{grp[a], grp[b]};
+                        if (constant_of(pr, k)) fold(pr, k);
+                    }
+            }
+        }
+        s = e;
+    }
+    if (zero_term) { rows.clear(); c = Quad{}; return; }
+    std::vector<PairRow> kept;
+    for (size_t i = 0; i < rows.size(); ++i)
+        if (!gone[i]) kept.push_back(rows[i]);
+    rows.swap(kept);
+}
+
 int compile_expr_range(const pzx_expr_view* v, uint64_t t_begin, uint64_t t_end, HostTable& h,
                        std::string& err) {
     h.n_params = v->n_params;
     const uint64_t allowed = param_mask(v->n_params);
+    std::vector<PairRow> pend;
     for (uint64_t t = t_begin; t < t_end; ++t) {
         Quad c;
         if (!canon_input(v->term_scalar + 5 * t, c)) { err = "term scalar out of range"; return PZX_E_OVERFLOW; }
@@ -336,7 +414,16 @@ int compile_expr_range(const pzx_expr_view* v, uint64_t t_begin, uint64_t t_end,
             Quad nc;
             if (!quad_mul(c, k, nc)) { err = "term constant overflow"; return PZX_E_OVERFLOW; }
             c = nc;
-            if (has) push_row(h, pr, e, lm);
+            if (has) {
+                if (h.simplify) pend.push_back(pr);
+                else push_row(h, pr, e, lm);
+            }
+        }
+        if (h.simplify) {
+            bool zero_term = false;
+            simplify_term(pend, c, zero_term);
+            for (const PairRow& pr : pend) push_row(h, pr, e, lm);
+            pend.clear();
         }
         int st = finish_term(h, c, e, lm, row0);
         if (st) { err = "term has more rows than supported"; return st; }
@@ -384,6 +471,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
         parts[i].n_params = h.n_params;
         parts[i].want_srows = h.want_srows;
         parts[i].want_qrows = h.want_qrows;
+        parts[i].simplify = h.simplify;
         th.emplace_back([&, i] {
             st[i] = compile_expr_range(v, m * i / nth, m * (i + 1) / nth, parts[i], errs[i]);
         });
@@ -750,10 +838,16 @@ const char* pzx_last_error(const pzx_ctx* ctx) { return ctx ? ctx->err.c_str() :
 uint64_t pzx_launch_count(const pzx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 pzx_status pzx_table_upload_expr(pzx_ctx* ctx, const pzx_expr_view* expr, pzx_table** out) {
+    return pzx_table_upload_expr_ex(ctx, expr, 0, out);
+}
+
+pzx_status pzx_table_upload_expr_ex(pzx_ctx* ctx, const pzx_expr_view* expr, uint32_t compile_flags,
+                                    pzx_table** out) {
     if (!ctx || !expr || !out || (expr->n_terms && (!expr->term_offset || !expr->term_scalar)))
         return PZX_E_INVALID;
     std::unique_ptr<pzx_table> t(new (std::nothrow) pzx_table);
     if (!t) return PZX_E_OOM;
+    t->host.simplify = (compile_flags & PZX_COMPILE_SIMPLIFY) != 0;
     std::string err;
     int st = compile_expr(expr, t->host, err);
     if (st) return set_err(ctx, st, err);

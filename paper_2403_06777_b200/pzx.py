@@ -364,10 +364,13 @@ class Context:
         return int(N.lib().pzx_launch_count(self.handle))
 
     # -- compile + upload ---------------------------------------------------
-    def compile_bit_table(self, expr: ScalarExpression) -> DeviceTable:
+    def compile_bit_table(self, expr: ScalarExpression, simplify: bool = False) -> DeviceTable:
+        """SPEC compile_bit_table; simplify=True folds assignment-independent row
+        groups (pairwise node cancellation, PZX_COMPILE_SIMPLIFY)."""
         v, keep = expr.view()
         h = C.c_void_p()
-        _check(N.lib().pzx_table_upload_expr(self.handle, C.byref(v), C.byref(h)), self.handle)
+        _check(N.lib().pzx_table_upload_expr_ex(self.handle, C.byref(v), 1 if simplify else 0, C.byref(h)),
+               self.handle)
         del keep
         return DeviceTable(self, h)
 

@@ -442,3 +442,34 @@ def test_fuzz_kernels_against_oracle(ctx, seed):
     except O.OracleError:  # the reference's int64 RingQuad overflows on long random terms (ring.cpp:61-63)
         return
     assert_close(gen[idx], want)
+
+
+def test_simplify_pairwise_node_cancellation(ctx):
+    """PZX_COMPILE_SIMPLIFY (PAPER "Conclusions"): Node rows on one mask whose
+    constants differ by pi fold into the term constant, 0/pi pairs zero the
+    term; values equal the unsimplified table and the oracle."""
+    R = P.RingQuad
+    nd = lambda k, m: P.Subterm.node(P.ParamPhase(k, m))  # noqa: E731
+    pp = lambda a, m1, b, m2: P.Subterm.phase_pair(P.ParamPhase(a, m1), P.ParamPhase(b, m2))  # noqa: E731
+    terms = [
+        (R.make(1, 0, 0, 0, 1), [nd(2, 0b011), nd(6, 0b011), pp(1, 0b100, 3, 0b010)]),     # (1+i)(1-i) = 2 folds
+        (R.make(3, 1, 0, 0, 2), [nd(0, 0b101), nd(4, 0b101), pp(1, 0b001, 1, 0b010)]),     # 0 / pi pair: zero term
+        (R.make(1, 0, 1, 0, 1), [nd(1, 0b110), nd(5, 0b110), nd(3, 0b110), nd(7, 0b110)]),  # two pairs
+        (R.make(-2, 0, 0, 1, 0), [pp(1, 0b111, 2, 0b001), nd(1, 0b010)]),                  # nothing to fold
+    ]
+    e = P.ScalarExpression.from_terms(3, terms)
+    plain = ctx.compile_bit_table(e)
+    simp = ctx.compile_bit_table(e, simplify=True)
+    assert simp.n_rows < plain.n_rows
+    words = np.arange(8, dtype=np.uint64)
+    _, want = O.eval_batch(e, words, 4)
+    assert_close(ctx.evaluate_batch(simp, words), want)
+    assert_close(ctx.evaluate_batch(plain, words), want)
+    # random tables over few parameters (many shared masks): identical values on every kernel
+    for seed in range(3):
+        e2 = synth.generate(4, 600, 2, 30, 4400 + seed)
+        t1, t2 = ctx.compile_bit_table(e2), ctx.compile_bit_table(e2, simplify=True)
+        assert t2.n_rows <= t1.n_rows
+        a1 = ctx.evaluate_range(t1, 0, 16, flags=P.KERNEL_GENERAL)
+        for fl in (0, P.KERNEL_GENERAL, P.KERNEL_SLICE):
+            assert_close(ctx.evaluate_range(t2, 0, 16, flags=fl), a1, 1e-12)
