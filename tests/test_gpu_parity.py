@@ -473,3 +473,21 @@ def test_simplify_pairwise_node_cancellation(ctx):
         a1 = ctx.evaluate_range(t1, 0, 16, flags=P.KERNEL_GENERAL)
         for fl in (0, P.KERNEL_GENERAL, P.KERNEL_SLICE):
             assert_close(ctx.evaluate_range(t2, 0, 16, flags=fl), a1, 1e-12)
+
+
+@pytest.mark.parametrize("P_", [33, 64])
+def test_wide_params_tmem_slice_path(ctx, P_):
+    """P > 32 through the 128-thread TMEM bit-sliced kernel (batches >= 16K)
+    and the warp-chunk kernel (small batches), against the POPC kernel and the
+    oracle; bits above the parameter count are ignored."""
+    e = synth.generate(P_, 300, 1, 40, 5200 + P_)
+    t = ctx.compile_bit_table(e)
+    first = (1 << (P_ - 2)) + 64 * 977
+    n = 1 << 15
+    amp = ctx.evaluate_range(t, first, n)
+    assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
+    small = ctx.evaluate_range(t, first, 2048)
+    assert_close(small, amp[:2048], 1e-13)
+    idx = np.random.default_rng(P_).choice(n, 24, replace=False)
+    _, want = O.eval_batch(e, (np.uint64(first) + idx.astype(np.uint64)), 8, impl="ref" if O.have_ref() else "port")
+    assert_close(amp[idx], want)
