@@ -754,6 +754,13 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;
         c = std::min<uint64_t>(c, kc == KC_SLICEWC ? std::max<uint64_t>(1, nterms / kWarpChunksHost) : nterms);
         c = std::min<uint64_t>(c, std::max<uint64_t>(1, (uint64_t(1) << 30) / (r.n * 16 + 1)));
+        // small tables: a chunk below ~512 rows costs more in per-CTA setup
+        // (table staging, TMEM allocation, the partial it writes) than it saves
+        const uint64_t total_rows = t->host.term_row.size() > r.term_end
+                                        ? t->host.term_row[r.term_end] - t->host.term_row[r.term_begin]
+                                        : t->dev.n_rows;
+        const uint64_t per = kc == KC_SLICEWC ? uint64_t(kWarpChunksHost) * 512 : 512;
+        c = std::min<uint64_t>(c, std::max<uint64_t>(1, total_rows / per));
         chunks = int(std::min<uint64_t>(c, 65535));
         // round the grid up to whole waves when that does not need more chunks than terms
         const uint64_t total = uint64_t(chunks) * ablocks;
