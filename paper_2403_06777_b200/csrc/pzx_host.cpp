@@ -688,6 +688,14 @@ void chunk_bounds(const HostTable& h, uint64_t tb, uint64_t te, int chunks, std:
     }
 }
 
+uint64_t min_chunk_rows() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("PZX_MIN_CHUNK_ROWS");
+        return e ? std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) : uint64_t(512);
+    }();
+    return v;
+}
+
 pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t flags) {
     if (!ctx || !t) return PZX_E_INVALID;
     if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table (pzx_table_compile_host)");
@@ -754,12 +762,12 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;
         c = std::min<uint64_t>(c, kc == KC_SLICEWC ? std::max<uint64_t>(1, nterms / kWarpChunksHost) : nterms);
         c = std::min<uint64_t>(c, std::max<uint64_t>(1, (uint64_t(1) << 30) / (r.n * 16 + 1)));
-        // small tables: a chunk below ~512 rows costs more in per-CTA setup
+        // small tables: a chunk below kMinChunkRows rows costs more in per-CTA setup
         // (table staging, TMEM allocation, the partial it writes) than it saves
         const uint64_t total_rows = t->host.term_row.size() > r.term_end
                                         ? t->host.term_row[r.term_end] - t->host.term_row[r.term_begin]
                                         : t->dev.n_rows;
-        const uint64_t per = kc == KC_SLICEWC ? uint64_t(kWarpChunksHost) * 512 : 512;
+        const uint64_t per = (kc == KC_SLICEWC ? uint64_t(kWarpChunksHost) : uint64_t(1)) * min_chunk_rows();
         c = std::min<uint64_t>(c, std::max<uint64_t>(1, total_rows / per));
         chunks = int(std::min<uint64_t>(c, 65535));
         // round the grid up to whole waves when that does not need more chunks than terms
