@@ -242,8 +242,8 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
             h.srows.push_back(make_uint4(walsh32(phi), uint32_t(psi >> 32), uint32_t(phi >> 32), op));
     }
     if (h.want_qrows) {
-        auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m)
-            return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * kSortedTableStride);
+        auto offs = [](uint64_t m, uint32_t k) {  // byte offset of table row (k, nibble k of m), 128-thread stride
+            return uint32_t((k * 16 + ((m >> (4 * k)) & 15)) * 512u);
         };
         h.qrows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, op));
         h.qrows.push_back(make_uint4(offs(psi, 0) | (offs(psi, 1) << 16), offs(psi, 2) | (offs(psi, 3) << 16),

@@ -71,9 +71,9 @@ struct DevTable {
     int slice_ok = 0;
     // sorted-batch bit-sliced kernel (arbitrary word lists, n_params <= 32):
     // rows as 2 x uint4 {psi, phi, op | flags, op}, {psi offsets 0|1, psi offsets 2|3,
-    // phi offsets 0|1, phi offsets 2|3}; offset k = (k * 16 + nibble_k(mask)) *
-    // kSortedTableStride (16-bit byte offsets into the per-thread Four-Russians
-    // tables of the low 16 parameter bits)
+    // phi offsets 0|1, phi offsets 2|3}; offset k = (k * 16 + nibble_k(mask)) * 512,
+    // 16-bit byte offsets into the per-thread Four-Russians tables ([row][thread])
+    // of a 128-thread CTA (256-thread CTAs double them)
     const uint4* qrows = nullptr;
     int sorted_ok = 0;
 };
@@ -81,7 +81,6 @@ struct DevTable {
 constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables (dense batches)
 constexpr int kSortedGroupsWide = 6;          // parameters 0..23 via tables (sparse batches, e.g. 2^16 of 2^32)
 constexpr int kSortedLowBits = 4 * kSortedGroups;
-constexpr uint32_t kSortedTableStride = 128 * 4;  // bytes between table rows (128 threads x 4 B)
 
 enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5, KC_SLICE2 = 6,
                     KC_SLICEWC = 7 /* small enumerated batches: 4 warps x 4 term chunks per CTA (auto only) */ };
@@ -127,6 +126,7 @@ int grid_assign_blocks(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r);
 bool tmem_accumulators();
 int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_groups = kSortedGroups);
+int sorted_threads(int sorted_groups);  // CTA width of the sorted kernel (256 for the wide tables with TMEM)
 int slice_threads(const LaunchReq& r);
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc);
 

@@ -459,15 +459,16 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 constexpr int kLoS = 4, kLoAB = 2;
 constexpr int kHiPlanes = (kPlanes - kLoS) + 2 * (kPlanes - kLoAB);  // 14 shared planes per thread
 
-template <int NT>
+template <int NT, bool LOCAL = false>
 struct KindCounters {
+    static constexpr uint32_t stride = LOCAL ? 1u : uint32_t(NT);  // planes [kHiPlanes][stride]
     uint32_t S[kLoS], A[kLoAB], B[kLoAB];
     uint32_t nS, nA, nB;
-    uint32_t* hi;  // this thread's column of the [kHiPlanes][NT] shared planes
+    uint32_t* hi;  // this thread's column of the shared planes, or its local array (LOCAL)
 
-    __device__ __forceinline__ uint32_t* hs(int i) { return hi + (i - kLoS) * NT; }
-    __device__ __forceinline__ uint32_t* ha(int i) { return hi + (kPlanes - kLoS + i - kLoAB) * NT; }
-    __device__ __forceinline__ uint32_t* hb(int i) { return hi + (2 * kPlanes - kLoS - kLoAB + i - kLoAB) * NT; }
+    __device__ __forceinline__ uint32_t* hs(int i) { return hi + (i - kLoS) * stride; }
+    __device__ __forceinline__ uint32_t* ha(int i) { return hi + (kPlanes - kLoS + i - kLoAB) * stride; }
+    __device__ __forceinline__ uint32_t* hb(int i) { return hi + (2 * kPlanes - kLoS - kLoAB + i - kLoAB) * stride; }
 
     __device__ __forceinline__ void init(uint32_t* h) {
         hi = h;
@@ -477,7 +478,7 @@ struct KindCounters {
         for (int i = 0; i < kLoAB; ++i) A[i] = B[i] = 0;
         nS = nA = nB = 0;
 #pragma unroll
-        for (int i = 0; i < kHiPlanes; ++i) hi[i * NT] = 0;
+        for (int i = 0; i < kHiPlanes; ++i) hi[i * stride] = 0;
     }
     // counter += v; n = rows that could have bumped it so far (warp-uniform),
     // so only planes below bit_length(n) move
@@ -585,7 +586,9 @@ __device__ __forceinline__ void tmem_sync_fence() {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// warp 0 allocates COLS columns; returns this thread's lane-quarter address
+// warp 0 allocates COLS columns; returns this thread's address: its warp's lane
+// quarter, and for CTAs of more than 4 warps the 128-column block of its warp
+// group (warps 4..7 use columns 128..255)
 template <uint32_t COLS = kTmemCols>
 __device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* base_s) {
     if ((threadIdx.x >> 5) == 0) {
@@ -595,7 +598,7 @@ __device__ __forceinline__ uint32_t tmem_alloc_cta(uint32_t* base_s) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     tmem_sync_fence();
-    return *base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16);
+    return *base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16) + (threadIdx.x >> 7) * kTmemCols;
 }
 __device__ __forceinline__ uint32_t tmem_base_of(uint32_t taddr) { return taddr & 0x0000FFFFu; }
 template <uint32_t COLS = kTmemCols>
@@ -700,10 +703,10 @@ __device__ __forceinline__ uint32_t nib_spread(const Nib& q, int m, int k) {
 // KINDS: some lambda / pi / pi' rows (the (sqrt2-1)^s pi^a pi'^b table is
 // read); AB: planes of the pi / pi' counters to decode (0: pi-free term, 1: a,
 // b < 2, 2: a, b < 4) -- known-zero planes are skipped
-template <int NT, bool TM, bool KINDS, bool ROLL, int AB = 2>
+template <int NT, bool TM, bool KINDS, bool ROLL, int AB = 2, bool LC = false>
 __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
                                                     uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
-                                                    const KindCounters<NT>& K) {
+                                                    const KindCounters<NT, LC>& K) {
     const uint32_t(&S)[kLoS] = K.S;
     const uint32_t(&A)[kLoAB] = K.A;
     const uint32_t(&B)[kLoAB] = K.B;
@@ -804,9 +807,9 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
 }
 
 // Any counter widths: one assignment's term value (0 when Z-marked).
-template <int NT>
+template <int NT, bool LC = false>
 __device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const double2* crot, uint32_t J0, uint32_t J1,
-                                                    uint32_t J2, uint32_t Z, KindCounters<NT>& K, int g) {
+                                                    uint32_t J2, uint32_t Z, KindCounters<NT, LC>& K, int g) {
     if ((Z >> g) & 1u) return make_double2(0.0, 0.0);
     const uint32_t j = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
     double2 v = crot[j];
@@ -846,10 +849,10 @@ __device__ __forceinline__ void slice_epilogue_begin(TermC& tc, const double2* s
 
 // Term epilogue, part 2 (per 32-assignment slice): fold 6*s1 into J, add
 // every live assignment's term value into its accumulator, reset the state.
-template <int NT, bool TM, bool ROLL = false>
+template <int NT, bool TM, bool ROLL = false, bool LC = false>
 __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const double2* crot, SliceAcc<NT, TM>& acc,
                                                      uint32_t& J0, uint32_t& J1, uint32_t& J2, uint32_t& Z,
-                                                     KindCounters<NT>& K) {
+                                                     KindCounters<NT, LC>& K) {
     if (K.nS) {  // (lambda/mu)^s1 = mu^.. * w^(6 s1) * (sqrt2-1)^s1: add 6*s1 mod 8 to J
         const uint32_t w1 = K.S[0], w2 = K.S[0] ^ K.S[1];
         const uint32_t c1 = J1 & w1;
@@ -858,11 +861,11 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
     }
     const bool kinds = K.any();
     if (!kinds) {
-        slice_epilogue_fast<NT, TM, false, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
+        slice_epilogue_fast<NT, TM, false, ROLL, 2, LC>(L, crot, acc, J0, J1, J2, Z, K);
     } else if (K.fits_fast()) {
-        if (!K.has_pi()) slice_epilogue_fast<NT, TM, true, ROLL, 0>(L, crot, acc, J0, J1, J2, Z, K);
-        else if (K.nA < 2 && K.nB < 2) slice_epilogue_fast<NT, TM, true, ROLL, 1>(L, crot, acc, J0, J1, J2, Z, K);
-        else slice_epilogue_fast<NT, TM, true, ROLL, 2>(L, crot, acc, J0, J1, J2, Z, K);
+        if (!K.has_pi()) slice_epilogue_fast<NT, TM, true, ROLL, 0, LC>(L, crot, acc, J0, J1, J2, Z, K);
+        else if (K.nA < 2 && K.nB < 2) slice_epilogue_fast<NT, TM, true, ROLL, 1, LC>(L, crot, acc, J0, J1, J2, Z, K);
+        else slice_epilogue_fast<NT, TM, true, ROLL, 2, LC>(L, crot, acc, J0, J1, J2, Z, K);
     } else if constexpr (TM) {
         tmem_wait_st();
 #pragma unroll 1
@@ -872,7 +875,7 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const double2 d = slice_value_slow<NT>(L, crot, J0, J1, J2, Z, K, 8 * ch + q);
+                const double2 d = slice_value_slow<NT, LC>(L, crot, J0, J1, J2, Z, K, 8 * ch + q);
                 double2 o = v2d(v + 4 * q);
                 o.x += d.x;
                 o.y += d.y;
@@ -885,7 +888,7 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
         while (alive) {
             const int g = __ffs(alive) - 1;
             alive &= alive - 1;
-            const double2 d = slice_value_slow<NT>(L, crot, J0, J1, J2, Z, K, g);
+            const double2 d = slice_value_slow<NT, LC>(L, crot, J0, J1, J2, Z, K, g);
             double2* ap = acc.amp_s + g * NT + threadIdx.x;
             double2 o = *ap;
             o.x += d.x;
@@ -897,12 +900,12 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
     if (kinds) K.reset();
 }
 
-template <int NT, bool TM, bool ROLL = false>
+template <int NT, bool TM, bool ROLL = false, bool LC = false>
 __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
                                                     SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
-                                                    uint32_t& J2, uint32_t& Z, KindCounters<NT>& K) {
+                                                    uint32_t& J2, uint32_t& Z, KindCounters<NT, LC>& K) {
     slice_epilogue_begin(tc, src, L, crot);
-    slice_epilogue_apply<NT, TM, ROLL>(L, crot, acc, J0, J1, J2, Z, K);
+    slice_epilogue_apply<NT, TM, ROLL, LC>(L, crot, acc, J0, J1, J2, Z, K);
 }
 
 
@@ -919,6 +922,7 @@ size_t slice_smem_bytes(const DevTable& t) {
 
 template <int NT, bool TM, bool FREE = true>
 __device__ __forceinline__ void slice_store_results(const LaunchReq& r, uint64_t off, SliceAcc<NT, TM>& acc) {
+    constexpr uint32_t kCols = NT > 128 ? 2 * kTmemCols : kTmemCols;
     if constexpr (TM) {
         tmem_wait_st();
 #pragma unroll 1
@@ -929,7 +933,7 @@ __device__ __forceinline__ void slice_store_results(const LaunchReq& r, uint64_t
 #pragma unroll
             for (int q = 0; q < 8; ++q) store_result(r, off + 8 * ch + q, v2d(v + 4 * q));
         }
-        if constexpr (FREE) tmem_free_cta(tmem_base_of(acc.taddr));
+        if constexpr (FREE) tmem_free_cta<kCols>(tmem_base_of(acc.taddr) - (threadIdx.x >> 7) * kTmemCols);
     } else {
 #pragma unroll 4
         for (int g = 0; g < kSliceG; ++g) store_result(r, off + g, acc.amp_s[g * NT + threadIdx.x]);
@@ -1374,9 +1378,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_eval_slice2(const DevTable
 // consecutive sorted words spans < 2^16). A thread owns 32 consecutive sorted
 // words, so their high parts (bits >= 16) take at most two values H0, H0 + 1:
 //   X = parity(psi & a_g) for g < 32
-//     = XOR_k T_k[nibble_k(psi)]                 (parameters 0..15: per-thread
-//                                                  Four-Russians tables, 4 x 16 words)
-//     ^ (g in M ? -parity(psi & H1) : -parity(psi & H0))   (parameters >= 16)
+//     = XOR_k T_k[nibble_k(psi)]                 (parameters 0..4G-1: per-thread
+//                                                  Four-Russians tables, G x 16 words)
+//     ^ -parity(psi & H0)                          (the group's shared high part)
 // with the tables built once per thread from its transposed low-bit planes.
 // The rest (dispatch, counters, epilogue) is the slice kernel's.
 template <int Dummy = 0>
@@ -1384,36 +1388,37 @@ __host__ __device__ constexpr uint32_t sorted_lut_offset() {
     return 2 * kSliceTile * 32 + 16;
 }
 
-template <bool TM = false, int G = kSortedGroups>
+template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads>
 size_t sorted_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
-    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * kSliceThreads * 16) +
-                     (kSliceThreads / 32) * kWarpScratch * 16 + size_t(G) * 16 * kSortedTableStride +
-                     size_t(kHiPlanes) * kSliceThreads * 4;
+    // (256-thread CTAs keep the rarely used high counter planes in local memory)
+    const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * NT * 16) + (NT / 32) * kWarpScratch * 16 +
+                     size_t(G) * 16 * NT * 4 + (NT > 128 ? 0 : size_t(kHiPlanes) * NT * 4);
     return TM ? (b > kTmemCtaSmem ? b : kTmemCtaSmem) : b;
 }
 
 
-template <bool TM = false, int G = kSortedGroups>
-__global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eval_sorted(const DevTable t,
-                                                                                       const LaunchReq r) {
+template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads>
+__global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1) k_eval_sorted(const DevTable t,
+                                                                                             const LaunchReq r) {
+    static_assert(!TM || NT == 128 || NT == 256, "TMEM: 4 or 8 warps per CTA");
     constexpr int kLow = 4 * G;  // parameters 0 .. kLow-1 through the per-thread tables
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint32_t tmem_base_s;
     const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset());
     const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
-    double2* crot = amp_s + (TM ? 0 : kSliceG * kSliceThreads) + (threadIdx.x >> 5) * kWarpScratch;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * kSliceThreads) +
-                                                (kSliceThreads / 32) * kWarpScratch);
-    uint32_t* hi_planes = tab + G * 16 * (kSortedTableStride / 4);
-    SliceAcc<kSliceThreads, TM> acc{amp_s, 0u};
-    if constexpr (TM) acc.taddr = tmem_alloc_cta(&tmem_base_s);
+    double2* crot = amp_s + (TM ? 0 : kSliceG * NT) + (threadIdx.x >> 5) * kWarpScratch;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * NT) +
+                                                (NT / 32) * kWarpScratch);
+    uint32_t* hi_planes = tab + G * 16 * NT;
+    SliceAcc<NT, TM> acc{amp_s, 0u};
+    if constexpr (TM) acc.taddr = tmem_alloc_cta<(NT > 128 ? 2 * kTmemCols : kTmemCols)>(&tmem_base_s);
     acc.zero();
 
     uint64_t tb, te;
     term_range(r, tb, te);
-    const uint64_t off = (uint64_t(blockIdx.x) * kSliceThreads + threadIdx.x) * kSliceG;
+    const uint64_t off = (uint64_t(blockIdx.x) * NT + threadIdx.x) * kSliceG;
     // ---- this thread's 32 sorted words -> planes -> Four-Russians tables ----
     uint32_t w[32];
 #pragma unroll
@@ -1431,14 +1436,17 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
 #pragma unroll
         for (int v = 1; v < 16; ++v) e[v] = e[v & (v - 1)] ^ w[4 * k + ((v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : 3)];
 #pragma unroll
-        for (int v = 0; v < 16; ++v) tab[(k * 16 + v) * kSliceThreads + threadIdx.x] = e[v];
+        for (int v = 0; v < 16; ++v) tab[(k * 16 + v) * NT + threadIdx.x] = e[v];
     }
     const uint32_t tab_s = smem_u32(tab) + threadIdx.x * 4;
     // per row (PZX_SORTED_ROWLOOP_G*): X = XOR_k T_k[nibble_k(psi)] ^ -parity(psi & H0)
 
     uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
-    KindCounters<kSliceThreads> K;
-    K.init(hi_planes + threadIdx.x);
+    // 256-thread CTAs keep the rarely used high counter planes in local memory
+    KindCounters<NT, (NT > 128)> K;
+    uint32_t hi_local[NT > 128 ? kHiPlanes : 1];
+    if constexpr (NT > 128) K.init(hi_local);
+    else K.init(hi_planes + threadIdx.x);
     __syncwarp();
 
     if (tb < te) {
@@ -1472,7 +1480,14 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
             uint32_t ad = a0;
             while (ad < aend) {
                 uint32_t vl, vpi, vpip, code;
-                if constexpr (G > 4) {
+                if constexpr (G > 4 && NT > 128) {
+                    asm volatile(PZX_SORTED_ROWLOOP_G6_256
+                                 : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
+                                   "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
+                                   "+r"(rb.y), "+r"(rb.z), "+r"(rb.w)
+                                 : "r"(aend), "r"(tab_s), "r"(H0)
+                                 : "memory");
+                } else if constexpr (G > 4) {
                     asm volatile(PZX_SORTED_ROWLOOP_G6
                                  : "+r"(ad), "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip),
                                    "=r"(code), "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x),
@@ -1492,7 +1507,7 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
                     if (code & kEndFlag)
-                        slice_term_epilogue<kSliceThreads, TM, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                        slice_term_epilogue<NT, TM, true, (NT > 128)>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                 }
             }
             __syncthreads();
@@ -1502,7 +1517,7 @@ __global__ void __launch_bounds__(kSliceThreads, TM ? (G > 4 ? 3 : 4) : 1) k_eva
             }
         }
     }
-    slice_store_results<kSliceThreads, TM>(r, off, acc);
+    slice_store_results<NT, TM>(r, off, acc);
 }
 
 
@@ -1610,15 +1625,16 @@ template <bool P64, bool LONG>
 cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc, dim3 grid) {
     const bool tm = tmem_accumulators();
     if (kc == KC_SORTED) {
+        // wide tables (48 KB per 128 threads) with TMEM: 256-thread CTAs, 2 per SM = 16 warps
         const bool wide = r.sorted_groups > kSortedGroups;
-        const size_t sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide>(t)
+        const size_t sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide, 256>(t)
                                      : sorted_smem_bytes<false, kSortedGroupsWide>(t))
                                : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
-        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide> : k_eval_sorted<false, kSortedGroupsWide>)
+        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide, 256> : k_eval_sorted<false, kSortedGroupsWide>)
                          : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
-        kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        kern<<<grid, sorted_threads(r.sorted_groups), sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     if (kc == KC_SLICEWC) {
@@ -1690,6 +1706,10 @@ bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
 // 32-thread CTAs only when a 128-thread CTA would leave warps idle (batches
 // of a few thousand assignments, C4); otherwise 128 threads with TMEM
 // accumulators -- term chunking supplies the CTAs a small batch lacks
+int sorted_threads(int sorted_groups) {
+    return (sorted_groups > kSortedGroups && tmem_accumulators()) ? 256 : kSliceThreads;
+}
+
 int slice_threads(const LaunchReq& r) {
     return r.n < uint64_t(4) * kSliceThreads * kSliceG ? 32 : kSliceThreads;
 }
@@ -1697,7 +1717,7 @@ int slice_threads(const LaunchReq& r) {
 int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
     const uint64_t per = kc == KC_SLICEWC                  ? uint64_t(32) * kSliceG
                        : kc == KC_SLICE2                   ? uint64_t(kSliceThreads) * 2 * kSliceG
-                       : kc == KC_SORTED                   ? uint64_t(kSliceThreads) * kSliceG
+                       : kc == KC_SORTED                   ? uint64_t(sorted_threads(r.sorted_groups)) * kSliceG
                        : (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(slice_threads(r)) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
@@ -1724,12 +1744,12 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_SORTED) {
         const bool wide = sorted_groups > kSortedGroups;
-        sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide>(t) : sorted_smem_bytes<false, kSortedGroupsWide>(t))
+        sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide, 256>(t) : sorted_smem_bytes<false, kSortedGroupsWide>(t))
                   : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
-        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide> : k_eval_sorted<false, kSortedGroupsWide>)
+        auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide, 256> : k_eval_sorted<false, kSortedGroupsWide>)
                          : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, sorted_threads(sorted_groups), sm);
     } else if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         if (nt == 32) {

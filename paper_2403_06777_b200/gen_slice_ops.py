@@ -309,18 +309,24 @@ def _loop_block(name, p64):
 # predicated off for one-parity rows (phi == 0 -> Y = 0).
 # operands: %0 ad, %1-%4 J0 J1 J2 Z, %5-%7 vl vpi vpip, %8 code (out),
 #   %9-%16 row registers, %17 aend, %18 tab (this thread's table address), %19 H0
-def _sorted_par(out, mask, o01, o23, G, pred=None):
+def _sorted_par(out, mask, o01, o23, G, pred=None, shift=9):
+    """X = XOR of the G table words ^ -parity(mask & H0); the row carries the
+    byte offsets (k * 16 + nibble_k) * 512 of groups 0..3 (128-thread tables),
+    shifted once more for 256-thread CTAs (shift = log2(4 x CTA threads))."""
     pp = f"@{pred} " if pred else ""
     L = []
     for i, (src, sh) in enumerate(((o01, False), (o01, True), (o23, False), (o23, True))):
         L.append(f"{'shr.b32' if sh else 'and.b32'} ta, {src}, {'16' if sh else '0xFFFF'};")
+        if shift > 9:  # the row's byte offsets assume 128-thread tables
+            L.append(f"shl.b32 ta, ta, {shift - 9};")
         L.append("add.u32 ta, ta, %18;")
         L.append(f"{pp}ld.shared.u32 t{i}, [ta];")
     for k in range(4, G):
         L.append(f"shr.b32 ta, {mask}, {4 * k};")
         L.append("and.b32 ta, ta, 15;")
-        L.append("mad.lo.u32 ta, ta, 512, %18;")
-        L.append(f"{pp}ld.shared.u32 t{k}, [ta+{k * 16 * 512}];")
+        L.append(f"shl.b32 ta, ta, {shift};")
+        L.append("add.u32 ta, ta, %18;")
+        L.append(f"{pp}ld.shared.u32 t{k}, [ta+{16 * k << shift}];")
     L.append(f"and.b32 ta, {mask}, %19;")
     L.append("popc.b32 ta, ta;")
     L.append("and.b32 ta, ta, 1;")
@@ -331,7 +337,7 @@ def _sorted_par(out, mask, o01, o23, G, pred=None):
     return L
 
 
-def _sorted_loop_block(name, G):
+def _sorted_loop_block(name, G, shift=9):
     n = 129
     bodies, label_of = {}, []
     for i in range(n):
@@ -344,10 +350,10 @@ def _sorted_loop_block(name, G):
          ".reg .pred pl, mo, cont, hp;",
          "ts%=: .branchtargets " + ", ".join(f"L{label_of[i]}_%=" for i in range(n)) + ";",
          "H%=:"]
-    b += _sorted_par("xx", "%9", "%13", "%14", G)
+    b += _sorted_par("xx", "%9", "%13", "%14", G, shift=shift)
     # one-parity rows (phi == 0, ~40 %) jump over the Y lookups (a uniform branch)
     b += ["setp.eq.b32 hp, %10, 0;", "mov.b32 yv, 0;", "@hp bra.uni NY%=;"]
-    b += _sorted_par("yv", "%10", "%15", "%16", G)
+    b += _sorted_par("yv", "%10", "%15", "%16", G, shift=shift)
     b += ["NY%=:"]
     b += ["mov.b32 opi, %12;", "mov.b32 %8, %11;",
           f"and.b32 tq, %11, {ROW_FLAG_MASK:#x};", "setp.eq.b32 pl, tq, 0;",
@@ -413,7 +419,9 @@ def generate() -> str:
     lines += _loop_block("PZX_SLICE_ROWLOOP_P32", False) + _loop_block("PZX_SLICE_ROWLOOP_P64", True)
     lines += ["// fused loop of the sorted-batch kernel (G = 4 / 6 table groups): %0 ad, %1-%4 J0 J1 J2 Z,",
               "//   %5-%7 vl vpi vpip, %8 code, %9-%16 row registers, %17 aend, %18 table, %19 H0"]
-    lines += _sorted_loop_block("PZX_SORTED_ROWLOOP_G4", 4) + _sorted_loop_block("PZX_SORTED_ROWLOOP_G6", 6)
+    # table rows are 4 B x CTA threads apart: 128 threads -> shift 9, 256 -> 10
+    lines += (_sorted_loop_block("PZX_SORTED_ROWLOOP_G4", 4, 9) + _sorted_loop_block("PZX_SORTED_ROWLOOP_G6", 6, 9) +
+              _sorted_loop_block("PZX_SORTED_ROWLOOP_G6_256", 6, 10))
     lines.append("// per-op row code-word flags (bit 8 lambda, 9 pi, 10 pi')")
     lines.append("#define PZX_SLICE_KIND_FLAGS { " + ", ".join(str(kind_flags(i)) for i in range(n)) + " }")
     lines.append("#define PZX_SLICE_JBASE { " + ", ".join(str(slice_op(i)[0]) for i in range(n)) + " }")
