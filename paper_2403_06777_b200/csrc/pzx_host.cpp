@@ -716,8 +716,21 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    constexpr uint64_t kSortedMaxBatch = uint64_t(1) << 26;  // bounds the sort / regroup scratch (~70 B per word)
+    if (kc == KC_SORTED && r.n > kSortedMaxBatch) {
+        // huge word lists: independent sub-batches (each sorted on its own)
+        const LaunchReq whole = r;
+        for (uint64_t o = 0; o < whole.n; o += kSortedMaxBatch) {
+            LaunchReq s = whole;
+            s.n = std::min(kSortedMaxBatch, whole.n - o);
+            s.d_asg = whole.d_asg + o;
+            s.d_amp = whole.d_amp ? whole.d_amp + o : nullptr;
+            s.d_prob = whole.d_prob ? whole.d_prob + o : nullptr;
+            if ((st = run_eval(ctx, t, s, flags))) return st;
+        }
+        return PZX_OK;
+    }
     if (kc == KC_SORTED) {  // sort word|position pairs; results are scattered back by position
-        if (r.n > uint64_t(UINT32_MAX)) return set_err(ctx, PZX_E_CAPACITY, "sorted kernel: batch > 2^32");
         if (!r.d_asg) return set_err(ctx, PZX_E_INVALID, "sorted kernel needs an explicit word list");
         if ((st = cuda_err(ctx, grow(&ctx->d_sort, &ctx->sort_cap, sort_scratch_bytes(r.n) + 256), "alloc sort scratch"))) return st;
         if ((st = cuda_err(ctx, sort_words(r.d_asg, r.n, t->dev.n_params, ctx->d_sort, &r.d_sorted, &r.d_perm,

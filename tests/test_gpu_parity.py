@@ -491,3 +491,16 @@ def test_wide_params_tmem_slice_path(ctx, P_):
     idx = np.random.default_rng(P_).choice(n, 24, replace=False)
     _, want = O.eval_batch(e, (np.uint64(first) + idx.astype(np.uint64)), 8, impl="ref" if O.have_ref() else "port")
     assert_close(amp[idx], want)
+
+
+def test_sorted_kernel_sub_batches(ctx):
+    """Word lists above the sorted kernel's 2^26 batch cap run as independent
+    sorted sub-batches (bounded scratch); results in the caller's order."""
+    e = synth.generate(24, 64, 1, 12, 5300)
+    t = ctx.compile_bit_table(e)
+    n = (1 << 26) + 1000
+    words = np.random.default_rng(1).integers(0, 1 << 24, n, dtype=np.uint64)
+    amp = ctx.evaluate_batch(t, words)
+    idx = np.random.default_rng(2).choice(n, 4096, replace=False)
+    idx[:2] = [n - 1, (1 << 26) - 1]
+    assert_close(amp[idx], ctx.evaluate_batch(t, words[idx], flags=P.KERNEL_GENERAL), 1e-13)
