@@ -1135,11 +1135,12 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
 // memory accumulators. Every warp's partial amplitudes go to its own chunk
 // slot; the fixed-order chunk reduction sums them.
 constexpr int kWarpChunks = kSliceThreads / 32;
+constexpr int kWcTile = 128;  // rows per per-warp TMA tile (the row streams come from HBM)
 static_assert(kWarpChunks == kWarpChunksHost, "warp-chunk count shared with the host");
 
 template <bool P64>
 __host__ __device__ constexpr uint32_t slicewc_lut_offset() {
-    return kWarpChunks * 2 * kSliceTile * 32 + kWarpChunks * 16 + 16;
+    return kWarpChunks * 2 * kWcTile * 32 + kWarpChunks * 16 + 16;
 }
 
 template <bool P64>
@@ -1157,7 +1158,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
     // the warp index through a lane-0 shuffle: provably warp-uniform, so the
     // row loop's branches stay uniform (no divergence bookkeeping)
     const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31u;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpChunks * 2 * kSliceTile * 32) + 2 * warp;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpChunks * 2 * kWcTile * 32) + 2 * warp;
     if (lane == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -1183,17 +1184,17 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
     K.init(hi_planes + threadIdx.x);
 
     if (tb < te) {
-        uint4* tiles = reinterpret_cast<uint4*>(smem) + warp * (2 * kSliceTile * 2);
+        uint4* tiles = reinterpret_cast<uint4*>(smem) + warp * (2 * kWcTile * 2);
         const uint32_t tiles_s = smem_u32(tiles);
         const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
-        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        const uint32_t ntiles = uint32_t((R1 - R0 + kWcTile - 1) / kWcTile);
         auto issue = [&](uint32_t tile) {
-            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
-            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint64_t rr = R0 + uint64_t(tile) * kWcTile;
+            const uint64_t n = (R1 - rr) < uint64_t(kWcTile) ? (R1 - rr) : uint64_t(kWcTile);
             const uint32_t bytes = uint32_t(n) * 32u;
             uint64_t* bar = &bars[tile & 1];
             mbar_expect_tx(bar, bytes);
-            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.srows + rr * 2, bytes, bar);
+            tma_load_1d(tiles + (tile & 1) * kWcTile * 2, t.srows + rr * 2, bytes, bar);
         };
         if (lane == 0) {
             if (ntiles > 0) issue(0);
@@ -1203,9 +1204,9 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
         termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
         for (uint32_t i = 0; i < ntiles; ++i) {
             mbar_wait(&bars[i & 1], (i >> 1) & 1u);
-            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
-            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
-            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint64_t rem = R1 - R0 - uint64_t(i) * kWcTile;
+            const uint32_t n = rem < uint64_t(kWcTile) ? uint32_t(rem) : uint32_t(kWcTile);
+            const uint32_t a0 = tiles_s + (i & 1) * kWcTile * 32;
             const uint32_t aend = a0 + n * 32;
             uint4 ra = lds128(a0), rb = lds128(a0 + 16);
             uint32_t ad = a0;
