@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const 
 constexpr int kSliceThreads = 128;
 constexpr int kSliceBits = 5;
 constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread, one bit each
-constexpr int kSliceTile = 64;            // rows (32 B each) per TMA-staged tile (3 CTAs/SM fit)
+constexpr int kSliceTile = 128;           // rows (32 B each) per TMA-staged tile
 constexpr int kPlanes = 7;                // bit-sliced counters up to 127 (terms <= kSegRows rows)
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -1384,14 +1384,20 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_eval_slice2(const DevTable
 //     ^ -parity(psi & H0)                          (the group's shared high part)
 // with the tables built once per thread from its transposed low-bit planes.
 // The rest (dispatch, counters, epilogue) is the slice kernel's.
-template <int Dummy = 0>
+// row tiles: 128 rows, 64 for the 256-thread wide-table variant (its 96 KB of
+// tables must leave room for two CTAs per SM)
+template <int NT = kSliceThreads>
+__host__ __device__ constexpr int sorted_tile() {
+    return NT > 128 ? 64 : kSliceTile;
+}
+template <int NT = kSliceThreads>
 __host__ __device__ constexpr uint32_t sorted_lut_offset() {
-    return 2 * kSliceTile * 32 + 16;
+    return 2 * sorted_tile<NT>() * 32 + 16;
 }
 
 template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads>
 size_t sorted_smem_bytes(const DevTable& t) {
-    const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    const uint32_t amp_off = (sorted_lut_offset<NT>() + t.lut_layout.bytes + 127u) & ~127u;
     // (256-thread CTAs keep the rarely used high counter planes in local memory)
     const size_t b = amp_off + (TM ? 0 : size_t(kSliceG) * NT * 16) + (NT / 32) * kWarpScratch * 16 +
                      size_t(G) * 16 * NT * 4 + (NT > 128 ? 0 : size_t(kHiPlanes) * NT * 4);
@@ -1403,11 +1409,12 @@ template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads>
 __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1) k_eval_sorted(const DevTable t,
                                                                                              const LaunchReq r) {
     static_assert(!TM || NT == 128 || NT == 256, "TMEM: 4 or 8 warps per CTA");
+    constexpr int ST = sorted_tile<NT>();
     constexpr int kLow = 4 * G;  // parameters 0 .. kLow-1 through the per-thread tables
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint32_t tmem_base_s;
-    const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset());
-    const uint32_t amp_off = (sorted_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    const SmemLut L = kernel_prologue(t, smem, sorted_lut_offset<NT>());
+    const uint32_t amp_off = (sorted_lut_offset<NT>() + t.lut_layout.bytes + 127u) & ~127u;
     double2* amp_s = reinterpret_cast<double2*>(smem + amp_off);
     double2* crot = amp_s + (TM ? 0 : kSliceG * NT) + (threadIdx.x >> 5) * kWarpScratch;
     uint32_t* tab = reinterpret_cast<uint32_t*>(amp_s + (TM ? 0 : kSliceG * NT) +
@@ -1452,17 +1459,17 @@ __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1)
 
     if (tb < te) {
         uint4* tiles = reinterpret_cast<uint4*>(smem);
-        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSliceTile * 32);
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * ST * 32);
         const uint32_t tiles_s = smem_u32(tiles);
         const uint64_t R0 = t.term_row[tb], R1 = t.term_row[te];
-        const uint32_t ntiles = uint32_t((R1 - R0 + kSliceTile - 1) / kSliceTile);
+        const uint32_t ntiles = uint32_t((R1 - R0 + ST - 1) / ST);
         auto issue = [&](uint32_t tile) {
-            const uint64_t rr = R0 + uint64_t(tile) * kSliceTile;
-            const uint64_t n = (R1 - rr) < uint64_t(kSliceTile) ? (R1 - rr) : uint64_t(kSliceTile);
+            const uint64_t rr = R0 + uint64_t(tile) * ST;
+            const uint64_t n = (R1 - rr) < uint64_t(ST) ? (R1 - rr) : uint64_t(ST);
             const uint32_t bytes = uint32_t(n) * 32u;
             uint64_t* bar = &bars[tile & 1];
             mbar_expect_tx(bar, bytes);
-            tma_load_1d(tiles + (tile & 1) * kSliceTile * 2, t.qrows + rr * 2, bytes, bar);
+            tma_load_1d(tiles + (tile & 1) * ST * 2, t.qrows + rr * 2, bytes, bar);
         };
         if (threadIdx.x == 0) {
             if (ntiles > 0) issue(0);
@@ -1472,9 +1479,9 @@ __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1)
         termc_init(tc, crot + kCrot, t.sterm_c, tb, te);
         for (uint32_t i = 0; i < ntiles; ++i) {
             mbar_wait(&bars[i & 1], (i >> 1) & 1u);
-            const uint64_t rem = R1 - R0 - uint64_t(i) * kSliceTile;
-            const uint32_t n = rem < uint64_t(kSliceTile) ? uint32_t(rem) : uint32_t(kSliceTile);
-            const uint32_t a0 = tiles_s + (i & 1) * kSliceTile * 32;
+            const uint64_t rem = R1 - R0 - uint64_t(i) * ST;
+            const uint32_t n = rem < uint64_t(ST) ? uint32_t(rem) : uint32_t(ST);
+            const uint32_t a0 = tiles_s + (i & 1) * ST * 32;
             const uint32_t aend = a0 + n * 32;
             // fused row loop (generated PTX): rows prefetched one ahead in ra / rb
             uint4 ra = lds128(a0), rb = lds128(a0 + 16);
