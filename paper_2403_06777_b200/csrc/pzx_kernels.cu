@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const 
 constexpr int kSliceThreads = 128;
 constexpr int kSliceBits = 5;
 constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread, one bit each
-constexpr int kSliceTile = 128;           // rows (32 B each) per TMA-staged tile
+constexpr int kSliceTile = 256;           // rows (32 B each) per TMA-staged tile
 constexpr int kPlanes = 7;                // bit-sliced counters up to 127 (terms <= kSegRows rows)
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -1388,7 +1388,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_eval_slice2(const DevTable
 // tables must leave room for two CTAs per SM)
 template <int NT = kSliceThreads>
 __host__ __device__ constexpr int sorted_tile() {
-    return NT > 128 ? 64 : kSliceTile;
+    return NT > 128 ? 64 : 128;
 }
 template <int NT = kSliceThreads>
 __host__ __device__ constexpr uint32_t sorted_lut_offset() {
