@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_gray(const DevTable t, const 
 constexpr int kSliceThreads = 128;
 constexpr int kSliceBits = 5;
 constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread, one bit each
-constexpr int kSliceTile = 256;           // rows (32 B each) per TMA-staged tile
+constexpr int kSliceTile = 512;           // rows (32 B each) per TMA-staged tile
 constexpr int kPlanes = 7;                // bit-sliced counters up to 127 (terms <= kSegRows rows)
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
