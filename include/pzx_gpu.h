@@ -165,6 +165,19 @@ pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assign
 pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n,
                               double* amp, double* prob, uint32_t flags);
 
+/* Exact evaluation -- the SPEC's integer-ring backend contract (S:441-498:
+ * "identical RingQuad outputs", "no floats in the kernel path"): out[5n] gets
+ * the canonical RingQuad {a, b, c, d, exp} (ring.hpp:17-38, ring.cpp:20-48) of
+ * S(a) per assignment, bit-identical to the reference's sequential fold
+ * (ring_add over instantiate_diagram values, diagram.cpp:149-165; replaces
+ * ParamScalarExpression::evaluate with exact output). Returns PZX_E_OVERFLOW
+ * (pzx::OverflowError, ring.cpp:13-18) when a value or an intermediate term
+ * product leaves int64; those entries get exp = -1 and the rest are written.
+ * The reference may overflow earlier on intermediates of its own fold order. */
+pzx_status pzx_evaluate_exact(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments, uint64_t n,
+                              int64_t* out);
+pzx_status pzx_evaluate_exact_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n, int64_t* out);
+
 /* Asynchronous DEVICE-pointer variants on `stream` (used as given, NULL = default stream):
  * d_assignments may be NULL for the enumerated batch starting at `first`.
  * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)

@@ -21,7 +21,8 @@ EXPORTS = (
     "pzx_slice_op_table", "pzx_marginal_sum", "pzx_weak_sample", "pzx_pzx1_encode", "pzx_pzx1_encode_expr",
     "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
     "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
-    "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex",
+    "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex", "pzx_evaluate_exact",
+    "pzx_evaluate_exact_range",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -89,6 +90,8 @@ def lib() -> C.CDLL:
     L.pzx_table_term_info.argtypes = [vp, C.c_uint64, i64p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.pzx_evaluate.argtypes = [vp, vp, u64p, C.c_uint64, dblp, dblp, C.c_uint32]
     L.pzx_evaluate_range.argtypes = [vp, vp, C.c_uint64, C.c_uint64, dblp, dblp, C.c_uint32]
+    L.pzx_evaluate_exact.argtypes = [vp, vp, u64p, C.c_uint64, i64p]
+    L.pzx_evaluate_exact_range.argtypes = [vp, vp, C.c_uint64, C.c_uint64, i64p]
     L.pzx_evaluate_device.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                       vp, vp, C.c_uint32, vp]
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]

@@ -580,6 +580,7 @@ struct pzx_ctx {
     void* d_prob = nullptr; size_t prob_cap = 0;
     void* d_partial = nullptr; size_t partial_cap = 0;
     void* d_chunks = nullptr; size_t chunks_cap = 0;
+    void* d_xout = nullptr; size_t xout_cap = 0;  // exact outputs + overflow flags
     void* d_dbg = nullptr; size_t dbg_cap = 0;
     void* d_sort = nullptr; size_t sort_cap = 0;
 };
@@ -596,6 +597,8 @@ struct pzx_table {
     void* d_srows = nullptr;
     void* d_sterm_c = nullptr;
     void* d_qrows = nullptr;
+    void* d_exact = nullptr;  // exact-evaluation tables (built on first pzx_evaluate_exact)
+    ExactDev exact;
 };
 
 namespace {
@@ -807,6 +810,159 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     return PZX_OK;
 }
 
+// --------------------------------------------------- exact evaluation ----
+// Z[w] products with the device kernel's operand rule (x within 62 bits, every
+// product coefficient within int64), so a table entry the host accepts is one
+// the kernel can multiply.
+bool zw_fits62(const Zw& z) {
+    for (int i = 0; i < 4; ++i)
+        if (z.c[i] >= (int64_t(1) << 62) || z.c[i] <= -(int64_t(1) << 62)) return false;
+    return true;
+}
+bool zw_mul_chk(const Zw& x, const Zw& y, Zw& out) {
+    if (!zw_fits62(x)) return false;
+    i128 t[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const i128 p = i128(x.c[i]) * y.c[j];
+            if (i + j < 4) t[i + j] += p; else t[i + j - 4] -= p;
+        }
+    for (int k = 0; k < 4; ++k) {
+        if (t[k] > INT64_MAX || t[k] < INT64_MIN) return false;
+        out.c[k] = int64_t(t[k]);
+    }
+    return true;
+}
+
+// Per-term integral constants F_t (C'_t * sqrt2^E_t * mu^nLM_t scaled by 2^e_t,
+// e_t reduced while F_t is divisible by 2), the common exponent K, and the
+// power tables of the assignment-dependent factors.
+pzx_status build_exact(pzx_ctx* ctx, pzx_table* t) {
+    const HostTable& h = t->host;
+    const uint64_t m = h.coef.size();
+    const uint32_t M = std::max<uint32_t>(h.max_rows, 1);
+    std::vector<int64_t> dt(4 * m, 0);
+    std::vector<int32_t> ex(m, 0);
+    std::vector<uint8_t> bad(m, 0);
+    const Zw s2 = zw(0, 1, 0, -1), mu = zw_generator(K_MU);
+    int32_t K = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        const Quad& c = h.coef[i];
+        // a + b sqrt2 + i(c + d sqrt2) = a + (b + d) w + c w^2 + (d - b) w^3
+        const i128 c1 = i128(c.b) + c.d, c3 = i128(c.d) - c.b;
+        bool ok = c1 <= INT64_MAX && c1 >= INT64_MIN && c3 <= INT64_MAX && c3 >= INT64_MIN;
+        Zw f = ok ? zw(c.a, int64_t(c1), c.c, int64_t(c3)) : Zw{};
+        for (int k = 0; ok && k < h.e_t[i]; ++k) ok = zw_mul_chk(s2, f, f);
+        for (int k = 0; ok && k < h.nlm_t[i]; ++k) ok = zw_mul_chk(mu, f, f);
+        int32_t e = c.e;
+        if (ok && f.zero()) e = 0;
+        while (ok && e > 0 && ((f.c[0] | f.c[1] | f.c[2] | f.c[3]) & 1) == 0) {
+            for (int k = 0; k < 4; ++k) f.c[k] /= 2;
+            --e;
+        }
+        if (!ok) { bad[i] = 1; f = Zw{}; e = 0; }
+        for (int k = 0; k < 4; ++k) dt[4 * i + k] = f.c[k];
+        ex[i] = e;
+        K = std::max(K, e);
+    }
+    std::vector<uint8_t> sh(m);
+    for (uint64_t i = 0; i < m; ++i) sh[i] = bad[i] ? 255 : uint8_t(std::min<int32_t>(K - ex[i], 255));
+    std::vector<int64_t> u, pd, p3;
+    Zw x = zw(1, 0, 0, 0);
+    const Zw s2m1 = zw(-1, 1, 0, -1);
+    for (uint32_t s = 0; s <= M && zw_fits62(x); ++s) {
+        for (int k = 0; k < 4; ++k) u.push_back(x.c[k]);
+        if (!zw_mul_chk(x, s2m1, x)) break;
+    }
+    std::vector<Zw> pp, pm;
+    Zw a = zw(1, 0, 0, 0), b = a;
+    const Zw pi = zw_generator(K_PI), pip = zw_generator(K_PIP);
+    for (uint32_t d = 0; d <= M && zw_fits62(a) && zw_fits62(b); ++d) {
+        pp.push_back(a);
+        pm.push_back(b);
+        if (!zw_mul_chk(a, pi, a) || !zw_mul_chk(b, pip, b)) break;
+    }
+    const uint32_t pd_n = uint32_t(pp.size());
+    for (uint32_t i = 0; i < 2 * pd_n - 1; ++i) {
+        const int d = int(i) - int(pd_n - 1);
+        const Zw& z = d >= 0 ? pp[size_t(d)] : pm[size_t(-d)];
+        for (int k = 0; k < 4; ++k) pd.push_back(z.c[k]);
+    }
+    int64_t v3 = 1;
+    for (uint32_t k = 0; k <= M / 2 + 1; ++k) {
+        p3.push_back(v3);
+        if (v3 > (int64_t(1) << 61) / 3) break;
+        v3 *= 3;
+    }
+    // one allocation: dt | u | pd | p3 | sh
+    const size_t o_u = dt.size() * 8, o_pd = o_u + u.size() * 8, o_p3 = o_pd + pd.size() * 8,
+                 o_sh = o_p3 + p3.size() * 8, bytes = o_sh + sh.size() + 16;
+    std::vector<unsigned char> blob(bytes, 0);
+    std::memcpy(blob.data(), dt.data(), dt.size() * 8);
+    std::memcpy(blob.data() + o_u, u.data(), u.size() * 8);
+    std::memcpy(blob.data() + o_pd, pd.data(), pd.size() * 8);
+    std::memcpy(blob.data() + o_p3, p3.data(), p3.size() * 8);
+    std::memcpy(blob.data() + o_sh, sh.data(), sh.size());
+    pzx_status st;
+    if ((st = cuda_err(ctx, upload_vec(&t->d_exact, blob), "upload exact tables"))) return st;
+    const unsigned char* base = static_cast<const unsigned char*>(t->d_exact);
+    ExactDev& X = t->exact;
+    X.dt = reinterpret_cast<const int64_t*>(base);
+    X.u = reinterpret_cast<const int64_t*>(base + o_u);
+    X.pd = reinterpret_cast<const int64_t*>(base + o_pd);
+    X.p3 = reinterpret_cast<const int64_t*>(base + o_p3);
+    X.sh = base + o_sh;
+    X.u_n = uint32_t(u.size() / 4);
+    X.pd_n = pd_n;
+    X.p3_n = uint32_t(p3.size());
+    X.K = K;
+    return PZX_OK;
+}
+
+pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t first, uint64_t n, int64_t* out) {
+    if (!ctx || !t || (n && !out)) return PZX_E_INVALID;
+    if (t->device < 0 || !t->dev.rows) return set_err(ctx, PZX_E_INVALID, "evaluate_exact: host-only table");
+    if (n == 0) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    if (!t->d_exact && (st = build_exact(ctx, t))) return st;
+    const uint64_t m = t->dev.n_terms;
+    const uint64_t* d_asg = nullptr;
+    if (asg) {
+        if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc assignments"))) return st;
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_asg, asg, n * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D assignments"))) return st;
+        d_asg = static_cast<const uint64_t*>(ctx->d_asg);
+    }
+    // grid: >= 8 waves of 4 resident CTAs per SM via row-balanced term chunks
+    const uint64_t blocks = (n + kExactThreads - 1) / kExactThreads;
+    const uint64_t target = uint64_t(ctx->n_sm) * 4 * 8;
+    uint64_t chunks = blocks >= target ? 1 : (target + blocks - 1) / blocks;
+    chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, m));
+    chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, t->dev.n_rows / min_chunk_rows()));
+    chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, (uint64_t(1) << 30) / (n * 64 + 1)));
+    chunks = std::min<uint64_t>(chunks, 65535);
+    const uint64_t* d_chunks = nullptr;
+    if (chunks > 1) {
+        std::vector<uint64_t> b;
+        chunk_bounds(t->host, 0, m, int(chunks), b);
+        if ((st = cuda_err(ctx, grow(&ctx->d_chunks, &ctx->chunks_cap, b.size() * 8), "alloc chunks"))) return st;
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_chunks, b.data(), b.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy chunks"))) return st;
+        if ((st = cuda_err(ctx, grow(&ctx->d_partial, &ctx->partial_cap, size_t(chunks) * n * 64), "alloc partials"))) return st;
+        d_chunks = static_cast<const uint64_t*>(ctx->d_chunks);
+    }
+    if ((st = cuda_err(ctx, grow(&ctx->d_xout, &ctx->xout_cap, n * 44 + 16), "alloc exact outputs"))) return st;
+    int64_t* d_out = static_cast<int64_t*>(ctx->d_xout);
+    uint32_t* d_flag = reinterpret_cast<uint32_t*>(d_out + 5 * n);
+    if ((st = cuda_err(ctx, cudaMemsetAsync(d_flag, 0, n * 4, ctx->stream), "clear flags"))) return st;
+    if ((st = cuda_err(ctx, launch_exact(t->dev, t->exact, d_asg, first, n, d_chunks, int(chunks), ctx->d_partial, d_flag,
+                                         d_out, ctx->stream, &ctx->launches), "exact kernel"))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(out, d_out, n * 40, cudaMemcpyDeviceToHost, ctx->stream), "D2H exact"))) return st;
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "evaluate_exact"))) return st;
+    for (uint64_t i = 0; i < n; ++i)
+        if (out[5 * i + 4] < 0) return set_err(ctx, PZX_E_OVERFLOW, "evaluate_exact: ring coefficient out of 64-bit range");
+    return PZX_OK;
+}
+
 int prob_mode_of(uint32_t flags) {
     return (flags & PZX_PROB_REAL) ? 2 : (flags & PZX_PROB_ABS2) ? 1 : 1;
 }
@@ -855,7 +1011,7 @@ void pzx_destroy(pzx_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg, ctx->d_sort})
+    for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg, ctx->d_sort, ctx->d_xout})
         if (p) cudaFree(p);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1169,7 +1325,7 @@ void pzx_table_free(pzx_table* t) {
     if (!t) return;
     if (t->device < 0) { delete t; return; }
     cudaSetDevice(t->device);
-    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows})
+    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows, t->d_exact})
         if (p) cudaFree(p);
     delete t;
 }
@@ -1241,6 +1397,15 @@ pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assign
 pzx_status pzx_evaluate_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n,
                               double* amp, double* prob, uint32_t flags) {
     return eval_host(ctx, t, nullptr, first, n, amp, prob, flags);
+}
+
+pzx_status pzx_evaluate_exact(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments, uint64_t n, int64_t* out) {
+    if (n && !assignments) return PZX_E_INVALID;
+    return exact_host(ctx, const_cast<pzx_table*>(t), assignments, 0, n, out);
+}
+
+pzx_status pzx_evaluate_exact_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n, int64_t* out) {
+    return exact_host(ctx, const_cast<pzx_table*>(t), nullptr, first, n, out);
 }
 
 // Marginal summing: out[i] = sum over b < 2^m of prob(fixed[i] | b),

@@ -2100,4 +2100,168 @@ cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_
     return cudaGetLastError();
 }
 
+
+// --------------------------------------------------------- exact kernel ----
+// pzx_evaluate_exact: the SPEC's integer-ring backend contract (S:444, 486,
+// 493: identical RingQuad outputs, no floats in the kernel path). Each thread
+// owns one assignment and walks the rows of its term chunk (uniform loads,
+// broadcast through L1), accumulating the wide counters of DESIGN.md §2; a
+// term's value is then
+//   F_t * w^(j + 6 s1) * (sqrt2 - 1)^s1 * 3^min(a,b) * pi^(a-b) / 2^e_t
+// evaluated in Z[w] (power basis 1, w, w^2, w^3; w^4 = -1; every factor but the
+// 2^-e_t is an algebraic integer) with int64 operands, int128 products and an
+// int128 sum over terms; the sum is converted to the reference's canonical
+// RingQuad (ring.cpp:20-48) once per assignment.
+using i128d = __int128;
+
+__device__ __forceinline__ bool fits_i62(long long v) { return v < (1ll << 62) && v > -(1ll << 62); }
+__device__ __forceinline__ bool fits_i64(i128d v) { return v == i128d((long long)v); }
+
+// out = x * y in Z[w]; false when x exceeds 62 bits or a coefficient of the
+// product exceeds int64 (the reference's narrow(), ring.cpp:13-18). With
+// |x| < 2^62 and |y| < 2^63 every int128 partial sum stays below 2^127.
+__device__ __forceinline__ bool zw_mul_dev(const long long* x, const long long* y, long long* out) {
+    i128d t[4] = {0, 0, 0, 0};
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ok &= fits_i62(x[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const i128d p = i128d(x[i]) * y[j];
+            if (i + j < 4) t[i + j] += p; else t[i + j - 4] -= p;
+        }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { ok &= fits_i64(t[k]); out[k] = (long long)t[k]; }
+    return ok;
+}
+
+// value = (c0 + c1 w + c2 w^2 + c3 w^3) / 2^K -> canonical RingQuad {a,b,c,d,exp}
+// (w = (sqrt2 + i sqrt2)/2: a = 2c0, b = c1 - c3, c = 2c2, d = c1 + c3 over 2^(K+1));
+// exp = -1 marks an assignment whose value does not fit (PZX_E_OVERFLOW)
+__device__ void exact_store(const i128d* c, int K, bool ok, long long* out) {
+    i128d a = 2 * c[0], b = c[1] - c[3], cc = 2 * c[2], d = c[1] + c[3];
+    long long e = K + 1;
+    if (ok && a == 0 && b == 0 && cc == 0 && d == 0) e = 0;
+    while (ok && e > 0 && ((((long long)a) | ((long long)b) | ((long long)cc) | ((long long)d)) & 1) == 0) {
+        a >>= 1; b >>= 1; cc >>= 1; d >>= 1; --e;  // exact: all even
+    }
+    ok = ok && fits_i64(a) && fits_i64(b) && fits_i64(cc) && fits_i64(d);
+    out[0] = ok ? (long long)a : 0;
+    out[1] = ok ? (long long)b : 0;
+    out[2] = ok ? (long long)cc : 0;
+    out[3] = ok ? (long long)d : 0;
+    out[4] = ok ? e : -1;
+}
+
+template <bool P64>
+__global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, const ExactDev x, const uint64_t* __restrict__ asg,
+                                                      uint64_t first, uint64_t n, const uint64_t* __restrict__ chunk_terms,
+                                                      int n_chunks, i128d* __restrict__ partial, uint32_t* __restrict__ pflag,
+                                                      long long* __restrict__ out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLut L = stage_lut(t, smem);
+    __syncthreads();
+    const uint64_t idx = uint64_t(blockIdx.x) * kExactThreads + threadIdx.x;
+    const uint64_t a = idx < n ? (asg ? asg[idx] : first + idx) : 0;
+    const uint64_t tb = n_chunks > 1 ? chunk_terms[blockIdx.y] : 0;
+    const uint64_t te = n_chunks > 1 ? chunk_terms[blockIdx.y + 1] : t.n_terms;
+    i128d acc[4] = {0, 0, 0, 0};
+    bool ok = true;
+    const uint64_t r1 = tb < te ? t.term_row[te] : 0;
+    uint64_t term = tb;
+    Wide w{0, 0, 0, 0, 0};
+    for (uint64_t row = tb < te ? t.term_row[tb] : 0; row < r1; ++row) {
+        const Row<P64> v = load_row_global<P64>(t, row);
+        widen(w, L.codes[((v.code & kCodeMask) >> 2) + (v.p(a) | (v.q(a) << 1))]);
+        if (!(v.code & kEndFlag)) continue;
+        if (w.z == 0) {
+            const uint32_t j = (w.j + 6u * w.s1) & 7u;
+            const uint32_t m = min(w.a, w.b);
+            const int dd = int(w.a) - int(w.b);
+            const uint32_t ad = uint32_t(dd < 0 ? -dd : dd);
+            const uint32_t sh = x.sh[term];
+            if (w.s1 >= x.u_n || ad >= x.pd_n || m >= x.p3_n || sh > 62) {
+                ok = false;
+            } else {
+                long long u[4], p[4], q[4], dt[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    u[k] = x.u[4 * w.s1 + k];
+                    p[k] = x.pd[4 * (int(x.pd_n) - 1 + dd) + k];
+                    dt[k] = x.dt[4 * term + k];
+                }
+                ok &= zw_mul_dev(u, p, q);
+                const long long t3 = x.p3[m];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const i128d v3 = i128d(q[k]) * t3;
+                    ok &= fits_i64(v3);
+                    q[k] = (long long)v3;
+                }
+                ok &= zw_mul_dev(q, dt, p);
+                // w^j: j & 4 negates, j & 3 rotates (w^4 = -1)
+                long long r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int src = (k - int(j & 3u)) & 3;
+                    const long long v0 = p[src];
+                    r[k] = (k < int(j & 3u)) ? -v0 : v0;
+                    if (j & 4u) r[k] = -r[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] += i128d(r[k]) << sh;
+            }
+        }
+        w = Wide{0, 0, 0, 0, 0};
+        ++term;
+    }
+    if (idx >= n) return;
+    if (n_chunks > 1) {
+        i128d* pp = partial + 4 * (uint64_t(blockIdx.y) * n + idx);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pp[k] = acc[k];
+        if (!ok) pflag[idx] = 1u;
+        return;
+    }
+    exact_store(acc, x.K, ok, out + 5 * idx);
+}
+
+// sum of the chunk partials of each assignment (integer: order-free) + canonical store
+__global__ void k_exact_reduce(const i128d* __restrict__ partial, const uint32_t* __restrict__ pflag, int n_chunks,
+                               uint64_t n, int K, long long* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    i128d acc[4] = {0, 0, 0, 0};
+    for (int c = 0; c < n_chunks; ++c) {
+        const i128d* pp = partial + 4 * (uint64_t(c) * n + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] += pp[k];
+    }
+    exact_store(acc, K, pflag[i] == 0u, out + 5 * i);
+}
+
+cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
+                         const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
+                         int64_t* d_out, cudaStream_t s, uint64_t* launches) {
+    if (n == 0) return cudaSuccess;
+    const size_t sm = t.lut_layout.bytes;
+    auto kern = t.p64 ? k_eval_exact<true> : k_eval_exact<false>;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
+    const dim3 grid(unsigned((n + kExactThreads - 1) / kExactThreads), unsigned(n_chunks));
+    i128d* part = static_cast<i128d*>(d_partial);
+    long long* o = reinterpret_cast<long long*>(d_out);
+    kern<<<grid, kExactThreads, sm, s>>>(t, x, d_asg, first, n, d_chunk_terms, n_chunks, part, d_pflag, o);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || n_chunks <= 1) return e;
+    k_exact_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(part, d_pflag, n_chunks, n, x.K, o);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 }  // namespace pzxb

@@ -427,6 +427,29 @@ class Context:
                                               N.ptr(pr, C.c_double), fl), self.handle)
         return (amp, pr) if pr is not None else amp
 
+    def evaluate_exact(self, table: DeviceTable, assignments, *, allow_overflow: bool = False) -> np.ndarray:
+        """Exact S(a) per assignment as canonical RingQuads, int64 [n, 5] =
+        (a, b, c, d, exp) -- the SPEC's integer backend, the same
+        layout as oracle_py.eval_batch's exact output. OverflowError when a
+        value leaves int64 (allow_overflow: return with exp = -1 there)."""
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        out = np.zeros((a.size, 5), np.int64)
+        if a.size:
+            st = N.lib().pzx_evaluate_exact(self.handle, table.handle, a.ctypes.data_as(N.u64p), a.size,
+                                            out.ctypes.data_as(N.i64p))
+            if not (allow_overflow and st == 4):
+                _check(st, self.handle)
+        return out
+
+    def evaluate_exact_range(self, table: DeviceTable, first: int, n: int, *,
+                             allow_overflow: bool = False) -> np.ndarray:
+        out = np.zeros((n, 5), np.int64)
+        if n:
+            st = N.lib().pzx_evaluate_exact_range(self.handle, table.handle, first, n, out.ctypes.data_as(N.i64p))
+            if not (allow_overflow and st == 4):
+                _check(st, self.handle)
+        return out
+
     def evaluate_device(self, table: DeviceTable, n: int, *, d_assignments: int = 0, first: int = 0,
                         term_begin: int = 0, term_end: int = 2**64 - 1, d_amp: int = 0, d_prob: int = 0,
                         flags: int = PROB_ABS2, stream: int = 0) -> None:
