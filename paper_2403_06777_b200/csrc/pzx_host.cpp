@@ -834,55 +834,61 @@ bool zw_mul_chk(const Zw& x, const Zw& y, Zw& out) {
     return true;
 }
 
-// Per-term integral constants F_t (C'_t * sqrt2^E_t * mu^nLM_t scaled by 2^e_t,
-// e_t reduced while F_t is divisible by 2), the common exponent K, and the
-// power tables of the assignment-dependent factors.
+// Per-term constants C'_t * sqrt2^E_t = F_t * 2^fx_t (F_t in Z[w], divided by
+// 2 while even), nLM_t, and the power tables of the assignment-dependent factors.
 pzx_status build_exact(pzx_ctx* ctx, pzx_table* t) {
     const HostTable& h = t->host;
     const uint64_t m = h.coef.size();
     const uint32_t M = std::max<uint32_t>(h.max_rows, 1);
-    std::vector<int64_t> dt(4 * m, 0);
-    std::vector<int32_t> ex(m, 0);
-    std::vector<uint8_t> bad(m, 0);
-    const Zw s2 = zw(0, 1, 0, -1), mu = zw_generator(K_MU);
-    int32_t K = 0;
+    std::vector<int64_t> ft(4 * m, 0);
+    std::vector<int32_t> fx(m, 0);
+    std::vector<uint32_t> nlm(m, 0);
+    const Zw s2 = zw(0, 1, 0, -1);
     for (uint64_t i = 0; i < m; ++i) {
         const Quad& c = h.coef[i];
         // a + b sqrt2 + i(c + d sqrt2) = a + (b + d) w + c w^2 + (d - b) w^3
         const i128 c1 = i128(c.b) + c.d, c3 = i128(c.d) - c.b;
         bool ok = c1 <= INT64_MAX && c1 >= INT64_MIN && c3 <= INT64_MAX && c3 >= INT64_MIN;
         Zw f = ok ? zw(c.a, int64_t(c1), c.c, int64_t(c3)) : Zw{};
-        for (int k = 0; ok && k < h.e_t[i]; ++k) ok = zw_mul_chk(s2, f, f);
-        for (int k = 0; ok && k < h.nlm_t[i]; ++k) ok = zw_mul_chk(mu, f, f);
-        int32_t e = c.e;
-        if (ok && f.zero()) e = 0;
-        while (ok && e > 0 && ((f.c[0] | f.c[1] | f.c[2] | f.c[3]) & 1) == 0) {
+        int64_t e = -int64_t(c.e) + h.e_t[i] / 2;  // sqrt2^(2q) = 2^q
+        if (ok && (h.e_t[i] & 1)) ok = zw_mul_chk(s2, f, f);
+        while (ok && !f.zero() && ((f.c[0] | f.c[1] | f.c[2] | f.c[3]) & 1) == 0) {
             for (int k = 0; k < 4; ++k) f.c[k] /= 2;
-            --e;
+            ++e;
         }
-        if (!ok) { bad[i] = 1; f = Zw{}; e = 0; }
-        for (int k = 0; k < 4; ++k) dt[4 * i + k] = f.c[k];
-        ex[i] = e;
-        K = std::max(K, e);
+        if (ok && f.zero()) e = 0;
+        ok = ok && e > INT32_MIN / 2 && e < INT32_MAX / 2;
+        for (int k = 0; k < 4; ++k) ft[4 * i + k] = ok ? f.c[k] : 0;
+        fx[i] = ok ? int32_t(e) : INT32_MIN;
+        nlm[i] = uint32_t(h.nlm_t[i]);
     }
-    std::vector<uint8_t> sh(m);
-    for (uint64_t i = 0; i < m; ++i) sh[i] = bad[i] ? 255 : uint8_t(std::min<int32_t>(K - ex[i], 255));
-    std::vector<int64_t> u, pd, p3;
-    Zw x = zw(1, 0, 0, 0);
-    const Zw s2m1 = zw(-1, 1, 0, -1);
-    for (uint32_t s = 0; s <= M && zw_fits62(x); ++s) {
-        for (int k = 0; k < 4; ++k) u.push_back(x.c[k]);
-        if (!zw_mul_chk(x, s2m1, x)) break;
-    }
-    std::vector<Zw> pp, pm;
-    Zw a = zw(1, 0, 0, 0), b = a;
-    const Zw pi = zw_generator(K_PI), pip = zw_generator(K_PIP);
-    for (uint32_t d = 0; d <= M && zw_fits62(a) && zw_fits62(b); ++d) {
-        pp.push_back(a);
-        pm.push_back(b);
-        if (!zw_mul_chk(a, pi, a) || !zw_mul_chk(b, pip, b)) break;
-    }
-    const uint32_t pd_n = uint32_t(pp.size());
+    std::vector<Zw> lam, mu, pp, pm;
+    // g^r / 2^(r/4) (lambda, mu) and g^r (pi, pi'), r = 0, 1, ... while the
+    // entry can be a kernel multiply's x operand
+    auto qpowers = [M](const Zw& g, std::vector<Zw>& out) {
+        Zw x = zw(1, 0, 0, 0);
+        for (uint32_t r = 0; r <= M && zw_fits62(x); ++r) {
+            out.push_back(x);
+            if (!zw_mul_chk(x, g, x)) break;
+            if ((r + 1) % 4 == 0)
+                for (int k = 0; k < 4; ++k) x.c[k] /= 2;  // exact: g^4 = 2 * unit for g = lambda, mu
+        }
+    };
+    auto ipowers = [M](const Zw& g, std::vector<Zw>& out) {
+        Zw x = zw(1, 0, 0, 0);
+        for (uint32_t r = 0; r <= M && zw_fits62(x); ++r) {
+            out.push_back(x);
+            if (!zw_mul_chk(x, g, x)) break;
+        }
+    };
+    qpowers(zw_generator(K_LAMBDA), lam);
+    qpowers(zw_generator(K_MU), mu);
+    ipowers(zw_generator(K_PI), pp);
+    ipowers(zw_generator(K_PIP), pm);
+    const uint32_t pd_n = uint32_t(std::min(pp.size(), pm.size()));
+    std::vector<int64_t> vl, vm, pd, p3;
+    for (const Zw& z : lam) for (int k = 0; k < 4; ++k) vl.push_back(z.c[k]);
+    for (const Zw& z : mu) for (int k = 0; k < 4; ++k) vm.push_back(z.c[k]);
     for (uint32_t i = 0; i < 2 * pd_n - 1; ++i) {
         const int d = int(i) - int(pd_n - 1);
         const Zw& z = d >= 0 ? pp[size_t(d)] : pm[size_t(-d)];
@@ -894,28 +900,33 @@ pzx_status build_exact(pzx_ctx* ctx, pzx_table* t) {
         if (v3 > (int64_t(1) << 61) / 3) break;
         v3 *= 3;
     }
-    // one allocation: dt | u | pd | p3 | sh
-    const size_t o_u = dt.size() * 8, o_pd = o_u + u.size() * 8, o_p3 = o_pd + pd.size() * 8,
-                 o_sh = o_p3 + p3.size() * 8, bytes = o_sh + sh.size() + 16;
+    // one allocation: ft | lam | mu | pd | p3 | fx | nlm
+    const size_t o_l = ft.size() * 8, o_m = o_l + vl.size() * 8, o_pd = o_m + vm.size() * 8,
+                 o_p3 = o_pd + pd.size() * 8, o_fx = o_p3 + p3.size() * 8, o_n = o_fx + fx.size() * 4,
+                 bytes = o_n + nlm.size() * 4 + 16;
     std::vector<unsigned char> blob(bytes, 0);
-    std::memcpy(blob.data(), dt.data(), dt.size() * 8);
-    std::memcpy(blob.data() + o_u, u.data(), u.size() * 8);
+    std::memcpy(blob.data(), ft.data(), ft.size() * 8);
+    std::memcpy(blob.data() + o_l, vl.data(), vl.size() * 8);
+    std::memcpy(blob.data() + o_m, vm.data(), vm.size() * 8);
     std::memcpy(blob.data() + o_pd, pd.data(), pd.size() * 8);
     std::memcpy(blob.data() + o_p3, p3.data(), p3.size() * 8);
-    std::memcpy(blob.data() + o_sh, sh.data(), sh.size());
+    std::memcpy(blob.data() + o_fx, fx.data(), fx.size() * 4);
+    std::memcpy(blob.data() + o_n, nlm.data(), nlm.size() * 4);
     pzx_status st;
     if ((st = cuda_err(ctx, upload_vec(&t->d_exact, blob), "upload exact tables"))) return st;
     const unsigned char* base = static_cast<const unsigned char*>(t->d_exact);
     ExactDev& X = t->exact;
-    X.dt = reinterpret_cast<const int64_t*>(base);
-    X.u = reinterpret_cast<const int64_t*>(base + o_u);
+    X.ft = reinterpret_cast<const int64_t*>(base);
+    X.lam = reinterpret_cast<const int64_t*>(base + o_l);
+    X.mu = reinterpret_cast<const int64_t*>(base + o_m);
     X.pd = reinterpret_cast<const int64_t*>(base + o_pd);
     X.p3 = reinterpret_cast<const int64_t*>(base + o_p3);
-    X.sh = base + o_sh;
-    X.u_n = uint32_t(u.size() / 4);
+    X.fx = reinterpret_cast<const int32_t*>(base + o_fx);
+    X.nlm = reinterpret_cast<const uint32_t*>(base + o_n);
+    X.lam_n = uint32_t(lam.size());
+    X.mu_n = uint32_t(mu.size());
     X.pd_n = pd_n;
     X.p3_n = uint32_t(p3.size());
-    X.K = K;
     return PZX_OK;
 }
 
@@ -939,7 +950,7 @@ pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t 
     uint64_t chunks = blocks >= target ? 1 : (target + blocks - 1) / blocks;
     chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, m));
     chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, t->dev.n_rows / min_chunk_rows()));
-    chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, (uint64_t(1) << 30) / (n * 64 + 1)));
+    chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, (uint64_t(1) << 30) / (n * 80 + 1)));
     chunks = std::min<uint64_t>(chunks, 65535);
     const uint64_t* d_chunks = nullptr;
     if (chunks > 1) {
@@ -947,7 +958,7 @@ pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t 
         chunk_bounds(t->host, 0, m, int(chunks), b);
         if ((st = cuda_err(ctx, grow(&ctx->d_chunks, &ctx->chunks_cap, b.size() * 8), "alloc chunks"))) return st;
         if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_chunks, b.data(), b.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy chunks"))) return st;
-        if ((st = cuda_err(ctx, grow(&ctx->d_partial, &ctx->partial_cap, size_t(chunks) * n * 64), "alloc partials"))) return st;
+        if ((st = cuda_err(ctx, grow(&ctx->d_partial, &ctx->partial_cap, size_t(chunks) * n * 80), "alloc partials"))) return st;
         d_chunks = static_cast<const uint64_t*>(ctx->d_chunks);
     }
     if ((st = cuda_err(ctx, grow(&ctx->d_xout, &ctx->xout_cap, n * 44 + 16), "alloc exact outputs"))) return st;

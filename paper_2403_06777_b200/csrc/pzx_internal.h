@@ -151,18 +151,21 @@ cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_
                                uint32_t* d_out5, cudaStream_t s, uint64_t* launches);
 
 // Exact (integer-ring) evaluation tables, built per table on first use
-// (pzx_evaluate_exact). All Z[w] elements in the power basis (1, w, w^2, w^3).
+// (pzx_evaluate_exact). All Z[w] elements in the power basis (1, w, w^2, w^3);
+// powers of 2 are kept out of the numerators (binary exponents), as the
+// reference's canonical RingQuad does (ring.cpp:20-48).
 struct ExactDev {
-    const int64_t* dt = nullptr;  // [n_terms * 4] F_t = C'_t * 2^e_t * sqrt2^E_t * mu^nLM_t (integral)
-    const uint8_t* sh = nullptr;  // [n_terms] K - e_t (> 62: the term cannot be represented)
-    const int64_t* u = nullptr;   // [u_n * 4] (sqrt2 - 1)^s
-    const int64_t* pd = nullptr;  // [(2 pd_n - 1) * 4] centred at pd_n - 1: pi^d (d >= 0), pi'^-d (d < 0)
-    const int64_t* p3 = nullptr;  // [p3_n] 3^m
-    uint32_t u_n = 0, pd_n = 0, p3_n = 0;  // valid entries (a larger index: OVERFLOW)
-    int32_t K = 0;                // the sum over terms is an element of Z[w] / 2^K
+    const int64_t* ft = nullptr;    // [n_terms * 4] F_t: C'_t * sqrt2^E_t = F_t * 2^fx_t
+    const int32_t* fx = nullptr;    // [n_terms] fx_t (INT32_MIN: the constant is not representable)
+    const uint32_t* nlm = nullptr;  // [n_terms] nLM_t
+    const int64_t* lam = nullptr;   // [lam_n * 4] lambda^r / 2^(r/4)
+    const int64_t* mu = nullptr;    // [mu_n * 4] mu^r / 2^(r/4)
+    const int64_t* pd = nullptr;    // [(2 pd_n - 1) * 4] centred at pd_n - 1: pi^d (d >= 0), pi'^-d (d < 0)
+    const int64_t* p3 = nullptr;    // [p3_n] 3^m
+    uint32_t lam_n = 0, mu_n = 0, pd_n = 0, p3_n = 0;  // valid entries (a larger index: OVERFLOW)
 };
 constexpr int kExactThreads = 128;
-// d_partial: n_chunks * n * 4 int128 when n_chunks > 1; d_pflag: n uint32, zeroed by the caller;
+// d_partial: n_chunks * n * (4 int128 + int32 exponent) when n_chunks > 1; d_pflag: n uint32, zeroed by the caller;
 // d_out: n * 5 int64 {a, b, c, d, exp} (exp = -1: overflow)
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,

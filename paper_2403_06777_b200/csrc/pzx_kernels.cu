@@ -2105,21 +2105,32 @@ cudaError_t launch_debug_codes(const DevTable& t, const uint64_t* d_asg, uint64_
 // pzx_evaluate_exact: the SPEC's integer-ring backend contract (S:444, 486,
 // 493: identical RingQuad outputs, no floats in the kernel path). Each thread
 // owns one assignment and walks the rows of its term chunk (uniform loads,
-// broadcast through L1), accumulating the wide counters of DESIGN.md §2; a
-// term's value is then
-//   F_t * w^(j + 6 s1) * (sqrt2 - 1)^s1 * 3^min(a,b) * pi^(a-b) / 2^e_t
-// evaluated in Z[w] (power basis 1, w, w^2, w^3; w^4 = -1; every factor but the
-// 2^-e_t is an algebraic integer) with int64 operands, int128 products and an
-// int128 sum over terms; the sum is converted to the reference's canonical
+// broadcast through L1), accumulating the wide counters of DESIGN.md §2. With
+// k = nLM_t - s1, mn = min(s1, k), r = |s1 - k| a term's value is
+//   lambda^s1 mu^k = 2^(mn/2 + r/4) w^(6 (mn/2)) (1 - w^2)^(mn % 2) {lambda|mu}^r / 2^(r/4)
+//   value = F_t 2^fx_t * w^j * lambda^s1 mu^k * 3^min(a,b) * pi^(a-b)
+// (lambda mu = 1 - w^2, (1 - w^2)^2 = -2 w^2): an odd-ish Z[w] numerator
+// (power basis 1, w, w^2, w^3; w^4 = -1) times a binary exponent. Numerators
+// are int64 (int128 products, narrowed like the reference's narrow(),
+// ring.cpp:13-18); the sum over terms is an int128 numerator with a running
+// exponent, rescaled like ring_add (ring.cpp:57-70: a spread beyond what the
+// numerator can absorb is an overflow), and converted to the canonical
 // RingQuad (ring.cpp:20-48) once per assignment.
 using i128d = __int128;
 
 __device__ __forceinline__ bool fits_i62(long long v) { return v < (1ll << 62) && v > -(1ll << 62); }
 __device__ __forceinline__ bool fits_i64(i128d v) { return v == i128d((long long)v); }
+__device__ __forceinline__ bool fits_i126(i128d v) { return v < (i128d(1) << 126) && v > -(i128d(1) << 126); }
+__device__ __forceinline__ bool shl_ok(i128d v, int s) {
+    if (v == 0) return true;
+    if (s > 124) return false;
+    const i128d lim = i128d(1) << (126 - s);
+    return v < lim && v > -lim;
+}
 
 // out = x * y in Z[w]; false when x exceeds 62 bits or a coefficient of the
-// product exceeds int64 (the reference's narrow(), ring.cpp:13-18). With
-// |x| < 2^62 and |y| < 2^63 every int128 partial sum stays below 2^127.
+// product exceeds int64. With |x| < 2^62 and |y| < 2^63 every int128 partial
+// sum stays below 2^127.
 __device__ __forceinline__ bool zw_mul_dev(const long long* x, const long long* y, long long* out) {
     i128d t[4] = {0, 0, 0, 0};
     bool ok = true;
@@ -2137,22 +2148,124 @@ __device__ __forceinline__ bool zw_mul_dev(const long long* x, const long long* 
     return ok;
 }
 
-// value = (c0 + c1 w + c2 w^2 + c3 w^3) / 2^K -> canonical RingQuad {a,b,c,d,exp}
-// (w = (sqrt2 + i sqrt2)/2: a = 2c0, b = c1 - c3, c = 2c2, d = c1 + c3 over 2^(K+1));
-// exp = -1 marks an assignment whose value does not fit (PZX_E_OVERFLOW)
-__device__ void exact_store(const i128d* c, int K, bool ok, long long* out) {
-    i128d a = 2 * c[0], b = c[1] - c[3], cc = 2 * c[2], d = c[1] + c[3];
-    long long e = K + 1;
-    if (ok && a == 0 && b == 0 && cc == 0 && d == 0) e = 0;
-    while (ok && e > 0 && ((((long long)a) | ((long long)b) | ((long long)cc) | ((long long)d)) & 1) == 0) {
-        a >>= 1; b >>= 1; cc >>= 1; d >>= 1; --e;  // exact: all even
+// value = (c0 + c1 w + c2 w^2 + c3 w^3) * 2^e, exact; any == false: zero
+struct XAcc {
+    i128d c[4];
+    int e;
+    bool any;
+};
+
+__device__ __forceinline__ void xacc_norm(XAcc& A) {
+    for (;;) {
+        const i128d o = A.c[0] | A.c[1] | A.c[2] | A.c[3];
+        if (o == 0) { A.any = false; return; }
+        const unsigned long long lo = (unsigned long long)o;
+        const int tz = lo ? __ffsll((long long)lo) - 1 : 64;
+        if (tz == 0) return;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) A.c[k] >>= tz;
+        A.e += tz;
     }
-    ok = ok && fits_i64(a) && fits_i64(b) && fits_i64(cc) && fits_i64(d);
+}
+
+__device__ __noinline__ void xacc_add(XAcc& A, const i128d* v, int ev, bool& ok) {
+    if (!A.any) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) A.c[k] = v[k];
+        A.e = ev;
+        A.any = true;
+    } else if (ev >= A.e) {
+        const int sh = ev - A.e;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            ok &= shl_ok(v[k], sh);
+            if (ok) A.c[k] += v[k] << sh;
+        }
+    } else {
+        const int sh = A.e - ev;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            ok &= shl_ok(A.c[k], sh);
+            if (ok) A.c[k] = (A.c[k] << sh) + v[k];
+        }
+        A.e = ev;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ok &= fits_i126(A.c[k]);
+    xacc_norm(A);
+}
+
+// canonical RingQuad {a,b,c,d,exp} of A (w = (sqrt2 + i sqrt2)/2: numerator
+// a = 2c0, b = c1 - c3, c = 2c2, d = c1 + c3 over 2^(1 - e)); exp = -1 marks an
+// assignment whose value does not fit (PZX_E_OVERFLOW)
+__device__ __noinline__ void exact_store(const XAcc& A, bool ok, long long* out) {
+    i128d a = 0, b = 0, cc = 0, d = 0;
+    long long ex = 0;
+    if (ok && A.any) {
+        a = 2 * A.c[0]; b = A.c[1] - A.c[3]; cc = 2 * A.c[2]; d = A.c[1] + A.c[3];
+        ex = 1 - (long long)A.e;
+        if (ex < 0) {
+            ok = shl_ok(a, int(-ex)) && shl_ok(b, int(-ex)) && shl_ok(cc, int(-ex)) && shl_ok(d, int(-ex));
+            if (ok) { a <<= -ex; b <<= -ex; cc <<= -ex; d <<= -ex; }
+            ex = 0;
+        }
+        while (ok && ex > 0 && ((((long long)a) | ((long long)b) | ((long long)cc) | ((long long)d)) & 1) == 0) {
+            a >>= 1; b >>= 1; cc >>= 1; d >>= 1; --ex;  // exact: all even
+        }
+        ok = ok && fits_i64(a) && fits_i64(b) && fits_i64(cc) && fits_i64(d) && ex <= 0x7FFFFFFF;
+    }
     out[0] = ok ? (long long)a : 0;
     out[1] = ok ? (long long)b : 0;
     out[2] = ok ? (long long)cc : 0;
     out[3] = ok ? (long long)d : 0;
-    out[4] = ok ? e : -1;
+    out[4] = ok ? ex : -1;
+}
+
+// one term's value at one assignment: numerator n[4] (int64 in int128) and exponent
+__device__ __forceinline__ bool exact_term(const ExactDev& x, uint64_t term, const Wide& w, i128d* n, int& ev) {
+    const uint32_t nlm = x.nlm[term];
+    const int fx = x.fx[term];
+    if (w.s1 > nlm || fx == INT_MIN) return false;
+    const uint32_t k = nlm - w.s1, mn = min(w.s1, k);
+    const uint32_t r = w.s1 >= k ? w.s1 - k : k - w.s1;
+    const uint32_t m = min(w.a, w.b);
+    const int dd = int(w.a) - int(w.b);
+    const uint32_t ad = uint32_t(dd < 0 ? -dd : dd);
+    const bool use_lam = w.s1 >= k;
+    if ((use_lam ? r >= x.lam_n : r >= x.mu_n) || ad >= x.pd_n || m >= x.p3_n) return false;
+    const int64_t* base = use_lam ? x.lam + 4 * r : x.mu + 4 * r;
+    long long q[4], p[4], t[4], f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        q[i] = base[i];
+        p[i] = x.pd[4 * (int(x.pd_n) - 1 + dd) + i];
+        f[i] = x.ft[4 * term + i];
+    }
+    if (mn & 1u) {  // * (1 - w^2): c - w^2 c = (c0 + c2, c1 + c3, c2 - c0, c3 - c1)
+        const long long c0 = q[0], c1 = q[1], c2 = q[2], c3 = q[3];
+        q[0] = c0 + c2; q[1] = c1 + c3; q[2] = c2 - c0; q[3] = c3 - c1;  // |c| < 2^62: no wrap
+    }
+    bool ok = zw_mul_dev(q, p, t);
+    const long long t3 = x.p3[m];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const i128d v3 = i128d(t[i]) * t3;
+        ok &= fits_i64(v3);
+        t[i] = (long long)v3;
+    }
+    ok &= zw_mul_dev(t, f, p);
+    // w^j: j & 4 negates, j & 3 rotates (w^4 = -1)
+    const uint32_t j = (w.j + 6u * (mn >> 1)) & 7u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int src = (i - int(j & 3u)) & 3;
+        long long v0 = p[src];
+        if (i < int(j & 3u)) v0 = -v0;
+        if (j & 4u) v0 = -v0;
+        n[i] = i128d(v0);
+    }
+    ev = fx + int(mn >> 1) + int(r >> 2);
+    return ok;
 }
 
 template <bool P64>
@@ -2167,7 +2280,9 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
     const uint64_t a = idx < n ? (asg ? asg[idx] : first + idx) : 0;
     const uint64_t tb = n_chunks > 1 ? chunk_terms[blockIdx.y] : 0;
     const uint64_t te = n_chunks > 1 ? chunk_terms[blockIdx.y + 1] : t.n_terms;
-    i128d acc[4] = {0, 0, 0, 0};
+    XAcc A;
+    A.any = false;
+    A.e = 0;
     bool ok = true;
     const uint64_t r1 = tb < te ? t.term_row[te] : 0;
     uint64_t term = tb;
@@ -2176,70 +2291,43 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
         const Row<P64> v = load_row_global<P64>(t, row);
         widen(w, L.codes[((v.code & kCodeMask) >> 2) + (v.p(a) | (v.q(a) << 1))]);
         if (!(v.code & kEndFlag)) continue;
-        if (w.z == 0) {
-            const uint32_t j = (w.j + 6u * w.s1) & 7u;
-            const uint32_t m = min(w.a, w.b);
-            const int dd = int(w.a) - int(w.b);
-            const uint32_t ad = uint32_t(dd < 0 ? -dd : dd);
-            const uint32_t sh = x.sh[term];
-            if (w.s1 >= x.u_n || ad >= x.pd_n || m >= x.p3_n || sh > 62) {
-                ok = false;
-            } else {
-                long long u[4], p[4], q[4], dt[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    u[k] = x.u[4 * w.s1 + k];
-                    p[k] = x.pd[4 * (int(x.pd_n) - 1 + dd) + k];
-                    dt[k] = x.dt[4 * term + k];
-                }
-                ok &= zw_mul_dev(u, p, q);
-                const long long t3 = x.p3[m];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const i128d v3 = i128d(q[k]) * t3;
-                    ok &= fits_i64(v3);
-                    q[k] = (long long)v3;
-                }
-                ok &= zw_mul_dev(q, dt, p);
-                // w^j: j & 4 negates, j & 3 rotates (w^4 = -1)
-                long long r[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int src = (k - int(j & 3u)) & 3;
-                    const long long v0 = p[src];
-                    r[k] = (k < int(j & 3u)) ? -v0 : v0;
-                    if (j & 4u) r[k] = -r[k];
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] += i128d(r[k]) << sh;
-            }
+        if (w.z == 0 && ok) {
+            i128d nv[4];
+            int ev = 0;
+            ok &= exact_term(x, term, w, nv, ev);
+            if (ok) xacc_add(A, nv, ev, ok);
         }
         w = Wide{0, 0, 0, 0, 0};
         ++term;
     }
     if (idx >= n) return;
     if (n_chunks > 1) {
-        i128d* pp = partial + 4 * (uint64_t(blockIdx.y) * n + idx);
+        i128d* pp = partial + 5 * (uint64_t(blockIdx.y) * n + idx);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pp[k] = acc[k];
+        for (int k = 0; k < 4; ++k) pp[k] = A.any ? A.c[k] : 0;
+        pp[4] = A.any ? i128d(A.e) : i128d(INT_MIN);
         if (!ok) pflag[idx] = 1u;
         return;
     }
-    exact_store(acc, x.K, ok, out + 5 * idx);
+    exact_store(A, ok, out + 5 * idx);
 }
 
-// sum of the chunk partials of each assignment (integer: order-free) + canonical store
+// merge of the chunk partials of each assignment (exact, order-free) + canonical store
 __global__ void k_exact_reduce(const i128d* __restrict__ partial, const uint32_t* __restrict__ pflag, int n_chunks,
-                               uint64_t n, int K, long long* __restrict__ out) {
+                               uint64_t n, long long* __restrict__ out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    i128d acc[4] = {0, 0, 0, 0};
-    for (int c = 0; c < n_chunks; ++c) {
-        const i128d* pp = partial + 4 * (uint64_t(c) * n + i);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] += pp[k];
+    XAcc A;
+    A.any = false;
+    A.e = 0;
+    bool ok = pflag[i] == 0u;
+    for (int c = 0; c < n_chunks && ok; ++c) {
+        const i128d* pp = partial + 5 * (uint64_t(c) * n + i);
+        if (pp[4] == i128d(INT_MIN)) continue;
+        const i128d v[4] = {pp[0], pp[1], pp[2], pp[3]};
+        xacc_add(A, v, int(pp[4]), ok);
     }
-    exact_store(acc, K, pflag[i] == 0u, out + 5 * i);
+    exact_store(A, ok, out + 5 * i);
 }
 
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
@@ -2259,7 +2347,7 @@ cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || n_chunks <= 1) return e;
-    k_exact_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(part, d_pflag, n_chunks, n, x.K, o);
+    k_exact_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(part, d_pflag, n_chunks, n, o);
     ++*launches;
     return cudaGetLastError();
 }
