@@ -945,7 +945,7 @@ pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t 
         d_asg = static_cast<const uint64_t*>(ctx->d_asg);
     }
     // grid: >= 8 waves of 4 resident CTAs per SM via row-balanced term chunks
-    const uint64_t blocks = (n + kExactThreads - 1) / kExactThreads;
+    const uint64_t blocks = (n + kExactThreads * kExactK - 1) / (kExactThreads * kExactK);
     const uint64_t target = uint64_t(ctx->n_sm) * 4 * 8;
     uint64_t chunks = blocks >= target ? 1 : (target + blocks - 1) / blocks;
     chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, m));

@@ -165,6 +165,7 @@ struct ExactDev {
     uint32_t lam_n = 0, mu_n = 0, pd_n = 0, p3_n = 0;  // valid entries (a larger index: OVERFLOW)
 };
 constexpr int kExactThreads = 128;
+constexpr int kExactK = 2;  // assignments per thread, exact kernel
 // d_partial: n_chunks * n * (4 int128 + int32 exponent) when n_chunks > 1; d_pflag: n uint32, zeroed by the caller;
 // d_out: n * 5 int64 {a, b, c, d, exp} (exp = -1: overflow)
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,

@@ -2148,6 +2148,28 @@ __device__ __forceinline__ bool zw_mul_dev(const long long* x, const long long* 
     return ok;
 }
 
+// bit length of the largest |coefficient| (|INT64_MIN| counts as 64)
+__device__ __forceinline__ int zw_bits(const long long* x) {
+    unsigned long long o = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o |= (unsigned long long)(x[i] < 0 ? -x[i] : x[i]);
+    return 64 - __clzll((long long)o);
+}
+
+// x * y in Z[w] with int64 arithmetic (caller guarantees no overflow)
+__device__ __forceinline__ void zw_mul64(const long long* x, const long long* y, long long* out) {
+    long long t[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long p = x[i] * y[j];
+            if (i + j < 4) t[i + j] += p; else t[i + j - 4] -= p;
+        }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = t[k];
+}
+
 // value = (c0 + c1 w + c2 w^2 + c3 w^3) * 2^e, exact; any == false: zero
 struct XAcc {
     i128d c[4];
@@ -2168,42 +2190,65 @@ __device__ __forceinline__ void xacc_norm(XAcc& A) {
     }
 }
 
-__device__ __noinline__ void xacc_add(XAcc& A, const i128d* v, int ev, bool& ok) {
+// A += v * 2^ev. The numerator is left unnormalised (normalising costs more
+// than the rare rescue): the exponent only moves down to the smallest one seen,
+// and a shift that would overflow first strips A's factors of 2.
+__device__ __forceinline__ bool xacc_shift_in(XAcc& A, const i128d* v, int ev) {
+    if (ev >= A.e) {
+        const int sh = ev - A.e;
+        bool fit = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fit &= shl_ok(v[k], sh);
+        if (!fit) return false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) A.c[k] += v[k] << sh;
+    } else {
+        const int sh = A.e - ev;
+        bool fit = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fit &= shl_ok(A.c[k], sh);
+        if (!fit) return false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) A.c[k] = (A.c[k] << sh) + v[k];
+        A.e = ev;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void xacc_add(XAcc& A, const i128d* v, int ev, bool& ok) {
     if (!A.any) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) A.c[k] = v[k];
         A.e = ev;
         A.any = true;
-    } else if (ev >= A.e) {
-        const int sh = ev - A.e;
+        return;
+    }
+    if (!xacc_shift_in(A, v, ev)) {
+        xacc_norm(A);
+        if (!A.any) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            ok &= shl_ok(v[k], sh);
-            if (ok) A.c[k] += v[k] << sh;
+            for (int k = 0; k < 4; ++k) A.c[k] = v[k];
+            A.e = ev;
+            A.any = true;
+            return;
         }
-    } else {
-        const int sh = A.e - ev;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            ok &= shl_ok(A.c[k], sh);
-            if (ok) A.c[k] = (A.c[k] << sh) + v[k];
-        }
-        A.e = ev;
+        ok &= xacc_shift_in(A, v, ev);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) ok &= fits_i126(A.c[k]);
-    xacc_norm(A);
 }
 
 // canonical RingQuad {a,b,c,d,exp} of A (w = (sqrt2 + i sqrt2)/2: numerator
 // a = 2c0, b = c1 - c3, c = 2c2, d = c1 + c3 over 2^(1 - e)); exp = -1 marks an
 // assignment whose value does not fit (PZX_E_OVERFLOW)
-__device__ __noinline__ void exact_store(const XAcc& A, bool ok, long long* out) {
+__device__ __forceinline__ void exact_store(const XAcc& A, bool ok, long long* out) {
     i128d a = 0, b = 0, cc = 0, d = 0;
     long long ex = 0;
-    if (ok && A.any) {
-        a = 2 * A.c[0]; b = A.c[1] - A.c[3]; cc = 2 * A.c[2]; d = A.c[1] + A.c[3];
-        ex = 1 - (long long)A.e;
+    XAcc N = A;
+    if (ok && N.any) xacc_norm(N);
+    if (ok && N.any) {
+        a = 2 * N.c[0]; b = N.c[1] - N.c[3]; cc = 2 * N.c[2]; d = N.c[1] + N.c[3];
+        ex = 1 - (long long)N.e;
         if (ex < 0) {
             ok = shl_ok(a, int(-ex)) && shl_ok(b, int(-ex)) && shl_ok(cc, int(-ex)) && shl_ok(d, int(-ex));
             if (ok) { a <<= -ex; b <<= -ex; cc <<= -ex; d <<= -ex; }
@@ -2245,15 +2290,25 @@ __device__ __forceinline__ bool exact_term(const ExactDev& x, uint64_t term, con
         const long long c0 = q[0], c1 = q[1], c2 = q[2], c3 = q[3];
         q[0] = c0 + c2; q[1] = c1 + c3; q[2] = c2 - c0; q[3] = c3 - c1;  // |c| < 2^62: no wrap
     }
-    bool ok = zw_mul_dev(q, p, t);
     const long long t3 = x.p3[m];
+    bool ok = true;
+    // coefficient bound of a Z[w] product: |x y| < 4 |x| |y|, so when the bit
+    // lengths of the four factors sum to <= 58 the whole chain fits int64
+    if (zw_bits(q) + zw_bits(p) + (64 - __clzll(t3)) + zw_bits(f) + 4 <= 62) {
+        zw_mul64(q, p, t);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const i128d v3 = i128d(t[i]) * t3;
-        ok &= fits_i64(v3);
-        t[i] = (long long)v3;
+        for (int i = 0; i < 4; ++i) t[i] *= t3;
+        zw_mul64(t, f, p);
+    } else {
+        ok = zw_mul_dev(q, p, t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const i128d v3 = i128d(t[i]) * t3;
+            ok &= fits_i64(v3);
+            t[i] = (long long)v3;
+        }
+        ok &= zw_mul_dev(t, f, p);
     }
-    ok &= zw_mul_dev(t, f, p);
     // w^j: j & 4 negates, j & 3 rotates (w^4 = -1)
     const uint32_t j = (w.j + 6u * (mn >> 1)) & 7u;
 #pragma unroll
@@ -2268,48 +2323,98 @@ __device__ __forceinline__ bool exact_term(const ExactDev& x, uint64_t term, con
     return ok;
 }
 
+// row consumer of stream_rows: KX assignments per thread, SWAR code words
+// (flushed into wide counters at segment / term ends), the Z[w] epilogue per term
+template <bool P64, int KX>
+struct ExactCons {
+    const SmemLut& L;
+    const ExactDev& x;
+    XAcc* acc_s;  // this thread's KX accumulators in shared memory: kept out of the
+                  // row loop's registers (in registers the compiler copies all
+                  // 32 of them on every row)
+    uint64_t a[KX];
+    uint32_t acc[KX];
+    Wide w[KX];
+    bool ok[KX];
+    uint64_t term;
+    __device__ __forceinline__ ExactCons(const SmemLut& l, const ExactDev& xx) : L(l), x(xx) {}
+    __device__ __forceinline__ void row(const Row<P64>& v) {
+        const uint32_t cb = L.codes_s + (v.code & kCodeMask);
+#pragma unroll
+        for (int k = 0; k < KX; ++k) acc[k] += lds_u32(cb | (v.p(a[k]) << 2) | (v.q(a[k]) << 3));
+    }
+    __device__ __forceinline__ void flush() {
+#pragma unroll
+        for (int k = 0; k < KX; ++k) { widen(w[k], acc[k]); acc[k] = 0; }
+    }
+    __device__ __forceinline__ void close_term() {
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+            if (w[k].z == 0 && ok[k]) {
+                i128d nv[4];
+                int ev = 0;
+                ok[k] &= exact_term(x, term, w[k], nv, ev);
+                if (ok[k]) {
+                    XAcc A = acc_s[k];
+                    xacc_add(A, nv, ev, ok[k]);
+                    acc_s[k] = A;
+                }
+            }
+            w[k] = Wide{0, 0, 0, 0, 0};
+        }
+    }
+    __device__ __forceinline__ void end_term(const double2) {
+#pragma unroll
+        for (int k = 0; k < KX; ++k) { widen(w[k], acc[k]); acc[k] = 0; }
+        close_term();
+        ++term;
+    }
+};
+
+template <bool P64>
+__host__ __device__ constexpr uint32_t exact_acc_offset(uint32_t lut_bytes) {
+    return (smem_lut_offset<P64>() + lut_bytes + 15u) & ~15u;
+}
+
 template <bool P64>
 __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, const ExactDev x, const uint64_t* __restrict__ asg,
                                                       uint64_t first, uint64_t n, const uint64_t* __restrict__ chunk_terms,
                                                       int n_chunks, i128d* __restrict__ partial, uint32_t* __restrict__ pflag,
                                                       long long* __restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLut L = stage_lut(t, smem);
-    __syncthreads();
-    const uint64_t idx = uint64_t(blockIdx.x) * kExactThreads + threadIdx.x;
-    const uint64_t a = idx < n ? (asg ? asg[idx] : first + idx) : 0;
+    const SmemLut L = kernel_prologue(t, smem, smem_lut_offset<P64>());
     const uint64_t tb = n_chunks > 1 ? chunk_terms[blockIdx.y] : 0;
     const uint64_t te = n_chunks > 1 ? chunk_terms[blockIdx.y + 1] : t.n_terms;
-    XAcc A;
-    A.any = false;
-    A.e = 0;
-    bool ok = true;
-    const uint64_t r1 = tb < te ? t.term_row[te] : 0;
-    uint64_t term = tb;
-    Wide w{0, 0, 0, 0, 0};
-    for (uint64_t row = tb < te ? t.term_row[tb] : 0; row < r1; ++row) {
-        const Row<P64> v = load_row_global<P64>(t, row);
-        widen(w, L.codes[((v.code & kCodeMask) >> 2) + (v.p(a) | (v.q(a) << 1))]);
-        if (!(v.code & kEndFlag)) continue;
-        if (w.z == 0 && ok) {
-            i128d nv[4];
-            int ev = 0;
-            ok &= exact_term(x, term, w, nv, ev);
-            if (ok) xacc_add(A, nv, ev, ok);
-        }
-        w = Wide{0, 0, 0, 0, 0};
-        ++term;
-    }
-    if (idx >= n) return;
-    if (n_chunks > 1) {
-        i128d* pp = partial + 5 * (uint64_t(blockIdx.y) * n + idx);
+    ExactCons<P64, kExactK> c(L, x);
+    c.acc_s = reinterpret_cast<XAcc*>(smem + exact_acc_offset<P64>(t.lut_layout.bytes)) + threadIdx.x * kExactK;
+    const uint64_t idx0 = uint64_t(blockIdx.x) * (kExactThreads * kExactK) + threadIdx.x;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pp[k] = A.any ? A.c[k] : 0;
-        pp[4] = A.any ? i128d(A.e) : i128d(INT_MIN);
-        if (!ok) pflag[idx] = 1u;
-        return;
+    for (int k = 0; k < kExactK; ++k) {
+        const uint64_t idx = idx0 + uint64_t(k) * kExactThreads;
+        c.a[k] = idx < n ? (asg ? asg[idx] : first + idx) : 0;
+        c.acc[k] = 0;
+        c.w[k] = Wide{0, 0, 0, 0, 0};
+        c.acc_s[k].any = false;
+        c.acc_s[k].e = 0;
+        c.ok[k] = true;
     }
-    exact_store(A, ok, out + 5 * idx);
+    c.term = tb;
+    if (tb < te) stream_rows<Row<P64>, true>(t, t.rows, t.term_c, tb, te, smem, c);
+#pragma unroll
+    for (int k = 0; k < kExactK; ++k) {
+        const uint64_t idx = idx0 + uint64_t(k) * kExactThreads;
+        if (idx >= n) continue;
+        const XAcc A = c.acc_s[k];
+        if (n_chunks > 1) {
+            i128d* pp = partial + 5 * (uint64_t(blockIdx.y) * n + idx);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pp[i] = A.any ? A.c[i] : 0;
+            pp[4] = A.any ? i128d(A.e) : i128d(INT_MIN);
+            if (!c.ok[k]) pflag[idx] = 1u;
+        } else {
+            exact_store(A, c.ok[k], out + 5 * idx);
+        }
+    }
 }
 
 // merge of the chunk partials of each assignment (exact, order-free) + canonical store
@@ -2334,13 +2439,14 @@ cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
                          int64_t* d_out, cudaStream_t s, uint64_t* launches) {
     if (n == 0) return cudaSuccess;
-    const size_t sm = t.lut_layout.bytes;
+    const size_t sm = (t.p64 ? exact_acc_offset<true>(t.lut_layout.bytes) : exact_acc_offset<false>(t.lut_layout.bytes)) +
+                      size_t(kExactThreads) * kExactK * sizeof(XAcc);
     auto kern = t.p64 ? k_eval_exact<true> : k_eval_exact<false>;
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid(unsigned((n + kExactThreads - 1) / kExactThreads), unsigned(n_chunks));
+    const dim3 grid(unsigned((n + kExactThreads * kExactK - 1) / (kExactThreads * kExactK)), unsigned(n_chunks));
     i128d* part = static_cast<i128d*>(d_partial);
     long long* o = reinterpret_cast<long long*>(d_out);
     kern<<<grid, kExactThreads, sm, s>>>(t, x, d_asg, first, n, d_chunk_terms, n_chunks, part, d_pflag, o);
