@@ -173,6 +173,11 @@ struct Row<false> {
         const uint4 w = *p;
         psi = w.x; phi = w.y; code = w.z; pat = w.w;
     }
+    // from a shared-window address (no generic-to-shared conversion per row)
+    __device__ __forceinline__ void load_s(uint32_t a) {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(psi), "=r"(phi), "=r"(code), "=r"(pat) : "r"(a));
+    }
     __device__ __forceinline__ uint32_t p(uint64_t a) const { return __popc(psi & uint32_t(a)) & 1u; }
     __device__ __forceinline__ uint32_t q(uint64_t a) const { return __popc(phi & uint32_t(a)) & 1u; }
 };
@@ -185,6 +190,13 @@ struct Row<true> {
         const uint4 w = p[0];
         const uint4 x = p[1];
         psi_lo = w.x; psi_hi = w.y; phi_lo = w.z; phi_hi = w.w; code = x.x; pat = x.y;
+    }
+    __device__ __forceinline__ void load_s(uint32_t a) {
+        uint32_t z0, z1;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(psi_lo), "=r"(psi_hi), "=r"(phi_lo), "=r"(phi_hi) : "r"(a));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(code), "=r"(pat), "=r"(z0), "=r"(z1) : "r"(a + 16u));
     }
     __device__ __forceinline__ uint32_t p(uint64_t a) const {
         return __popc((psi_lo & uint32_t(a)) ^ (psi_hi & uint32_t(a >> 32))) & 1u;
@@ -236,13 +248,13 @@ __device__ __forceinline__ void stream_rows(const DevTable& t, const uint4* rows
     double2 C = __ldg(term_c + tb);
     double2 Cn = (tb + 1 < te) ? __ldg(term_c + tb + 1) : make_double2(0.0, 0.0);
     for (uint32_t i = 0; i < ntiles; ++i) {
-        const uint4* buf = tiles + (i & 1) * kTileRows * RW;
+        const uint32_t sbuf = smem_u32(tiles) + (i & 1) * uint32_t(kTileRows) * RW * 16u;
         mbar_wait(&bars[i & 1], (i >> 1) & 1u);
         const uint64_t rem = R1 - R0 - uint64_t(i) * kTileRows;
         const uint32_t n = rem < uint64_t(kTileRows) ? uint32_t(rem) : uint32_t(kTileRows);
         for (uint32_t k = 0; k < n; ++k) {
             RowT row;
-            row.load(buf + k * RW);
+            row.load_s(sbuf + k * RW * 16u);
             cons.row(row);
             if (row.code & kEndFlag) {
                 cons.end_term(C);
@@ -2175,6 +2187,7 @@ struct XAcc {
     i128d c[4];
     int e;
     bool any;
+    bool ok;  // (exact kernel's shared-memory slots) no overflow so far
 };
 
 __device__ __forceinline__ void xacc_norm(XAcc& A) {
@@ -2335,7 +2348,6 @@ struct ExactCons {
     uint64_t a[KX];
     uint32_t acc[KX];
     Wide w[KX];
-    bool ok[KX];
     uint64_t term;
     __device__ __forceinline__ ExactCons(const SmemLut& l, const ExactDev& xx) : L(l), x(xx) {}
     __device__ __forceinline__ void row(const Row<P64>& v) {
@@ -2350,15 +2362,16 @@ struct ExactCons {
     __device__ __forceinline__ void close_term() {
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
-            if (w[k].z == 0 && ok[k]) {
+            if (w[k].z == 0 && acc_s[k].ok) {
                 i128d nv[4];
                 int ev = 0;
-                ok[k] &= exact_term(x, term, w[k], nv, ev);
-                if (ok[k]) {
+                bool ok = exact_term(x, term, w[k], nv, ev);
+                if (ok) {
                     XAcc A = acc_s[k];
-                    xacc_add(A, nv, ev, ok[k]);
+                    xacc_add(A, nv, ev, ok);
                     acc_s[k] = A;
                 }
+                acc_s[k].ok = ok;
             }
             w[k] = Wide{0, 0, 0, 0, 0};
         }
@@ -2395,8 +2408,8 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
         c.acc[k] = 0;
         c.w[k] = Wide{0, 0, 0, 0, 0};
         c.acc_s[k].any = false;
+        c.acc_s[k].ok = true;
         c.acc_s[k].e = 0;
-        c.ok[k] = true;
     }
     c.term = tb;
     if (tb < te) stream_rows<Row<P64>, true>(t, t.rows, t.term_c, tb, te, smem, c);
@@ -2410,9 +2423,9 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
 #pragma unroll
             for (int i = 0; i < 4; ++i) pp[i] = A.any ? A.c[i] : 0;
             pp[4] = A.any ? i128d(A.e) : i128d(INT_MIN);
-            if (!c.ok[k]) pflag[idx] = 1u;
+            if (!A.ok) pflag[idx] = 1u;
         } else {
-            exact_store(A, c.ok[k], out + 5 * idx);
+            exact_store(A, A.ok, out + 5 * idx);
         }
     }
 }
