@@ -178,6 +178,18 @@ pzx_status pzx_evaluate_exact(pzx_ctx* ctx, const pzx_table* t, const uint64_t* 
                               int64_t* out);
 pzx_status pzx_evaluate_exact_range(pzx_ctx* ctx, const pzx_table* t, uint64_t first, uint64_t n, int64_t* out);
 
+
+/* Exact combine of the term split: out[i] = sum over r < n_parts of
+ * parts[r][i], every entry a canonical RingQuad {a, b, c, d, exp} (int64 [n_parts][n][5],
+ * part-major, e.g. the all-gathered pzx_evaluate_exact results of disjoint term
+ * ranges); replaces the ring_add fold over terms (ring.cpp:57-70) across ranks.
+ * The result is canonical and order-free. An input with exp = -1 (overflowed)
+ * or a sum outside int64 gives exp = -1 and PZX_E_OVERFLOW (host form). The
+ * _device form is asynchronous on `stream` (NULL = default) and reports
+ * overflow only through exp = -1. */
+pzx_status pzx_ringquad_sum(pzx_ctx* ctx, const int64_t* parts, uint32_t n_parts, uint64_t n, int64_t* out);
+pzx_status pzx_ringquad_sum_device(pzx_ctx* ctx, const int64_t* d_parts, uint32_t n_parts, uint64_t n,
+                                   int64_t* d_out, void* stream);
 /* Asynchronous DEVICE-pointer variants on `stream` (used as given, NULL = default stream):
  * d_assignments may be NULL for the enumerated batch starting at `first`.
  * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)

@@ -22,7 +22,7 @@ EXPORTS = (
     "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
     "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
     "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex", "pzx_evaluate_exact",
-    "pzx_evaluate_exact_range",
+    "pzx_evaluate_exact_range", "pzx_ringquad_sum", "pzx_ringquad_sum_device",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -92,6 +92,8 @@ def lib() -> C.CDLL:
     L.pzx_evaluate_range.argtypes = [vp, vp, C.c_uint64, C.c_uint64, dblp, dblp, C.c_uint32]
     L.pzx_evaluate_exact.argtypes = [vp, vp, u64p, C.c_uint64, i64p]
     L.pzx_evaluate_exact_range.argtypes = [vp, vp, C.c_uint64, C.c_uint64, i64p]
+    L.pzx_ringquad_sum.argtypes = [vp, i64p, C.c_uint32, C.c_uint64, i64p]
+    L.pzx_ringquad_sum_device.argtypes = [vp, vp, C.c_uint32, C.c_uint64, vp, vp]
     L.pzx_evaluate_device.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                       vp, vp, C.c_uint32, vp]
     L.pzx_amp_to_prob_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]

@@ -1419,6 +1419,37 @@ pzx_status pzx_evaluate_exact_range(pzx_ctx* ctx, const pzx_table* t, uint64_t f
     return exact_host(ctx, const_cast<pzx_table*>(t), nullptr, first, n, out);
 }
 
+pzx_status pzx_ringquad_sum_device(pzx_ctx* ctx, const int64_t* d_parts, uint32_t n_parts, uint64_t n,
+                                   int64_t* d_out, void* stream) {
+    if (!ctx || (n && (!d_out || (n_parts && !d_parts)))) return PZX_E_INVALID;
+    if (n == 0) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    return cuda_err(ctx, launch_ringquad_sum(d_parts, n_parts, n, d_out, static_cast<cudaStream_t>(stream),
+                                             &ctx->launches), "ringquad_sum");
+}
+
+pzx_status pzx_ringquad_sum(pzx_ctx* ctx, const int64_t* parts, uint32_t n_parts, uint64_t n, int64_t* out) {
+    if (!ctx || (n && (!out || (n_parts && !parts)))) return PZX_E_INVALID;
+    if (n == 0) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    const size_t in_b = size_t(n_parts) * n * 40, out_b = size_t(n) * 40;
+    void* d = nullptr;
+    if ((st = cuda_err(ctx, cudaMallocAsync(&d, in_b + out_b, ctx->stream), "alloc ringquad_sum"))) return st;
+    int64_t* d_in = static_cast<int64_t*>(d);
+    int64_t* d_out = d_in + size_t(n_parts) * n * 5;
+    st = cuda_err(ctx, cudaMemcpyAsync(d_in, parts, in_b, cudaMemcpyHostToDevice, ctx->stream), "H2D ringquad parts");
+    if (!st) st = pzx_ringquad_sum_device(ctx, d_in, n_parts, n, d_out, ctx->stream);
+    if (!st) st = cuda_err(ctx, cudaMemcpyAsync(out, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream), "D2H ringquad sum");
+    cudaFreeAsync(d, ctx->stream);
+    if (!st) st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "ringquad_sum");
+    if (st) return st;
+    for (uint64_t i = 0; i < n; ++i)
+        if (out[5 * i + 4] < 0) return set_err(ctx, PZX_E_OVERFLOW, "ringquad_sum: ring coefficient out of 64-bit range");
+    return PZX_OK;
+}
+
 // Marginal summing: out[i] = sum over b < 2^m of prob(fixed[i] | b),
 // prob = |amp|^2 (default) or Re(amp) (PZX_PROB_REAL). The don't-care outputs
 // are the low m parameters. Large groups run as enumerated ranges (bit-sliced

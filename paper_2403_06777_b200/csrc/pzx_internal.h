@@ -172,6 +172,10 @@ cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
                          int64_t* d_out, cudaStream_t s, uint64_t* launches);
 
+// d_parts: g * n canonical RingQuads (rank-major), d_out: n * 5 int64 (exp = -1: overflow)
+cudaError_t launch_ringquad_sum(const int64_t* d_parts, uint32_t g, uint64_t n, int64_t* d_out, cudaStream_t s,
+                                uint64_t* launches);
+
 constexpr int kThreads = 256;
 constexpr int kGeneralK = 4;  // assignments per thread, general kernel
 

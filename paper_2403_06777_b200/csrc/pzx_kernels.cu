@@ -2448,6 +2448,39 @@ __global__ void k_exact_reduce(const i128d* __restrict__ partial, const uint32_t
     exact_store(A, ok, out + 5 * i);
 }
 
+// exact sum of G canonical RingQuads per assignment (the term split's combine,
+// partials of disjoint term ranges, all-gathered rank-major
+// [G][n][5]). (a + b sqrt2 + i(c + d sqrt2)) 2^-exp in the w power basis is
+// (a, b + d, c, d - b) 2^-exp (sqrt2 = w - w^3, i sqrt2 = w + w^3); the sum is
+// exact, so every order gives the one canonical result (ring.hpp:15-16).
+// exp = -1 in any part (an overflowed partial) marks the output overflowed.
+__global__ void k_ringquad_sum(const long long* __restrict__ parts, uint32_t g, uint64_t n, long long* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    XAcc A;
+    A.any = false;
+    A.e = 0;
+    bool ok = true;
+    for (uint32_t r = 0; r < g && ok; ++r) {
+        const long long* q = parts + 5 * (uint64_t(r) * n + i);
+        const long long a = q[0], b = q[1], c = q[2], d = q[3], ex = q[4];
+        if (ex < 0 || ex > 0x7FFFFFFF) { ok = false; break; }
+        if ((a | b | c | d) == 0) continue;
+        const i128d v[4] = {i128d(a), i128d(b) + d, i128d(c), i128d(d) - b};
+        xacc_add(A, v, -int(ex), ok);
+    }
+    exact_store(A, ok, out + 5 * i);
+}
+
+cudaError_t launch_ringquad_sum(const int64_t* d_parts, uint32_t g, uint64_t n, int64_t* d_out, cudaStream_t s,
+                                uint64_t* launches) {
+    if (n == 0) return cudaSuccess;
+    k_ringquad_sum<<<unsigned((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const long long*>(d_parts), g, n,
+                                                             reinterpret_cast<long long*>(d_out));
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
                          int64_t* d_out, cudaStream_t s, uint64_t* launches) {

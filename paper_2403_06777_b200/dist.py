@@ -76,6 +76,31 @@ def evaluate_term_split(partial_fn: Callable[[int, int], torch.Tensor], term_row
     return combine_partials(partial_fn(t0, t1), group, deterministic)
 
 
+def combine_exact_partials(partial: torch.Tensor, sum_fn: Callable[[torch.Tensor], torch.Tensor],
+                           group=None) -> torch.Tensor:
+    """Exact term-split combine ("exact: ncclAllGather + a rank-ordered
+    sum"): every rank's canonical RingQuads (int64 [n, 5]) are all-gathered
+    rank-major into [world, n, 5] and summed exactly by ``sum_fn`` (on B200s
+    ``gpu_exact_sum_fn``: the ``pzx_ringquad_sum_device`` kernel). An exact sum
+    has one canonical value, so the result is identical for every world size."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return partial
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(partial) for _ in range(world)]
+    dist.all_gather(parts, partial.contiguous(), group=group)
+    return sum_fn(torch.stack(parts))
+
+
+def evaluate_term_split_exact(partial_fn: Callable[[int, int], torch.Tensor], term_row_offset: np.ndarray,
+                              sum_fn: Callable[[torch.Tensor], torch.Tensor], group=None) -> torch.Tensor:
+    """Exact term split: partial_fn(t0, t1) -> canonical RingQuads [n, 5] of this
+    rank's row-balanced term range, combined by combine_exact_partials."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    t0, t1 = term_ranges(term_row_offset, world)[rank]
+    return combine_exact_partials(partial_fn(t0, t1), sum_fn, group)
+
+
 def gather_shards(local: torch.Tensor, n_total: int, width: int = 1, group=None) -> torch.Tensor:
     """All-gather contiguous per-rank result slices (`width` values per assignment).
     Output plumbing after the evaluation, not part of the hot path."""
@@ -103,5 +128,35 @@ def gpu_partial_fn(ctx, expr, n: int, first: int = 0, d_words: torch.Tensor | No
                                 first=first, d_amp=out.data_ptr(), stream=torch.cuda.current_stream(dev).cuda_stream)
             torch.cuda.synchronize(dev)
             table.free()
+        return out
+    return fn
+
+
+def gpu_exact_partial_fn(ctx, expr, words: np.ndarray, device: int | None = None):
+    """Exact partial_fn backed by the CUDA evaluator: canonical RingQuads of this
+    rank's term slice at every word, as an int64 [n, 5] device tensor."""
+    def fn(t0: int, t1: int) -> torch.Tensor:
+        dev = torch.device("cuda", ctx.device if device is None else device)
+        if t1 <= t0:
+            return torch.zeros((len(words), 5), dtype=torch.int64, device=dev)
+        table = ctx.compile_bit_table(expr.slice_terms(t0, t1))
+        try:
+            out = ctx.evaluate_exact(table, words, allow_overflow=True)
+        finally:
+            table.free()
+        return torch.from_numpy(out).to(dev)
+    return fn
+
+
+def gpu_exact_sum_fn(ctx, device: int | None = None):
+    """sum_fn for combine_exact_partials: the pzx_ringquad_sum_device kernel on
+    the gathered [world, n, 5] device tensor (exp = -1 marks overflow)."""
+    def fn(parts: torch.Tensor) -> torch.Tensor:
+        dev = torch.device("cuda", ctx.device if device is None else device)
+        parts = parts.to(dev).contiguous()
+        out = torch.empty(parts.shape[1:], dtype=torch.int64, device=dev)
+        ctx.ringquad_sum_device(parts.data_ptr(), parts.shape[0], parts.shape[1], out.data_ptr(),
+                                stream=torch.cuda.current_stream(dev).cuda_stream)
+        torch.cuda.synchronize(dev)
         return out
     return fn

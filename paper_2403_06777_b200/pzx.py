@@ -450,6 +450,26 @@ class Context:
                 _check(st, self.handle)
         return out
 
+    def ringquad_sum(self, parts, *, allow_overflow: bool = False) -> np.ndarray:
+        """Exact sum over axis 0 of canonical RingQuads, int64 [G, n, 5] -> [n, 5]
+        (the term split's combine; order-free, canonical).
+        OverflowError when a sum leaves int64 (allow_overflow: exp = -1 there)."""
+        p = np.ascontiguousarray(np.asarray(parts, dtype=np.int64))
+        if p.ndim != 3 or p.shape[2] != 5:
+            raise ValueError("ringquad_sum: parts must be int64 [G, n, 5]")
+        out = np.zeros((p.shape[1], 5), np.int64)
+        if p.shape[1]:
+            st = N.lib().pzx_ringquad_sum(self.handle, p.ctypes.data_as(N.i64p), p.shape[0], p.shape[1],
+                                          out.ctypes.data_as(N.i64p))
+            if not (allow_overflow and st == 4):
+                _check(st, self.handle)
+        return out
+
+    def ringquad_sum_device(self, d_parts: int, n_parts: int, n: int, d_out: int, stream: int = 0) -> None:
+        """Async device-pointer form of ringquad_sum (raw CUDA pointers as ints)."""
+        _check(N.lib().pzx_ringquad_sum_device(self.handle, d_parts or None, n_parts, n, d_out or None,
+                                               stream or None), self.handle)
+
     def evaluate_device(self, table: DeviceTable, n: int, *, d_assignments: int = 0, first: int = 0,
                         term_begin: int = 0, term_end: int = 2**64 - 1, d_amp: int = 0, d_prob: int = 0,
                         flags: int = PROB_ABS2, stream: int = 0) -> None:

@@ -74,6 +74,59 @@ def test_term_split_and_assignment_shards_world2():
     assert np.array_equal(gathered, full)
 
 
+def _oracle_ring_sum(O):
+    def fn(parts):
+        p = parts.numpy()
+        out = np.zeros(p.shape[1:], np.int64)
+        for i in range(p.shape[1]):
+            acc = tuple(int(v) for v in p[0, i])
+            for r in range(1, p.shape[0]):
+                acc = O.ring_add(acc, tuple(int(v) for v in p[r, i]))
+            out[i] = acc[:5]
+        return torch.from_numpy(out)
+    return fn
+
+
+def _exact_worker(rank, world, port, q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(os.path.dirname(here), "oracle"))
+    import oracle_py as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        e = synth.generate(9, 40, 2, 20, 7)
+        words = np.arange(300, dtype=np.uint64)
+
+        def partial_fn(t0, t1):
+            if t1 <= t0:
+                return torch.zeros((len(words), 5), dtype=torch.int64)
+            return torch.from_numpy(O.eval_batch(e.slice_terms(t0, t1), words, 2)[0])
+
+        got = D.evaluate_term_split_exact(partial_fn, e.term_offset, _oracle_ring_sum(O))
+        if rank == 0:
+            q.put((got.numpy(), O.eval_batch(e, words, 2)[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exact_term_split_world(world):
+    """Exact term split: all-gathered canonical partials summed exactly equal the
+    whole table's canonical values (bit-identical, any world size)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exact_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, full = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(got, full)
+
+
 def test_term_ranges_balance_rows():
     off = np.concatenate([[0], np.cumsum(np.random.default_rng(0).integers(1, 64, 10000))])
     for world in (1, 2, 3, 8):

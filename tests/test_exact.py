@@ -151,3 +151,59 @@ def test_exact_full_size_tables_vs_float_kernels(ctx, cid):
     assert np.array_equal(ctx.evaluate_exact(t, words[::-1]), ex[::-1])
     # oracle spot check at full size
     assert np.array_equal(ex[:4], O.eval_batch(e, words[:4], 8)[0])
+
+
+@pytest.mark.parametrize("G", [1, 2, 5])
+def test_ringquad_sum_term_split(ctx, G):
+    """pzx_ringquad_sum: exact partials of G row-balanced term ranges (the term
+    split) summed on the device equal the whole table's values."""
+    from paper_2403_06777_b200 import dist as D
+    e = synth.generate(16, 300, 2, 40, 11 + G)
+    words = np.random.default_rng(G).integers(0, 1 << 16, 2000, dtype=np.uint64)
+    full = ctx.evaluate_exact(ctx.compile_bit_table(e), words)
+    parts = []
+    for t0, t1 in D.term_ranges(e.term_offset, G):
+        t = ctx.compile_bit_table(e.slice_terms(t0, t1))
+        parts.append(ctx.evaluate_exact(t, words))
+        t.free()
+    got = ctx.ringquad_sum(np.stack(parts))
+    assert np.array_equal(got, full)
+    assert np.array_equal(got, exact_oracle(e, words))
+    # the device-pointer path used by dist.gpu_exact_sum_fn
+    import torch
+    dev = torch.from_numpy(np.stack(parts)).cuda()
+    got_d = D.gpu_exact_sum_fn(ctx)(dev).cpu().numpy()
+    assert np.array_equal(got_d, full)
+
+
+def test_ringquad_sum_vs_oracle_ring_add(ctx):
+    """Random canonical RingQuads (mixed exponents, cancellations, zeros): the
+    device sum equals the reference's ring_add fold (ring.cpp:57-70)."""
+    rng = np.random.default_rng(5)
+    G, n = 4, 3000
+    parts = np.zeros((G, n, 5), np.int64)
+    for r in range(G):
+        for i in range(n):
+            v = rng.integers(-2**20, 2**20, 4) if rng.random() < 0.8 else np.zeros(4, np.int64)
+            parts[r, i] = O.make(*(int(x) for x in v), int(rng.integers(0, 30)))[:5]
+    parts[1, :100, :4] = -parts[0, :100, :4]  # exact cancellation -> canonical zero
+    parts[1, :100, 4] = parts[0, :100, 4]
+    parts[2:, :100] = 0
+    got = ctx.ringquad_sum(parts)
+    for i in range(n):
+        acc = tuple(int(x) for x in parts[0, i])
+        for r in range(1, G):
+            acc = O.ring_add(acc, tuple(int(x) for x in parts[r, i]))
+        assert tuple(got[i]) == acc[:5], i
+    assert not got[:100].any()
+
+
+def test_ringquad_sum_overflow_is_explicit(ctx):
+    big = np.array([[[2**62, 0, 0, 0, 0]], [[2**62, 0, 0, 0, 0]]], np.int64)
+    with pytest.raises(P.OverflowError):
+        ctx.ringquad_sum(big)
+    got = ctx.ringquad_sum(big, allow_overflow=True)
+    assert got[0, 4] == -1
+    flagged = np.array([[[1, 0, 0, 0, 0]], [[0, 0, 0, 0, -1]]], np.int64)  # an overflowed partial
+    assert ctx.ringquad_sum(flagged, allow_overflow=True)[0, 4] == -1
+    assert np.array_equal(ctx.ringquad_sum(np.zeros((3, 0, 5), np.int64)), np.zeros((0, 5), np.int64))
