@@ -945,7 +945,9 @@ pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t 
         d_asg = static_cast<const uint64_t*>(ctx->d_asg);
     }
     // grid: >= 8 waves of 4 resident CTAs per SM via row-balanced term chunks
-    const uint64_t blocks = (n + kExactThreads * kExactK - 1) / (kExactThreads * kExactK);
+    const char* ek = std::getenv("PZX_EXACT_K");  // tuning knob: assignments per thread
+    const int kx = ek && (std::atoi(ek) == 1 || std::atoi(ek) == 4) ? std::atoi(ek) : kExactK;
+    const uint64_t blocks = (n + kExactThreads * kx - 1) / (kExactThreads * kx);
     const uint64_t target = uint64_t(ctx->n_sm) * 4 * 8;
     uint64_t chunks = blocks >= target ? 1 : (target + blocks - 1) / blocks;
     chunks = std::min<uint64_t>(chunks, std::max<uint64_t>(1, m));
@@ -966,7 +968,7 @@ pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t 
     uint32_t* d_flag = reinterpret_cast<uint32_t*>(d_out + 5 * n);
     if ((st = cuda_err(ctx, cudaMemsetAsync(d_flag, 0, n * 4, ctx->stream), "clear flags"))) return st;
     if ((st = cuda_err(ctx, launch_exact(t->dev, t->exact, d_asg, first, n, d_chunks, int(chunks), ctx->d_partial, d_flag,
-                                         d_out, ctx->stream, &ctx->launches), "exact kernel"))) return st;
+                                         d_out, ctx->stream, &ctx->launches, kx), "exact kernel"))) return st;
     if ((st = cuda_err(ctx, cudaMemcpyAsync(out, d_out, n * 40, cudaMemcpyDeviceToHost, ctx->stream), "D2H exact"))) return st;
     if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "evaluate_exact"))) return st;
     for (uint64_t i = 0; i < n; ++i)

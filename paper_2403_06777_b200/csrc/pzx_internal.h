@@ -165,12 +165,12 @@ struct ExactDev {
     uint32_t lam_n = 0, mu_n = 0, pd_n = 0, p3_n = 0;  // valid entries (a larger index: OVERFLOW)
 };
 constexpr int kExactThreads = 128;
-constexpr int kExactK = 2;  // assignments per thread, exact kernel
+constexpr int kExactK = 2;  // assignments per thread, exact kernel (default; 1, 2 or 4 via PZX_EXACT_K)
 // d_partial: n_chunks * n * (4 int128 + int32 exponent) when n_chunks > 1; d_pflag: n uint32, zeroed by the caller;
 // d_out: n * 5 int64 {a, b, c, d, exp} (exp = -1: overflow)
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
-                         int64_t* d_out, cudaStream_t s, uint64_t* launches);
+                         int64_t* d_out, cudaStream_t s, uint64_t* launches, int kx);
 
 // d_parts: g * n canonical RingQuads (rank-major), d_out: n * 5 int64 (exp = -1: overflow)
 cudaError_t launch_ringquad_sum(const int64_t* d_parts, uint32_t g, uint64_t n, int64_t* d_out, cudaStream_t s,

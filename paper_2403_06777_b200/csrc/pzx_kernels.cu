@@ -2389,7 +2389,7 @@ __host__ __device__ constexpr uint32_t exact_acc_offset(uint32_t lut_bytes) {
     return (smem_lut_offset<P64>() + lut_bytes + 15u) & ~15u;
 }
 
-template <bool P64>
+template <bool P64, int KX>
 __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, const ExactDev x, const uint64_t* __restrict__ asg,
                                                       uint64_t first, uint64_t n, const uint64_t* __restrict__ chunk_terms,
                                                       int n_chunks, i128d* __restrict__ partial, uint32_t* __restrict__ pflag,
@@ -2398,11 +2398,11 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
     const SmemLut L = kernel_prologue(t, smem, smem_lut_offset<P64>());
     const uint64_t tb = n_chunks > 1 ? chunk_terms[blockIdx.y] : 0;
     const uint64_t te = n_chunks > 1 ? chunk_terms[blockIdx.y + 1] : t.n_terms;
-    ExactCons<P64, kExactK> c(L, x);
-    c.acc_s = reinterpret_cast<XAcc*>(smem + exact_acc_offset<P64>(t.lut_layout.bytes)) + threadIdx.x * kExactK;
-    const uint64_t idx0 = uint64_t(blockIdx.x) * (kExactThreads * kExactK) + threadIdx.x;
+    ExactCons<P64, KX> c(L, x);
+    c.acc_s = reinterpret_cast<XAcc*>(smem + exact_acc_offset<P64>(t.lut_layout.bytes)) + threadIdx.x * KX;
+    const uint64_t idx0 = uint64_t(blockIdx.x) * (kExactThreads * KX) + threadIdx.x;
 #pragma unroll
-    for (int k = 0; k < kExactK; ++k) {
+    for (int k = 0; k < KX; ++k) {
         const uint64_t idx = idx0 + uint64_t(k) * kExactThreads;
         c.a[k] = idx < n ? (asg ? asg[idx] : first + idx) : 0;
         c.acc[k] = 0;
@@ -2414,7 +2414,7 @@ __global__ void __launch_bounds__(kExactThreads) k_eval_exact(const DevTable t, 
     c.term = tb;
     if (tb < te) stream_rows<Row<P64>, true>(t, t.rows, t.term_c, tb, te, smem, c);
 #pragma unroll
-    for (int k = 0; k < kExactK; ++k) {
+    for (int k = 0; k < KX; ++k) {
         const uint64_t idx = idx0 + uint64_t(k) * kExactThreads;
         if (idx >= n) continue;
         const XAcc A = c.acc_s[k];
@@ -2483,16 +2483,18 @@ cudaError_t launch_ringquad_sum(const int64_t* d_parts, uint32_t g, uint64_t n, 
 
 cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d_asg, uint64_t first, uint64_t n,
                          const uint64_t* d_chunk_terms, int n_chunks, void* d_partial, uint32_t* d_pflag,
-                         int64_t* d_out, cudaStream_t s, uint64_t* launches) {
+                         int64_t* d_out, cudaStream_t s, uint64_t* launches, int kx) {
     if (n == 0) return cudaSuccess;
     const size_t sm = (t.p64 ? exact_acc_offset<true>(t.lut_layout.bytes) : exact_acc_offset<false>(t.lut_layout.bytes)) +
-                      size_t(kExactThreads) * kExactK * sizeof(XAcc);
-    auto kern = t.p64 ? k_eval_exact<true> : k_eval_exact<false>;
+                      size_t(kExactThreads) * kx * sizeof(XAcc);
+    auto kern = kx == 4 ? (t.p64 ? k_eval_exact<true, 4> : k_eval_exact<false, 4>)
+              : kx == 1 ? (t.p64 ? k_eval_exact<true, 1> : k_eval_exact<false, 1>)
+                        : (t.p64 ? k_eval_exact<true, 2> : k_eval_exact<false, 2>);
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid(unsigned((n + kExactThreads * kExactK - 1) / (kExactThreads * kExactK)), unsigned(n_chunks));
+    const dim3 grid(unsigned((n + kExactThreads * kx - 1) / (kExactThreads * kx)), unsigned(n_chunks));
     i128d* part = static_cast<i128d*>(d_partial);
     long long* o = reinterpret_cast<long long*>(d_out);
     kern<<<grid, kExactThreads, sm, s>>>(t, x, d_asg, first, n, d_chunk_terms, n_chunks, part, d_pflag, o);
