@@ -691,6 +691,27 @@ void chunk_bounds(const HostTable& h, uint64_t tb, uint64_t te, int chunks, std:
     }
 }
 
+// grid waves the term-chunk policy aims for (tuning knob PZX_WAVES). Measured
+// on C2 / C3 (profiles/r01/waves*.log): 8 -> 64 waves is +9 % / +5 % (shorter
+// term chunks per CTA even out the per-CTA work), while the warp-chunk kernel
+// (C4) loses 35 % with more chunks and keeps 8.
+int grid_waves(bool warp_chunks) {
+    static const int v = [] {
+        const char* e = std::getenv("PZX_WAVES");
+        return e ? std::max(1, std::atoi(e)) : 64;
+    }();
+    return warp_chunks ? 8 : v;
+}
+
+// chunk-partial scratch bound (bytes); tuning knob PZX_PARTIAL_MIB
+uint64_t partial_cap() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("PZX_PARTIAL_MIB");
+        return (e ? std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) : uint64_t(2048)) << 20;
+    }();
+    return v;
+}
+
 uint64_t min_chunk_rows() {
     static const uint64_t v = [] {
         const char* e = std::getenv("PZX_MIN_CHUNK_ROWS");
@@ -771,13 +792,13 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const int ablocks = grid_assign_blocks(t->dev, r, kc);
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
-    constexpr int kWaves = 8;
+    const int kWaves = grid_waves(kc == KC_SLICEWC);
     const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc, slice_threads(r), r.sorted_groups);
     const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
         uint64_t c = (uint64_t(target) + ablocks - 1) / ablocks;
         c = std::min<uint64_t>(c, kc == KC_SLICEWC ? std::max<uint64_t>(1, nterms / kWarpChunksHost) : nterms);
-        c = std::min<uint64_t>(c, std::max<uint64_t>(1, (uint64_t(1) << 30) / (r.n * 16 + 1)));
+        c = std::min<uint64_t>(c, std::max<uint64_t>(1, partial_cap() / (r.n * 16 + 1)));
         // small tables: a chunk below kMinChunkRows rows costs more in per-CTA setup
         // (table staging, TMEM allocation, the partial it writes) than it saves
         const uint64_t total_rows = t->host.term_row.size() > r.term_end
@@ -791,7 +812,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         if (total % wave) {
             const uint64_t want = (total / wave + 1) * wave;
             const uint64_t c2 = (want + ablocks - 1) / ablocks;
-            if (c2 <= nterms && c2 <= 65535 && c2 * (r.n * 16) <= (uint64_t(1) << 30)) chunks = int(c2);
+            if (c2 <= nterms && c2 <= 65535 && c2 * (r.n * 16) <= partial_cap()) chunks = int(c2);
         }
     }
     if (kc == KC_SLICEWC) chunks *= kWarpChunksHost;  // 4 warp chunks per CTA row, always partials
