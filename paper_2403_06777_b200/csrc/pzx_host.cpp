@@ -691,10 +691,12 @@ void chunk_bounds(const HostTable& h, uint64_t tb, uint64_t te, int chunks, std:
     }
 }
 
-// grid waves the term-chunk policy aims for (tuning knob PZX_WAVES). Measured
-// on C2 / C3 (profiles/r01/waves*.log): 8 -> 64 waves is +9 % / +5 % (shorter
-// term chunks per CTA even out the per-CTA work), while the warp-chunk kernel
-// (C4) loses 35 % with more chunks and keeps 8.
+// grid waves the term-chunk policy aims for, in units of n_sm x
+// resident_ctas_per_sm (tuning knob PZX_WAVES). Measured on C2 / C3
+// (profiles/r01/waves*.log): 8 -> 64 is +9 % / +5 % (C2: grid 256 x 5 ->
+// 256 x 37 CTAs, i.e. ~2 -> ~16 waves of the 4 TMEM CTAs an SM holds: the
+// last-wave tail shrinks), while the warp-chunk kernel (C4) loses 35 % with
+// more chunks and keeps 8.
 int grid_waves(bool warp_chunks) {
     static const int v = [] {
         const char* e = std::getenv("PZX_WAVES");
