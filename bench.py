@@ -114,18 +114,24 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------
 def build_workload(cfg_name: str, part: tuple[int, int] | None = None):
-    """part = (rank, world): generate only this rank's share of the term chunks."""
+    """part = (rank, world): the term split -- this rank's ROW-balanced term range
+    (dist.term_ranges over the whole table's offsets, the same cut the gloo tests
+    exercise); only the generator chunks overlapping it are built."""
     from paper_2403_06777_b200 import synth
     cfg = synth.CONFIGS[cfg_name]
     t0 = time.time()
-    chunks = None
+    rng_terms = None
     if part is not None and part[1] > 1:
-        nc = synth.n_chunks(cfg)
-        if nc < part[1]:
-            raise SystemExit(f"--split terms needs >= {part[1]} term chunks, {cfg_name} has {nc}")
-        chunks = range(part[0] * nc // part[1], (part[0] + 1) * nc // part[1])
-    expr = synth.generate_config(cfg, chunks=chunks)
-    log(f"[bench] {cfg.name}: {expr.n_terms} terms, {expr.n_subterms} subterms, generated in {time.time() - t0:.1f}s")
+        from paper_2403_06777_b200 import dist as D
+        full_off = synth.term_row_offsets(cfg)
+        a, b = D.term_ranges(full_off, part[1])[part[0]]
+        expr = synth.generate_config_terms(cfg, a, b)
+        rng_terms = (a, b, int(full_off[b] - full_off[a]), int(full_off[-1]))
+    else:
+        expr = synth.generate_config(cfg)
+    log(f"[bench] {cfg.name}: {expr.n_terms} terms, {expr.n_subterms} subterms"
+        + (f" (terms [{rng_terms[0]}, {rng_terms[1]}): {rng_terms[2]} of {rng_terms[3]} rows)" if rng_terms else "")
+        + f", generated in {time.time() - t0:.1f}s")
     return cfg, expr
 
 
@@ -145,29 +151,63 @@ def cpu_sample_expr(expr):
                                      f"rate scaled by {sub.n_subterms / S:.4f}")
 
 
-def cpu_reference_rate(expr, cfg, seconds: float = 12.0, threads: int | None = None, step_sample=None):
-    """Reference CPU evaluator (oracle/_ref) on all host threads, bounded sample.
-    Returns (rate, kind, threads, n_assignments, seconds, table_note)."""
+def host_cpu_info() -> dict:
+    """CPU model, logical threads and physical cores of this host (lscpu)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        cores = {tuple(l.split(",")) for l in out.splitlines() if l and not l.startswith("#")}
+        info["physical_cores"] = len(cores)
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for l in out.splitlines():
+            if l.startswith("Model name:"):
+                info["model"] = l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return info
+
+
+def _ref_evaluator(expr):
+    """(prepared evaluator, kind): the reference's own evaluation path
+    (oracle/_ref, subterm_value / ring_mul / ring_add) with the term list
+    converted to the reference's value types ONCE, outside every timed region;
+    the plain-C port where oracle/_ref was not built."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_py as O
-    kind = "reference" if O.have_ref() else "port"
+    if O.have_ref():
+        p = O.RefPrepared(expr)
+        return (lambda w, thr: p.eval(w, thr, want_exact=False)), "reference", p
+    oe = O.OExpr(expr)
+    return (lambda w, thr: O.eval_batch(oe, w, thr, impl="port")), "port", oe
+
+
+def cpu_reference_rate(expr, cfg, seconds: float = 12.0, threads: int | None = None, prepared=None):
+    """Reference CPU evaluator (oracle/_ref) on `threads` host threads, bounded sample.
+    Returns (rate, kind, threads, n_assignments, seconds, table_note)."""
     threads = threads or os.cpu_count() or 1
     expr, scale, note = cpu_sample_expr(expr)
-    oe = O.OExpr(expr)
+    ev, kind, keep = prepared or _ref_evaluator(expr)
     from paper_2403_06777_b200 import synth
     words = synth.assignments(cfg, cfg.n_assign)
     # calibrate on one assignment per thread, then size the sample to ~seconds
     t0 = time.perf_counter()
-    O.eval_batch(oe, words[:threads], threads, impl="ref" if kind == "reference" else "port")
-    dt = time.perf_counter() - t0
-    per = dt  # seconds for `threads` assignments in parallel
-    n = step_sample or max(threads, int(threads * max(1, seconds / max(per, 1e-9))))
+    ev(words[:threads], threads)
+    per = time.perf_counter() - t0  # seconds for `threads` assignments in parallel
+    n = max(threads, int(threads * max(1, seconds / max(per, 1e-9))))
     n = min(n, len(words))
     sel = words[np.linspace(0, len(words) - 1, n).astype(np.int64)]
     t0 = time.perf_counter()
-    O.eval_batch(oe, sel, threads, impl="ref" if kind == "reference" else "port")
+    ev(sel, threads)
     el = time.perf_counter() - t0
     return n / el * scale, kind, threads, n, el, note
+
+
+def workload_config(cfg, n_terms: int, n_rows: int) -> dict:
+    """The `config` object of BOTH arms' JSON lines (same keys, same values)."""
+    return {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": int(n_terms), "n_rows": int(n_rows),
+            "n_assign": cfg.n_assign, "batch": "enumerated" if cfg.enumerated else "random",
+            "output": "Re(amp)" if cfg.prob_real else "amp + |amp|^2",
+            "l2": "flushed between timed steps (256 MiB memset outside the events)"}
 
 
 def run_reference_arm(args):
@@ -175,38 +215,39 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cfg, expr = build_workload(args.config)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle_py as O
     from paper_2403_06777_b200 import synth
-    kind = "reference" if O.have_ref() else "port"
-    impl = "ref" if kind == "reference" else "port"
     threads = os.cpu_count() or 1
     full_terms, full_rows = expr.n_terms, int(expr.n_subterms)
     expr, scale, note = cpu_sample_expr(expr)
-    oe = O.OExpr(expr)
+    t0 = time.perf_counter()
+    ev, kind, keep = _ref_evaluator(expr)   # conversion to the reference's types: outside the timed steps
+    prep_s = time.perf_counter() - t0
     words = synth.assignments(cfg, cfg.n_assign)
-    per_step = threads * max(1, args.ref_per_thread)
+    per_step = min(len(words), threads * max(1, args.ref_per_thread))
     rng = np.random.default_rng(0)
     times = []
     for s in range(args.warmup + args.steps):
         sel = words[rng.choice(len(words), per_step, replace=False)]
         t0 = time.perf_counter()
-        O.eval_batch(oe, sel, threads, impl=impl)
+        ev(sel, threads)
         el = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(el)
     total = sum(times)
     value = per_step * len(times) / total * scale
+    cpu = host_cpu_info()
     line = {
         "impl": "reference", "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
         "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times) / scale, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64 (exact Z[sqrt2,i])", "data": "synthetic",
-        "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": full_terms,
-                   "n_rows": full_rows, "n_assign": cfg.n_assign, "sample_per_step": per_step},
+        "config": workload_config(cfg, full_terms, full_rows),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": kind,
-                         "sample": f"{per_step} assignments per step of the {cfg.n_assign}-assignment batch "
-                                   f"(random subset), {note}"},
+                         "sample": f"{per_step} assignments per step ({args.ref_per_thread} per thread) of the "
+                                   f"{cfg.n_assign}-assignment batch (random subset), {note}; the term list is "
+                                   f"converted to the reference's types once before the steps ({prep_s:.1f}s, "
+                                   "not timed)",
+                         "host": cpu},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -234,6 +275,12 @@ def run_ours(args):
     # locally), every rank evaluates the whole batch, ONE all-reduce (NCCL)
     # sums the partial amplitudes before |.|^2
     cfg, expr = build_workload(args.config, (rank, world) if split_terms else None)
+    if split_terms and world > 1:
+        from paper_2403_06777_b200 import synth
+        _full = synth.term_row_offsets(cfg)
+        full_terms, full_rows = cfg.n_terms, int(_full[-1])
+    else:
+        full_terms, full_rows = expr.n_terms, int(expr.n_subterms)
     ctx = P.Context(dev)
     t0 = time.time()
     table = ctx.compile_bit_table(expr)
@@ -340,7 +387,17 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
         e2e_value = evals_per_step * len(e2e_times) / e2e_tot
-        same = True
+        # the host-buffer run must reproduce the device-resident step's result
+        # (same kernels, same words, same fixed-order reductions)
+        ref_amp = torch.empty_like(d_amp)
+        step()
+        ref_amp.copy_(d_amp)
+        torch.cuda.synchronize(dev)
+        # (an enumerated batch sent as a word list may take another kernel, so
+        # equality is to the 1e-12 relative tolerance, not bitwise)
+        got, want = pinned_amp.numpy(), ref_amp.cpu().numpy()
+        rms = float(np.sqrt(np.mean(want ** 2))) or 1.0
+        same = bool(np.max(np.abs(got - want)) <= 1e-12 * rms) if got.size else True
     elif not args.no_e2e:
         if words_host is None:
             words_e2e = np.arange(first, first + N, dtype=np.uint64)
@@ -380,35 +437,43 @@ def run_ours(args):
         # sanity: e2e results equal the device-resident ones (same kernel, same words)
         same = np.allclose(pinned_amp.numpy(), d_amp.cpu().numpy(), rtol=0, atol=0)
 
-    # ---- roofline (ALU / INT issue bound) -------------------
+    # ---- roofline: the bit-sliced algorithm's minimum work (roofline.py) ------
     mean_ms = tot_ms / args.steps
-    w_row = 8 if cfg.n_params <= 32 else 12
-    work = N * (w_row * R + 16 * m)                    # algorithmic int ops per launch
     f_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_tops = N_SM * INT_LANES_PER_SM * f_mhz * 1e6 / 1e12
-    mb_path = os.path.join(ROOT, "profiles", "r01", "microbench.json")
-    mb_lop3 = None
-    try:  # the int32 LOP3 rate measured on this pool's B200s (pzx_microbench)
-        with open(mb_path) as f:
-            mb_lop3 = json.load(f)["per_sm_per_clk"]["lop3_int32"]
-        peak_tops = N_SM * mb_lop3 * f_mhz * 1e6 / 1e12
-    except Exception:
-        pass
-    achieved = work / (mean_ms / 1e3) / 1e12
-    row_evals = N * R / (mean_ms / 1e3)
+    kinfo = ctx.last_kernel()
+    op_rows, term_kinds = table.slice_stats()
+    from paper_2403_06777_b200 import roofline as RL
+    model = "sorted" if kinfo["kernel"] == "sorted" else "slice"
+    roof = RL.roofline(op_rows, term_kinds, N, mean_ms / 1e3, f_mhz, model, kinfo["sorted_groups"] or 4)
+    # BASELINE's naive int-op count (8 ops per row-eval), kept for reference
+    w_row = 8 if cfg.n_params <= 32 else 12
+    work = N * (w_row * R + 16 * m)
+    naive_peak = N_SM * INT_LANES_PER_SM * f_mhz * 1e6 / 1e12
+    roof["naive_alu"] = {"achieved": work / (mean_ms / 1e3) / 1e12, "peak": naive_peak, "unit": "Tops/s (int32)",
+                         "frac": work / (mean_ms / 1e3) / 1e12 / naive_peak,
+                         "note": "BASELINE's 8 int ops per row-eval; bit-slicing does < 1 instruction per "
+                                 "row-eval, so this exceeds 1 and bounds nothing"}
+    roof["row_evals_per_s"] = N * R / (mean_ms / 1e3)
+    roof["peak_source"] = (f"148 SM x ({RL.ISSUE_PER_SM} issue | {RL.POPC_LANES_PER_SM} POPC lanes)/clk x "
+                           f"sm_max_mhz {f_mhz:.0f} ({peaks_kind} MEASURED_PEAKS.json clock)")
+    roof["kernel"] = kinfo
     table_bytes = R * 16 + m * 24
+    roof["hbm_gbs_if_table_streamed_once"] = table_bytes / (mean_ms / 1e3) / 1e9
+    roof["traffic"] = None
     clocks = clk.summary()
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                v, kind, thr, n, el, note = cpu_reference_rate(expr, cfg, seconds=args.cpu_seconds)
+                prep = _ref_evaluator(cpu_sample_expr(expr)[0])  # converted once, outside the timing
+                v, kind, thr, n, el, note = cpu_reference_rate(expr, cfg, seconds=args.cpu_seconds, prepared=prep)
                 cpu = {"value": v, "unit": "evals/s", "cores": thr, "kind": kind,
                        "sample": f"{n} assignments (evenly spaced) of the {cfg.n_assign}-assignment batch, "
-                                 f"{note}, {el:.1f}s on {thr} threads"}
+                                 f"{note}, {el:.1f}s on {thr} threads",
+                       "host": host_cpu_info()}
                 # SURVEY §8d baseline A asks for 1 core and all cores
                 v1, _, _, n1, el1, _ = cpu_reference_rate(expr, cfg, seconds=max(2.0, args.cpu_seconds / 4),
-                                                           threads=1)
+                                                           threads=1, prepared=prep)
                 cpu["single_core"] = {"value": v1, "unit": "evals/s", "cores": 1,
                                       "sample": f"{n1} assignments, {el1:.1f}s on 1 thread"}
                 # baseline B (non-parametric per-assignment re-reduction) cannot run
@@ -419,48 +484,40 @@ def run_ours(args):
             except Exception as ex:  # the baseline must not kill the GPU number
                 cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                        "sample": f"failed: {ex}"}
+        # ncu evidence (profiles/ncu_traffic.json) applies only to the run it was
+        # captured on: one GPU, the config's full batch, default grid knobs
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        traffic, ncu_info = None, None
         try:
             with open(prof) as f:
                 ncu_info = json.load(f).get(args.config)
-            if ncu_info and args.kernel == "auto":
-                traffic = ncu_info["dram_bytes_per_launch"]
-            else:
-                ncu_info = None
         except Exception:
-            pass
+            ncu_info = None
+        knobs = any(os.environ.get(k) for k in ("PZX_WAVES", "PZX_PARTIAL_MIB", "PZX_MIN_CHUNK_ROWS", "PZX_ACC"))
+        if (ncu_info and args.kernel == "auto" and world == 1 and args.split == "assign"
+                and N == cfg.n_assign and not knobs and ncu_info.get("kernel", kinfo["kernel"]) == kinfo["kernel"]):
+            roof["traffic"] = ncu_info["dram_bytes_per_launch"]
+            roof["ncu"] = {"issue_active_pct": ncu_info["issue_active_pct"],
+                           "warp_instructions": ncu_info["warp_instructions"],
+                           "warp_instructions_per_min": ncu_info["warp_instructions"] / roof["min_warp_instructions"],
+                           "source": ncu_info["source"]}
         line = {
             "metric": "parameter-assignment evaluations/sec (amplitudes/sec)",
             "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "int32 exact exponent codes + fp64 term sum", "data": "synthetic",
-            "config": {"workload": cfg.name, "n_params": cfg.n_params, "n_terms": m, "n_rows": R,
-                       "assignments_per_gpu": N, "assignments_total": evals_per_step, "batch": "enumerated" if cfg.enumerated else "random",
-                       "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                       "parallelism": (f"term split x{world} + NCCL all-reduce" if split_terms
-                                       else f"full batch per rank x{world}" if weak
-                                       else f"assignment shards x{world} (contiguous slices, no collective)"),
-                       "kernel": args.kernel},
+            "config": workload_config(cfg, full_terms, full_rows),
+            "run": {"assignments_per_gpu": N, "assignments_total": evals_per_step, "n_terms_this_rank": m,
+                    "n_rows_this_rank": R,
+                    "parallelism": (f"term split x{world} (row-balanced ranges) + NCCL all-reduce" if split_terms
+                                    else f"full batch per rank x{world}" if weak
+                                    else f"assignment shards x{world} (contiguous slices, no collective)"),
+                    "kernel": args.kernel},
             "e2e": None if e2e_value is None else {
                 "value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(N * 8),
                 "d2h_bytes_per_step": int(N * 24), "matches_device_run": bool(same)},
             "gpu_launches": int(launches),
-            "roofline": _roofline(ncu_info, mean_ms, f_mhz, peaks_kind, traffic, {
-                         "bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
-                         "frac": achieved / peak_tops, "traffic": traffic,
-                         "peak_source": (f"148 SM x {mb_lop3:.1f} int32 LOP3/clk/SM measured on this pool "
-                                         f"(profiles/r01/microbench.json) x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
-                                         "MEASURED_PEAKS.json clock)" if mb_lop3 else
-                                         f"148 SM x 64 int32 lanes/clk x sm_max_mhz {f_mhz:.0f} ({peaks_kind} "
-                                         "MEASURED_PEAKS.json clock; lane rate from the CUDA throughput table)"),
-                         "work_per_launch": work, "row_evals_per_s": row_evals,
-                         "hbm_gbs_if_table_streamed_once": table_bytes / (mean_ms / 1e3) / 1e9,
-                         "ncu": None if ncu_info is None else {
-                             "issue_active_pct": ncu_info["issue_active_pct"],
-                             "warp_instructions_per_row_eval": ncu_info["warp_instructions"] / (N * R),
-                             "source": ncu_info["source"]}}),
+            "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "step_ms": step_ms,
@@ -470,32 +527,6 @@ def run_ours(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
-
-
-def _roofline(ncu_info, mean_ms, f_mhz, peaks_kind, traffic, naive):
-    """Primary roofline object for the JSON line.
-
-    The BASELINE's algorithmic int-op roofline (``naive``: 8R+16m lane ops per
-    assignment) is exceeded by bit-slicing (< 1 instruction per row-eval), so
-    its fraction is > 1 and bounds nothing.  When the config's kernel has an
-    ncu capture (profiles/ncu_traffic.json: its warp-instruction count per
-    launch is fixed by the config and grid policy), the binding resource is
-    issue slots: 148 SM x 4 schedulers x 1 warp-instruction/clk.  achieved =
-    that launch's warp instructions / the live mean step time (the slice
-    kernel is > 99 % of the step).  The naive figures stay under
-    ``naive_alu``.
-    """
-    if not ncu_info:
-        return naive
-    peak = N_SM * 4 * f_mhz * 1e6 / 1e12
-    ach = ncu_info["warp_instructions"] / (mean_ms / 1e3) / 1e12
-    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "T warp-instructions/s",
-            "frac": ach / peak, "traffic": traffic,
-            "peak_source": (f"148 SM x 4 warp schedulers x 1 issue/clk x sm_max_mhz {f_mhz:.0f} "
-                            f"({peaks_kind} MEASURED_PEAKS.json clock)"),
-            "work_per_launch": ncu_info["warp_instructions"],
-            "work_source": ncu_info["source"],
-            "naive_alu": naive}
 
 
 def main():
@@ -513,7 +544,8 @@ def main():
     ap.add_argument("--assign", type=int, default=0,
                     help="override the config's batch size (0: config's); sharded across ranks unless --split weak")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-per-thread", type=int, default=2)
+    ap.add_argument("--ref-per-thread", type=int, default=16,
+                    help="reference arm: assignments per host thread per step")
     ap.add_argument("--kernel", default="auto", choices=["auto", "general", "gray", "slice", "slice_rand", "sorted", "slice2"],
                     help="force one evaluation kernel (default: the library's choice)")
     args = ap.parse_args()

@@ -38,7 +38,10 @@
  * Plain pointers and sizes only; no CUDA or torch types in the signatures
  * (streams are passed as void* = cudaStream_t and used as given: NULL is the
  * CUDA legacy default stream; the synchronous host entry points use the
- * context's own stream).
+ * context's own stream). The asynchronous *_device calls take their per-call
+ * scratch (sort buffers, term-chunk bounds and partials) from a stream-ordered
+ * pool on the caller's stream, so calls in flight on different streams of one
+ * context do not share buffers; the host thread rule above still applies.
  */
 #ifndef PZX_GPU_H
 #define PZX_GPU_H
@@ -133,6 +136,11 @@ void pzx_destroy(pzx_ctx* ctx);
 const char* pzx_last_error(const pzx_ctx* ctx);
 /* Number of kernel launches issued by this context since creation. */
 uint64_t pzx_launch_count(const pzx_ctx* ctx);
+/* The evaluation kernel the last pzx_evaluate* call of this context chose:
+ * 1 POPC, 2 gray, 3 bit-sliced, 4 bit-sliced word list, 5 sorted, 6 two-slice,
+ * 7 warp-chunk bit-sliced; the sorted kernel's table groups (4 or 6) and the
+ * term-chunk count of the grid. For reports (bench.py's roofline). */
+pzx_status pzx_last_kernel(const pzx_ctx* ctx, int32_t* kernel, int32_t* sorted_groups, int32_t* term_chunks);
 
 pzx_status pzx_table_upload_expr(pzx_ctx* ctx, const pzx_expr_view* expr, pzx_table** out);
 pzx_status pzx_table_upload(pzx_ctx* ctx, const pzx_table_view* view, pzx_table** out);
@@ -152,6 +160,11 @@ pzx_status pzx_slice_op_table(int32_t out[129 * 10]);
 /* shape: n_params, n_terms, n_rows (genuine rows), max rows in one term */
 pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_terms,
                            uint64_t* n_rows, uint32_t* max_term_rows);
+/* Work statistics behind bench.py's algorithmic roofline:
+ * op_rows[op] = rows of bit-sliced op (class * 2 + single-parity, 128 = unit
+ * row), term_kinds = terms whose epilogue is kind-free / lambda-only / with a
+ * pi or pi' row. Either pointer may be NULL. */
+pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]);
 /* Folded exact constant C'_t (a,b,c,d,exp), sqrt2 exponent E_t and the count
  * nLM_t of lambda/mu rows of term t (see pzx_term_code). */
 pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],
@@ -195,7 +208,8 @@ pzx_status pzx_ringquad_sum_device(pzx_ctx* ctx, const int64_t* d_parts, uint32_
  * Term range [term_begin, term_end) of the table (term_end = UINT64_MAX: all)
  * gives partial amplitudes for the term split; d_amp receives 2n doubles,
  * d_prob n doubles (either may be NULL). With PZX_ACCUMULATE the amplitudes are
- * added into d_amp (and d_prob is computed from the sum). */
+ * added into d_amp (and d_prob is computed from the sum); d_amp must then be
+ * given (PZX_E_INVALID otherwise). */
 pzx_status pzx_evaluate_device(pzx_ctx* ctx, const pzx_table* t, const uint64_t* d_assignments,
                                uint64_t first, uint64_t n, uint64_t term_begin,
                                uint64_t term_end, double* d_amp, double* d_prob,
@@ -285,6 +299,18 @@ pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t,
 /* Per (term, assignment) exact product codes, [n_terms][n]. */
 pzx_status pzx_debug_term_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
                                 uint64_t n, pzx_term_code* out);
+/* The PRODUCTION bit-sliced kernels' own per-term state (k_eval_slice,
+ * k_eval_slice_wc, k_eval_sorted -- whichever the batch and `flags` select,
+ * PZX_E_INVALID otherwise): the batch is evaluated as pzx_evaluate
+ * (assignments != NULL) or pzx_evaluate_range (first, n) would, and for terms
+ * [term_begin, term_end) every assignment's {j, z, s1, a, b} is read from the
+ * kernel's bit planes at the term's end row and written to
+ * out[(term - term_begin) * n + i] (z is a flag here; j includes the rows'
+ * base exponents folded into the term constant). Compare with
+ * instantiate_diagram (diagram.cpp:149-165) through pzx_table_term_info. */
+pzx_status pzx_debug_slice_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments, uint64_t first,
+                                 uint64_t n, uint64_t term_begin, uint64_t term_end, uint32_t flags,
+                                 pzx_term_code* out);
 
 #ifdef __cplusplus
 }

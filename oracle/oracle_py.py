@@ -74,6 +74,11 @@ def _proto(L, ref: bool):
         L.ref_make.argtypes = [C.c_int64] * 4 + [C.c_int32, qp]
         L.ref_to_complex.argtypes = [qp, dblp, dblp]
         L.ref_to_complex.restype = None
+        L.ref_prepare.argtypes = [ep, C.c_int, C.POINTER(C.c_int)]
+        L.ref_prepare.restype = C.c_void_p
+        L.ref_eval_prepared.argtypes = [C.c_void_p, u64p, C.c_uint64, C.c_int, qp, dblp]
+        L.ref_free.argtypes = [C.c_void_p]
+        L.ref_free.restype = None
     else:
         L.oq_make.argtypes = [C.c_int64] * 4 + [C.c_int32, qp]
         L.oq_add.argtypes = [qp, qp, qp]
@@ -160,6 +165,42 @@ def eval_batch(expr, words, threads: int = 1, impl: str = "port", mode: int = 0)
         raise OracleError(st)
     exact = np.stack([ex[f][:n].astype(np.int64) for f in ("a", "b", "c", "d", "exp")], axis=1)
     return exact, amp[:n]
+
+
+class RefPrepared:
+    """The reference's own evaluator with the term list converted to its value
+    types once (ref_prepare), so that timing covers only the evaluation path."""
+
+    def __init__(self, expr, mode: int = 0):
+        self.oe = expr if isinstance(expr, OExpr) else OExpr(expr)
+        st = C.c_int()
+        self.h = ref().ref_prepare(C.byref(self.oe.c), mode, C.byref(st))
+        if not self.h:
+            raise OracleError(st.value)
+
+    def eval(self, words, threads: int = 1, want_exact: bool = True):
+        w = np.ascontiguousarray(np.asarray(words, np.uint64))
+        n = w.size
+        ex = np.zeros(max(n, 1), QUAD_DT)
+        amp = np.zeros(max(n, 1), np.complex128)
+        st = ref().ref_eval_prepared(self.h, w.ctypes.data_as(C.POINTER(C.c_uint64)), n, threads,
+                                     ex.ctypes.data_as(C.POINTER(Quad)) if want_exact else None,
+                                     amp.ctypes.data_as(C.POINTER(C.c_double)))
+        if st:
+            raise OracleError(st)
+        exact = np.stack([ex[f][:n].astype(np.int64) for f in ("a", "b", "c", "d", "exp")], axis=1)
+        return exact, amp[:n]
+
+    def close(self):
+        if self.h:
+            ref().ref_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def term_value(expr, t: int, word: int, impl: str = "port"):

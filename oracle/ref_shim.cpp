@@ -109,15 +109,9 @@ pzx::RingQuad eval_literal(const Prepared& p, const pzx::ParamAssignment& a) {
     return total;
 }
 
-}  // namespace
-
-extern "C" {
-
-int ref_eval_batch(const oq_expr* e, const uint64_t* words, uint64_t n, int n_threads,
-                   int mode, oq_quad* exact, double* amp) {
-    Prepared p;
-    int st = guarded([&] { p = prepare(e, mode == 1); });
-    if (st) return st;
+// Evaluate words [0, n) against a prepared expression on n_threads threads.
+int eval_prepared(const Prepared& p, uint32_t n_params, const uint64_t* words, uint64_t n, int n_threads,
+                  int mode, oq_quad* exact, double* amp) {
     if (n_threads < 1) n_threads = 1;
     if (static_cast<uint64_t>(n_threads) > n) n_threads = n ? static_cast<int>(n) : 1;
     std::vector<int> status(n_threads, OQ_OK);
@@ -125,7 +119,7 @@ int ref_eval_batch(const oq_expr* e, const uint64_t* words, uint64_t n, int n_th
         const uint64_t b = n * tid / n_threads, en = n * (tid + 1) / n_threads;
         status[tid] = guarded([&] {
             for (uint64_t i = b; i < en; ++i) {
-                const auto a = pzx::ParamAssignment::total(words[i], e->n_params);
+                const auto a = pzx::ParamAssignment::total(words[i], n_params);
                 const pzx::RingQuad v = mode == 1 ? eval_literal(p, a) : eval_primitives(p, a);
                 if (exact) exact[i] = from_ref(v);
                 if (amp) {
@@ -143,6 +137,51 @@ int ref_eval_batch(const oq_expr* e, const uint64_t* words, uint64_t n, int n_th
     for (int s : status)
         if (s) return s;
     return OQ_OK;
+}
+
+struct PreparedHandle {
+    Prepared p;
+    uint32_t n_params = 0;
+    int mode = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+// Prepared form for timing: the conversion of the whole term list into the
+// reference's own value types (pzx::RingQuad scalars + std::vector<pzx::Subterm>
+// per term, and for mode 1 the leaf ZXDiagrams) happens once here, outside any
+// timed region; ref_eval_prepared then runs only the reference's evaluation
+// path (subterm_value / ring_mul / ring_add, or instantiate_diagram).
+void* ref_prepare(const oq_expr* e, int mode, int* status) {
+    PreparedHandle* h = new PreparedHandle;
+    h->n_params = e->n_params;
+    h->mode = mode;
+    const int st = guarded([&] { h->p = prepare(e, mode == 1); });
+    if (status) *status = st;
+    if (st) {
+        delete h;
+        return nullptr;
+    }
+    return h;
+}
+
+int ref_eval_prepared(const void* handle, const uint64_t* words, uint64_t n, int n_threads, oq_quad* exact,
+                      double* amp) {
+    const PreparedHandle* h = static_cast<const PreparedHandle*>(handle);
+    if (!h) return OQ_E_DOMAIN;
+    return eval_prepared(h->p, h->n_params, words, n, n_threads, h->mode, exact, amp);
+}
+
+void ref_free(void* handle) { delete static_cast<PreparedHandle*>(handle); }
+
+int ref_eval_batch(const oq_expr* e, const uint64_t* words, uint64_t n, int n_threads,
+                   int mode, oq_quad* exact, double* amp) {
+    Prepared p;
+    int st = guarded([&] { p = prepare(e, mode == 1); });
+    if (st) return st;
+    return eval_prepared(p, e->n_params, words, n, n_threads, mode, exact, amp);
 }
 
 int ref_term_value(const oq_expr* e, uint64_t t, uint64_t word, oq_quad* out) {

@@ -22,7 +22,8 @@ EXPORTS = (
     "pzx_pzx1_info", "pzx_pzx1_decode", "pzx_table_upload_pzx1", "pzx_backend_contract_get",
     "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
     "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex", "pzx_evaluate_exact",
-    "pzx_evaluate_exact_range", "pzx_ringquad_sum", "pzx_ringquad_sum_device",
+    "pzx_evaluate_exact_range", "pzx_ringquad_sum", "pzx_ringquad_sum_device", "pzx_table_slice_stats",
+    "pzx_last_kernel", "pzx_debug_slice_codes",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -122,6 +123,11 @@ def lib() -> C.CDLL:
     L.pzx_table_compile_host.argtypes = [C.POINTER(ExprView), C.POINTER(vp)]
     L.pzx_class_table.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.pzx_slice_op_table.argtypes = [C.POINTER(C.c_int32)]
+    L.pzx_table_slice_stats.argtypes = [vp, u64p, u64p]
+    i32p = C.POINTER(C.c_int32)
+    L.pzx_last_kernel.argtypes = [vp, i32p, i32p, i32p]
+    L.pzx_debug_slice_codes.argtypes = [vp, vp, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                        C.POINTER(TermCode)]
     _lib = L
     return L
 

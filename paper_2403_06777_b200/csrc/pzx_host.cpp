@@ -159,7 +159,12 @@ struct HostTable {
     std::vector<uint4> srows;               // bit-sliced kernel rows (2 per row)
     std::vector<uint4> qrows;               // sorted-batch kernel rows (2 per row, n_params <= 32)
     std::vector<double> sterm_c;            // its term constants (2 per term)
+    std::vector<uint8_t> jb_t;              // per term: sum of the rows' slice jbase mod 8 (folded into sterm_c)
     int jb_term = 0;                        // running sum of slice jbase in the open term
+    uint32_t kinds_term = 0;                // OR of the open term's row kind flags
+    // work statistics behind the algorithmic roofline (pzx_table_slice_stats)
+    uint64_t op_rows[kSliceOps] = {};       // rows per bit-sliced op
+    uint64_t term_kinds[3] = {};            // terms by epilogue: kind-free, lambda only, with pi / pi'
     bool want_srows = true;                 // build the bit-sliced layout (enumerated batches)
     bool want_qrows = true;                 // build the sorted-batch layout (word lists, n_params <= 32)
     bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
@@ -231,6 +236,8 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t cls = (code & kCodeMask) >> 4;
     const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
     h.jb_term += kSliceJbase[op];
+    h.op_rows[op] += 1;
+    h.kinds_term |= uint32_t(kSliceKindFlags[op]);
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
     if (h.want_srows) {
         h.srows.push_back(make_uint4(uint32_t(psi), uint32_t(phi), scode, walsh32(psi)));
@@ -296,11 +303,14 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
     for (int i = 0; i < lm; ++i) v = cmul(v, mu);
     h.term_c.push_back(double(v.re));
     h.term_c.push_back(double(v.im));
+    h.jb_t.push_back(uint8_t(h.jb_term & 7));
     const C128 wj = zw_to_c128(zw_pow_w(h.jb_term & 7));  // slice kernel: w^(sum of row jbase)
     const C128 vs = cmul(v, wj);
     h.sterm_c.push_back(double(vs.re));
     h.sterm_c.push_back(double(vs.im));
     h.jb_term = 0;
+    h.term_kinds[(h.kinds_term & (kSlicePiFlag | kSlicePipFlag)) ? 2 : (h.kinds_term & kSliceLamFlag) ? 1 : 0] += 1;
+    h.kinds_term = 0;
     h.term_row.push_back(h.n_dev_rows());
     return PZX_OK;
 }
@@ -444,12 +454,15 @@ void merge_into(HostTable& h, HostTable& part) {
     app(h.nlm_t, part.nlm_t);
     app(h.term_c, part.term_c);
     app(h.sterm_c, part.sterm_c);
+    app(h.jb_t, part.jb_t);
     app(h.rows, part.rows);
     app(h.srows, part.srows);
     app(h.qrows, part.qrows);
     app(h.swapped, part.swapped);
     app(h.unit, part.unit);
     h.max_rows = std::max(h.max_rows, part.max_rows);
+    for (int i = 0; i < kSliceOps; ++i) h.op_rows[i] += part.op_rows[i];
+    for (int i = 0; i < 3; ++i) h.term_kinds[i] += part.term_kinds[i];
 }
 
 // compile_bit_table over term ranges in parallel (terms are independent),
@@ -583,6 +596,14 @@ struct pzx_ctx {
     void* d_xout = nullptr; size_t xout_cap = 0;  // exact outputs + overflow flags
     void* d_dbg = nullptr; size_t dbg_cap = 0;
     void* d_sort = nullptr; size_t sort_cap = 0;
+    // per-call scratch of the evaluation kernels (sort buffers, chunk bounds,
+    // term-chunk partials): stream-ordered allocations from this pool on the
+    // call's stream, so concurrent pzx_evaluate_device calls on different
+    // streams never share a buffer (memory is recycled once the freeing
+    // stream has passed the free)
+    cudaMemPool_t pool = nullptr;
+    // what the last evaluation launched (pzx_last_kernel; bench.py's roofline)
+    int last_kernel = 0, last_groups = 0, last_chunks = 0;
 };
 
 struct pzx_table {
@@ -722,6 +743,29 @@ uint64_t min_chunk_rows() {
     return v;
 }
 
+// Stream-ordered scratch of one evaluation call: every buffer comes from the
+// context's pool on the call's stream and is released with cudaFreeAsync on
+// the same stream when the call returns (after its kernels are enqueued), so
+// the memory cannot be handed to another stream before those kernels finish.
+struct CallScratch {
+    pzx_ctx* ctx;
+    cudaStream_t s;
+    std::vector<void*> bufs;
+    CallScratch(pzx_ctx* c, cudaStream_t st) : ctx(c), s(st) {}
+    CallScratch(const CallScratch&) = delete;
+    CallScratch& operator=(const CallScratch&) = delete;
+    pzx_status alloc(size_t bytes, void** p) {
+        *p = nullptr;
+        cudaError_t e = cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 16), ctx->pool, s);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "stream-ordered scratch");
+        bufs.push_back(*p);
+        return PZX_OK;
+    }
+    ~CallScratch() {
+        for (void* p : bufs) cudaFreeAsync(p, s);
+    }
+};
+
 pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t flags) {
     if (!ctx || !t) return PZX_E_INVALID;
     if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table (pzx_table_compile_host)");
@@ -739,9 +783,13 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
         return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "
                                            "(enumerated kernels need a contiguous batch starting at a multiple "
                                            "of 16 (gray), 32 (slice) or 64 (slice2); slice needs terms of <= 127 rows)");
+    if (r.accumulate && !r.d_amp)
+        return set_err(ctx, PZX_E_INVALID, "PZX_ACCUMULATE needs an amplitude buffer (d_amp)");
     KernelChoice kc = choose_kernel(t->dev, r);
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    CallScratch scratch(ctx, r.stream);  // freed (stream-ordered) when this call returns
+    void* sort_buf = nullptr;
     constexpr uint64_t kSortedMaxBatch = uint64_t(1) << 26;  // bounds the sort / regroup scratch (~70 B per word)
     if (kc == KC_SORTED && r.n > kSortedMaxBatch) {
         // huge word lists: independent sub-batches (each sorted on its own)
@@ -758,13 +806,13 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     }
     if (kc == KC_SORTED) {  // sort word|position pairs; results are scattered back by position
         if (!r.d_asg) return set_err(ctx, PZX_E_INVALID, "sorted kernel needs an explicit word list");
-        if ((st = cuda_err(ctx, grow(&ctx->d_sort, &ctx->sort_cap, sort_scratch_bytes(r.n) + 256), "alloc sort scratch"))) return st;
-        if ((st = cuda_err(ctx, sort_words(r.d_asg, r.n, t->dev.n_params, ctx->d_sort, &r.d_sorted, &r.d_perm,
+        if ((st = scratch.alloc(sort_scratch_bytes(r.n) + 256, &sort_buf))) return st;
+        if ((st = cuda_err(ctx, sort_words(r.d_asg, r.n, t->dev.n_params, sort_buf, &r.d_sorted, &r.d_perm,
                                            r.stream, &ctx->launches), "sort words"))) return st;
         // regroup: every thread's 32 words must share their high part (bits >= 4 G);
         // 16 table bits for dense batches, 24 (wide tables) when 16 would pad by
         // more than 25 % (sparse batches such as 2^16 random 32-bit words)
-        void* gs = static_cast<unsigned char*>(ctx->d_sort) + sort_base_bytes(r.n);
+        void* gs = static_cast<unsigned char*>(sort_buf) + sort_base_bytes(r.n);
         uint64_t slots = 0;
         int groups = kSortedGroups;
         if ((st = cuda_err(ctx, group_slots(r.d_sorted, r.n, 4 * kSortedGroups, gs, &slots, r.stream, &ctx->launches), "group"))) return st;
@@ -790,7 +838,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     }
     // grid policy: split the terms into chunks so that the grid is >= kWaves
     // full waves of resident CTAs (keeps the last-wave tail small); chunk
-    // partials are bounded to ~1 GiB of scratch
+    // partials are bounded by partial_cap() (2 GiB by default, PZX_PARTIAL_MIB)
     const int ablocks = grid_assign_blocks(t->dev, r, kc);
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
@@ -822,13 +870,19 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     if (chunks > 1) {
         std::vector<uint64_t> b;
         chunk_bounds(t->host, r.term_begin, r.term_end, chunks, b);
-        if ((st = cuda_err(ctx, grow(&ctx->d_chunks, &ctx->chunks_cap, b.size() * 8), "alloc chunks"))) return st;
-        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_chunks, b.data(), b.size() * 8, cudaMemcpyHostToDevice, r.stream), "copy chunks"))) return st;
-        if ((st = cuda_err(ctx, grow(&ctx->d_partial, &ctx->partial_cap, size_t(chunks) * r.n * 16), "alloc partials"))) return st;
-        r.d_chunk_terms = static_cast<const uint64_t*>(ctx->d_chunks);
-        r.d_partial = static_cast<double2*>(ctx->d_partial);
+        void* d_b = nullptr;
+        void* d_p = nullptr;
+        if ((st = scratch.alloc(b.size() * 8, &d_b))) return st;
+        // pageable source: staged by the driver before the call returns, so `b` may go
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(d_b, b.data(), b.size() * 8, cudaMemcpyHostToDevice, r.stream), "copy chunks"))) return st;
+        if ((st = scratch.alloc(size_t(chunks) * r.n * 16, &d_p))) return st;
+        r.d_chunk_terms = static_cast<const uint64_t*>(d_b);
+        r.d_partial = static_cast<double2*>(d_p);
     }
     if (t->dev.lut_layout.bytes > 200 * 1024) return set_err(ctx, PZX_E_CAPACITY, "LUT exceeds 200 KiB");
+    ctx->last_kernel = int(kc);
+    ctx->last_groups = kc == KC_SORTED ? r.sorted_groups : 0;
+    ctx->last_chunks = chunks;
     if ((st = cuda_err(ctx, launch_evaluate(t->dev, r, kc, &ctx->launches), "evaluate kernel"))) return st;
     return PZX_OK;
 }
@@ -1057,6 +1111,14 @@ void pzx_destroy(pzx_ctx* ctx) {
 const char* pzx_last_error(const pzx_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 uint64_t pzx_launch_count(const pzx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+pzx_status pzx_last_kernel(const pzx_ctx* ctx, int32_t* kernel, int32_t* sorted_groups, int32_t* term_chunks) {
+    if (!ctx) return PZX_E_INVALID;
+    if (kernel) *kernel = ctx->last_kernel;
+    if (sorted_groups) *sorted_groups = ctx->last_groups;
+    if (term_chunks) *term_chunks = ctx->last_chunks;
+    return PZX_OK;
+}
 
 pzx_status pzx_table_upload_expr(pzx_ctx* ctx, const pzx_expr_view* expr, pzx_table** out) {
     return pzx_table_upload_expr_ex(ctx, expr, 0, out);
@@ -1377,6 +1439,15 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
     return PZX_OK;
 }
 
+pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]) {
+    if (!t) return PZX_E_INVALID;
+    if (op_rows)
+        for (int i = 0; i < kSliceOps; ++i) op_rows[i] = t->host.op_rows[i];
+    if (term_kinds)
+        for (int i = 0; i < 3; ++i) term_kinds[i] = t->host.term_kinds[i];
+    return PZX_OK;
+}
+
 pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],
                                int32_t* e_sqrt2, int32_t* n_lm) {
     if (!t || term >= t->dev.n_terms) return PZX_E_INVALID;
@@ -1657,6 +1728,56 @@ pzx_status pzx_debug_phase_indices(pzx_ctx* ctx, const pzx_table* t, const uint6
         else
             std::memcpy(dst, src, n);
         ++o;
+    }
+    return PZX_OK;
+}
+
+pzx_status pzx_debug_slice_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments, uint64_t first,
+                                 uint64_t n, uint64_t term_begin, uint64_t term_end, uint32_t flags,
+                                 pzx_term_code* out) {
+    if (!ctx || !t || (n && !out)) return PZX_E_INVALID;
+    if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table");
+    term_end = std::min<uint64_t>(term_end, t->dev.n_terms);
+    if (term_begin > term_end) return set_err(ctx, PZX_E_INVALID, "bad debug term range");
+    const uint64_t M = term_end - term_begin;
+    if (!n || !M) return PZX_OK;
+    pzx_status st;
+    if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
+    LaunchReq r;
+    r.stream = ctx->stream;
+    r.first = first;
+    r.n = n;
+    r.term_begin = 0;
+    r.term_end = t->dev.n_terms;
+    r.prob_mode = 1;
+    if (assignments) {
+        if ((st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc assignments"))) return st;
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(ctx->d_asg, assignments, n * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D assignments"))) return st;
+        r.d_asg = static_cast<const uint64_t*>(ctx->d_asg);
+        bool contig = n >= uint64_t(kGray);
+        for (uint64_t i = 1; contig && i < n; ++i) contig = assignments[i] == assignments[0] + i;
+        if (contig) { r.words_contiguous = 1; r.first = assignments[0]; }
+    }
+    if ((st = cuda_err(ctx, grow(&ctx->d_amp, &ctx->amp_cap, n * 16), "alloc amplitudes"))) return st;
+    r.d_amp = static_cast<double2*>(ctx->d_amp);
+    if ((st = cuda_err(ctx, grow(&ctx->d_dbg, &ctx->dbg_cap, M * n * 20), "alloc debug"))) return st;
+    if ((st = cuda_err(ctx, cudaMemsetAsync(ctx->d_dbg, 0xFF, M * n * 20, ctx->stream), "clear debug"))) return st;
+    r.d_dbg5 = static_cast<uint32_t*>(ctx->d_dbg);
+    r.dbg_t0 = term_begin;
+    r.dbg_t1 = term_end;
+    r.dbg_n = n;
+    if ((st = run_eval(ctx, t, r, flags))) return st;
+    const int k = ctx->last_kernel;
+    if (k != KC_SLICE && k != KC_SLICER && k != KC_SLICEWC && k != KC_SORTED)
+        return set_err(ctx, PZX_E_INVALID, "debug_slice_codes: the batch did not run on a bit-sliced kernel");
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(out, ctx->d_dbg, M * n * 20, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "debug slice codes"))) return st;
+    for (uint64_t tt = 0; tt < M; ++tt) {  // the slice kernels count w' relative to each row's jbase
+        const uint32_t jb = t->host.jb_t[term_begin + tt];
+        for (uint64_t i = 0; i < n; ++i) {
+            pzx_term_code& c = out[tt * n + i];
+            if (c.j != 0xFFFFFFFFu) c.j = (c.j + jb) & 7u;
+        }
     }
     return PZX_OK;
 }

@@ -105,6 +105,11 @@ struct LaunchReq {
     const uint64_t* d_sorted = nullptr;
     int sorted_groups = kSortedGroups;  // Four-Russians table groups of the sorted kernel (4 or 6)
     const uint32_t* d_perm = nullptr;
+    // debug (pzx_debug_slice_codes): the bit-sliced kernels write their own
+    // per-term planes {J (before the 6 s1 fold), Z, s1, a, b} for terms
+    // [dbg_t0, dbg_t1) at [term - dbg_t0][caller position < dbg_n][5]
+    uint32_t* d_dbg5 = nullptr;
+    uint64_t dbg_t0 = 0, dbg_t1 = 0, dbg_n = 0;
 };
 
 // Sort an arbitrary word list (masked to n_params bits) with its positions:

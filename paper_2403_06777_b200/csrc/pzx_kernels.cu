@@ -912,6 +912,32 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
     if (kinds) K.reset();
 }
 
+// Debug hook (LaunchReq::d_dbg5): the kernel's own per-term state for each of
+// the thread's 32 assignments, read from the bit planes exactly as the
+// epilogue sees them (before the 6 s1 fold into J). `term` = index of the
+// term whose end row was just consumed. Sorted batches map the slot back to
+// the caller's position (padding slots are skipped).
+template <int NT, bool LC>
+__device__ __noinline__ void debug_dump_codes(const LaunchReq& r, uint64_t term, uint64_t off, uint32_t J0,
+                                              uint32_t J1, uint32_t J2, uint32_t Z, KindCounters<NT, LC>& K) {
+    if (term < r.dbg_t0 || term >= r.dbg_t1) return;
+    for (int g = 0; g < 32; ++g) {
+        uint64_t idx = off + uint64_t(g);
+        if (idx >= r.n) break;
+        if (r.d_perm) {
+            idx = r.d_perm[idx];
+            if (idx == 0xFFFFFFFFu) continue;
+        }
+        if (idx >= r.dbg_n) continue;
+        uint32_t* o = r.d_dbg5 + ((term - r.dbg_t0) * r.dbg_n + idx) * 5;
+        o[0] = ((J0 >> g) & 1u) | (((J1 >> g) & 1u) << 1) | (((J2 >> g) & 1u) << 2);
+        o[1] = (Z >> g) & 1u;
+        o[2] = K.s_of(g);
+        o[3] = K.a_of(g);
+        o[4] = K.b_of(g);
+    }
+}
+
 template <int NT, bool TM, bool ROLL = false, bool LC = false>
 __device__ __forceinline__ void slice_term_epilogue(TermC& tc, const double2* src, const SmemLut& L, double2* crot,
                                                     SliceAcc<NT, TM>& acc, uint32_t& J0, uint32_t& J1,
@@ -1094,8 +1120,10 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         if (code & kSliceLamFlag) K.bump_s(vl);
                         if (code & kSlicePiFlag) K.bump_a(vpi);
                         if (code & kSlicePipFlag) K.bump_b(vpip);
-                        if (code & kEndFlag)
+                        if (code & kEndFlag) {
+                            if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                             slice_term_epilogue<NT, TM, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                        }
                     }
                 }
             } else {
@@ -1124,7 +1152,10 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         if (code & kSliceLamFlag) K.bump_s(vl);
                         if (code & kSlicePiFlag) K.bump_a(vpi);
                         if (code & kSlicePipFlag) K.bump_b(vpip);
-                        if (code & kEndFlag) slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                        if (code & kEndFlag) {
+                            if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
+                            slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                        }
                     }
                 }
             }
@@ -1243,8 +1274,10 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
                     if (code & kSliceLamFlag) K.bump_s(vl);
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
-                    if (code & kEndFlag)
+                    if (code & kEndFlag) {
+                        if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                         slice_term_epilogue<NT, true, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                    }
                 }
             }
             __syncwarp();  // the warp is done with buffer (i & 1)
@@ -1526,8 +1559,10 @@ __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1)
                     if (code & kSliceLamFlag) K.bump_s(vl);
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
-                    if (code & kEndFlag)
+                    if (code & kEndFlag) {
+                        if (r.d_dbg5) debug_dump_codes<NT, (NT > 128)>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                         slice_term_epilogue<NT, TM, true, (NT > 128)>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
+                    }
                 }
             }
             __syncthreads();

@@ -320,6 +320,15 @@ class DeviceTable:
         _check(N.lib().pzx_table_term_info(self.handle, t, N.ptr(coef, C.c_int64), C.byref(e), C.byref(lm)))
         return RingQuad(*map(int, coef)), e.value, lm.value
 
+    def slice_stats(self):
+        """(op_rows[129], term_kinds[3]): rows per bit-sliced op and terms per
+        epilogue kind (kind-free, lambda-only, with pi) -- the work counts behind
+        the algorithmic roofline (roofline.py)."""
+        ops = np.zeros(129, np.uint64)
+        kinds = np.zeros(3, np.uint64)
+        _check(N.lib().pzx_table_slice_stats(self.handle, N.ptr(ops, C.c_uint64), N.ptr(kinds, C.c_uint64)))
+        return ops, kinds
+
     def free(self) -> None:
         if self.handle:
             N.lib().pzx_table_free(self.handle)
@@ -362,6 +371,15 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(N.lib().pzx_launch_count(self.handle))
+
+    KERNEL_NAMES = {1: "popc", 2: "gray", 3: "slice", 4: "slice_rand", 5: "sorted", 6: "slice2", 7: "slice_wc"}
+
+    def last_kernel(self) -> dict:
+        """The evaluation kernel the last evaluate* call chose (pzx_last_kernel)."""
+        k, g, c = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(N.lib().pzx_last_kernel(self.handle, C.byref(k), C.byref(g), C.byref(c)), self.handle)
+        return {"kernel": self.KERNEL_NAMES.get(k.value, str(k.value)), "sorted_groups": g.value,
+                "term_chunks": c.value}
 
     # -- compile + upload ---------------------------------------------------
     def compile_bit_table(self, expr: ScalarExpression, simplify: bool = False) -> DeviceTable:
@@ -527,6 +545,25 @@ class Context:
         return out
 
 
+def _debug_slice_codes(self, table, assignments=None, first: int = 0, n: int | None = None, term_begin: int = 0,
+                       term_end: int | None = None, flags: int = 0):
+    """The production bit-sliced kernel's own per-term codes (pzx_debug_slice_codes):
+    uint32 [terms, n, 5] = {j, z (flag), s1, a, b} for terms [term_begin, term_end)."""
+    a = None
+    if assignments is not None:
+        a = np.ascontiguousarray(np.asarray(assignments, dtype=np.uint64))
+        n = a.size
+    te = table.n_terms if term_end is None else term_end
+    out = np.zeros((max(te - term_begin, 0), n, 5), np.uint32)
+    if out.size:
+        _check(N.lib().pzx_debug_slice_codes(self.handle, table.handle, N.ptr(a, C.c_uint64), first, n, term_begin,
+                                             te, flags, out.ctypes.data_as(C.POINTER(N.TermCode))), self.handle)
+    return out
+
+
+Context.debug_slice_codes = _debug_slice_codes
+
+
 class HostTable:
     """Host-only compiled table (pzx_table_compile_host): inspection and CPU tests."""
 
@@ -542,6 +579,7 @@ class HostTable:
         self.n_params, self.n_terms, self.n_rows, self.max_term_rows = p.value, m.value, r.value, mx.value
 
     term_info = DeviceTable.term_info
+    slice_stats = DeviceTable.slice_stats
     free = DeviceTable.free
     __del__ = DeviceTable.__del__
 

@@ -1,0 +1,87 @@
+"""Algorithmic roofline of the bit-sliced evaluators.
+
+The BASELINE's naive int-op count (8 ops per row-eval) is not a bound for a
+bit-sliced kernel: one 32-bit LOP3 updates a row for 32 assignments at once.
+The roofline reported instead is the MINIMUM instruction count of the
+bit-sliced algorithm itself, derived from the generated per-class LOP3 chains
+(gen_slice_ops.case_body) and the table's own row / term mix
+(pzx_table_slice_stats), against the two sm_100 resources it can saturate:
+
+* issue slots: 148 SMs x 4 schedulers x 1 warp-instruction / clk;
+* the XU pipe (POPC): 16 lanes / clk / SM (profiles/r01/microbench.json).
+
+Per row and warp (one warp = 32 threads x 32 assignments = 1024 assignments):
+
+    1 LDS (the row record)  +  per parity vector (1 or 2) the enumerated kernels'
+    X = W ^ -parity(mask & base):  AND + POPC + LOP3->P + SEL  (4, one POPC)
+    +  the class's LOP3 chain (len(case_body(op)): phase counter ripple add,
+       zero / lambda / pi / pi' indicators)
+
+Per term and warp (the epilogue, 32 assignments per thread), per assignment:
+
+    kind-free term: 1 LDS (C w^j) + 2 DADD            = 3
+    lambda-only   : 2 LDS + 2 DFMA (real (sqrt2-1)^s)  = 4
+    with pi / pi' : 2 LDS + 4 DFMA (complex factor)    = 6
+
+For word-list batches the sorted kernel forms each parity vector from G
+Four-Russians table words: G LDS + G XOR + AND + POPC + 1 = 2G + 3 per parity
+(G = 4 dense, 6 sparse batches). Loop control, row prefetch, TMA waits,
+counter decode, TMEM traffic and the chunk reduction are implementation
+overhead and are NOT in the minimum, so frac <= 1 by construction.
+"""
+from __future__ import annotations
+
+from functools import lru_cache
+
+import numpy as np
+
+N_SM = 148
+ISSUE_PER_SM = 4        # warp-instructions / clk / SM (one per scheduler)
+POPC_LANES_PER_SM = 16  # XU lanes / clk / SM (measured 15.9, profiles/r01/microbench.json)
+EPI_PER_ASSIGN = (3, 4, 6)  # kind-free, lambda-only, pi: minimum instructions per (term, assignment)
+
+
+@lru_cache(maxsize=None)
+def _op_table():
+    from . import gen_slice_ops as G
+    body = np.array([len(G.case_body(op, False, True)) for op in range(129)], np.int64)
+    par = np.array([0 if op >= 128 else (1 if op & 1 else 2) for op in range(129)], np.int64)
+    return body, par
+
+
+def min_counts(op_rows, term_kinds, n_assign: int, kernel: str = "slice", sorted_groups: int = 4) -> dict:
+    """Minimum warp-instructions and warp-POPCs of one evaluation launch."""
+    body, par = _op_table()
+    op_rows = np.asarray(op_rows, np.float64)
+    kinds = np.asarray(term_kinds, np.float64)
+    per_parity = 4 if kernel != "sorted" else 2 * sorted_groups + 3
+    row_inst = float(np.sum(op_rows * (1 + per_parity * par + body)))
+    popc = float(np.sum(op_rows * par))
+    term_inst = float(np.sum(kinds * 32 * np.array(EPI_PER_ASSIGN)))
+    warps = n_assign / 1024.0
+    return {"warp_instructions": warps * (row_inst + term_inst), "warp_popc": warps * popc,
+            "row_share": row_inst / max(row_inst + term_inst, 1.0),
+            "per_row_per_warp": row_inst / max(float(np.sum(op_rows)), 1.0),
+            "per_term_per_warp": term_inst / max(float(np.sum(kinds)), 1.0)}
+
+
+def roofline(op_rows, term_kinds, n_assign: int, seconds: float, f_mhz: float, kernel: str = "slice",
+             sorted_groups: int = 4) -> dict:
+    """The bench's `roofline` object: the binding resource of the algorithm's
+    minimum work (issue slots or the POPC pipe) against the measured launch time."""
+    c = min_counts(op_rows, term_kinds, n_assign, kernel, sorted_groups)
+    hz = f_mhz * 1e6
+    t_issue = c["warp_instructions"] / (N_SM * ISSUE_PER_SM * hz)
+    t_xu = c["warp_popc"] * 32 / (N_SM * POPC_LANES_PER_SM * hz)
+    if t_issue >= t_xu:
+        out = {"bound": "issue", "achieved": c["warp_instructions"] / seconds / 1e12,
+               "peak": N_SM * ISSUE_PER_SM * hz / 1e12, "unit": "T warp-instructions/s (algorithmic minimum)"}
+    else:
+        out = {"bound": "xu (POPC)", "achieved": c["warp_popc"] * 32 / seconds / 1e12,
+               "peak": N_SM * POPC_LANES_PER_SM * hz / 1e12, "unit": "T POPC lane-ops/s (algorithmic minimum)"}
+    out["frac"] = out["achieved"] / out["peak"]
+    out.update({"min_warp_instructions": c["warp_instructions"], "min_warp_popc": c["warp_popc"],
+                "min_time_issue_s": t_issue, "min_time_popc_s": t_xu,
+                "min_per_row_per_warp": c["per_row_per_warp"], "min_per_term_per_warp": c["per_term_per_warp"],
+                "kernel_model": kernel if kernel != "sorted" else f"sorted (G={sorted_groups})"})
+    return out

@@ -155,6 +155,41 @@ def generate_config(cfg: Config, n_terms: int | None = None, chunks: range | Non
     return concat(parts)
 
 
+def term_row_offsets(cfg: Config) -> np.ndarray:
+    """Subterm offsets [m + 1] of the whole config table without generating it:
+    the term sizes are the first draw of every (chunk) generator, so this is
+    cheap even for C5's 2^24 terms. Used to cut row-balanced term ranges
+    (dist.term_ranges) for the term split before any rank builds its table."""
+    seed = 20261018 + cfg.cid
+    n = cfg.n_terms
+    if n <= CHUNK_TERMS:
+        sizes = [np.random.Generator(np.random.MT19937(seed)).integers(cfg.n_lo, cfg.n_hi + 1, n)]
+    else:
+        sizes = [np.random.Generator(np.random.MT19937(seed * 4099 + c)).integers(
+                     cfg.n_lo, cfg.n_hi + 1, min(CHUNK_TERMS, n - c * CHUNK_TERMS)) for c in range(n_chunks(cfg))]
+    off = np.zeros(n + 1, np.uint64)
+    np.cumsum(np.concatenate(sizes), out=off[1:])
+    return off
+
+
+def generate_config_terms(cfg: Config, t0: int, t1: int) -> ScalarExpression:
+    """Terms [t0, t1) of the config table (only the chunks that overlap the
+    range are generated), rebased so the slice starts at subterm 0."""
+    if cfg.n_terms <= CHUNK_TERMS:
+        full = generate_config(cfg)
+        c0 = 0
+    else:
+        c0, c1 = t0 // CHUNK_TERMS, max(t0, t1 - 1) // CHUNK_TERMS + 1
+        full = generate_config(cfg, chunks=range(c0, c1))
+        c0 *= CHUNK_TERMS
+    a, b = t0 - c0, t1 - c0
+    off = full.term_offset
+    s0, s1 = int(off[a]), int(off[b])
+    return ScalarExpression(full.n_params, off[a:b + 1] - np.uint64(s0), full.term_scalar[a:b],
+                            full.kind[s0:s1], full.psi_k[s0:s1], full.psi_mask[s0:s1], full.phi_k[s0:s1],
+                            full.phi_mask[s0:s1])
+
+
 def assignments(cfg: Config, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
     """The config's assignment batch: enumerated 0..N-1 or seeded uniform P-bit words."""
     N = cfg.n_assign if n is None else n

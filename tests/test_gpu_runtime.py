@@ -1,0 +1,171 @@
+"""GPU runtime checks: stream-ordered scratch under concurrency, argument
+validation, compute-sanitizer runs of the hand-written pipelines (TMA bulk
+copies + mbarriers, TMEM alloc / ld / st, generated PTX jump tables), and the
+multi-GPU data path (per-rank GPU partials + the collectives that combine
+them) with two ranks sharing the box's one GPU over gloo.
+"""
+import os
+import shutil
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2403_06777_b200 as P
+from paper_2403_06777_b200 import synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SANITIZER = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def test_concurrent_streams_match_serial(ctx):
+    """Two pzx_evaluate_device calls in flight on two streams of ONE context
+    (each with term-chunk partials, chunk bounds and a sorted batch's scratch)
+    give exactly the serial results: per-call scratch is stream-ordered."""
+    import torch
+    e1 = synth.generate(18, 6000, 16, 40, 61)
+    e2 = synth.generate(22, 5000, 16, 40, 62)
+    t1, t2 = ctx.compile_bit_table(e1), ctx.compile_bit_table(e2)
+    n1, n2 = 1 << 16, 1 << 15
+    words = torch.from_numpy(np.random.default_rng(3).integers(0, 1 << 22, n2, dtype=np.uint64).view(np.int64)).cuda()
+    ser1 = torch.zeros(2 * n1, dtype=torch.float64, device="cuda:0")
+    ser2 = torch.zeros(2 * n2, dtype=torch.float64, device="cuda:0")
+    s0 = torch.cuda.current_stream().cuda_stream
+    ctx.evaluate_device(t1, n1, first=0, d_amp=ser1.data_ptr(), stream=s0)
+    ctx.evaluate_device(t2, n2, d_assignments=words.data_ptr(), d_amp=ser2.data_ptr(), stream=s0)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        c1 = torch.zeros_like(ser1)
+        c2 = torch.zeros_like(ser2)
+        torch.cuda.synchronize()
+        ctx.evaluate_device(t1, n1, first=0, d_amp=c1.data_ptr(), stream=sa.cuda_stream)
+        ctx.evaluate_device(t2, n2, d_assignments=words.data_ptr(), d_amp=c2.data_ptr(), stream=sb.cuda_stream)
+        ctx.evaluate_device(t1, n1, first=0, term_begin=0, term_end=3000, d_amp=c1.data_ptr(),
+                            stream=sa.cuda_stream)  # overwrites c1 with the first half ...
+        ctx.evaluate_device(t1, n1, first=0, term_begin=3000, d_amp=c1.data_ptr(), flags=P.ACCUMULATE,
+                            stream=sa.cuda_stream)  # ... and adds the second half
+        torch.cuda.synchronize()
+        assert torch.equal(c2, ser2)
+        d = (c1 - ser1).abs().max().item()
+        assert d <= 1e-13 * ser1.abs().max().item()
+
+
+def test_accumulate_needs_amplitudes(ctx):
+    import torch
+    t = ctx.compile_bit_table(synth.generate(8, 20, 2, 8, 1))
+    prob = torch.zeros(256, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(P.Error):
+        ctx.evaluate_device(t, 256, d_prob=prob.data_ptr(), flags=P.ACCUMULATE)
+
+
+def _sanitize(tool, code, env=None, timeout=900):
+    cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "99", "--print-limit", "20",
+           sys.executable, "-c", code]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
+                         env={**os.environ, **(env or {})})
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    return out
+
+
+SMOKE = "import sys; sys.path.insert(0, '.'); import __graft_entry__ as g; g.smoke()"
+# the bit-sliced kernel with shared-memory accumulators (PZX_ACC=smem) and the
+# POPC / sorted / warp-chunk kernels on small tables: racecheck's shadow memory
+# covers shared memory, so these are the variants it can see into
+SMALL = ("import sys; sys.path.insert(0, '.'); import numpy as np; import paper_2403_06777_b200 as P; "
+         "from paper_2403_06777_b200 import synth; c = P.Context(0); e = synth.generate(12, 300, 4, 40, 5); "
+         "t = c.compile_bit_table(e); a = c.evaluate_range(t, 0, 1 << 14, flags=P.KERNEL_SLICE); "
+         "b = c.evaluate_range(t, 0, 1 << 12, flags=P.KERNEL_GENERAL); "
+         "w = np.random.default_rng(0).integers(0, 1 << 12, 5000, dtype=np.uint64); "
+         "s = c.evaluate_batch(t, w, flags=P.KERNEL_SORTED); g = c.evaluate_batch(t, w, flags=P.KERNEL_GENERAL); "
+         "assert np.allclose(a[:4096], b, rtol=0, atol=1e-12 * np.abs(b).max()); "
+         "assert np.allclose(s, g, rtol=0, atol=1e-12 * np.abs(g).max()); print('small ok')")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_sanitizer_smoke(tool):
+    """smoke() (enumerated warp-chunk, POPC, TMEM bit-sliced, sorted, exact and
+    exact term-split kernels) under compute-sanitizer: zero errors."""
+    out = _sanitize(tool, SMOKE)
+    assert "smoke ok" in out
+
+
+def test_sanitizer_racecheck_smem_variants():
+    out = _sanitize("racecheck", SMALL, env={"PZX_ACC": "smem"})
+    assert "small ok" in out
+
+
+def test_sanitizer_memcheck_smem_variants():
+    out = _sanitize("memcheck", SMALL, env={"PZX_ACC": "smem"})
+    assert "small ok" in out
+
+
+# ---------------------------------------------------------------------------
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_worker(rank, world, port, q):
+    """One rank of the term split, its kernels on cuda:0 (the box's only GPU),
+    gloo carrying CUDA tensors between the ranks."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import paper_2403_06777_b200 as PP
+    from paper_2403_06777_b200 import dist as D
+    from paper_2403_06777_b200 import synth as S
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = PP.Context(0)
+        e = S.generate(14, 3000, 8, 40, 4242)
+        n = 1 << 14
+        fn = D.gpu_partial_fn(ctx, e, n, first=0)
+        summed = D.evaluate_term_split(fn, e.term_offset)
+        det = D.evaluate_term_split(fn, e.term_offset, deterministic=True)
+        words = np.random.default_rng(1).integers(0, 1 << 14, 512, dtype=np.uint64)
+        ex = D.evaluate_term_split_exact(D.gpu_exact_partial_fn(ctx, e, words), e.term_offset,
+                                         D.gpu_exact_sum_fn(ctx))
+        if rank == 0:
+            t = ctx.compile_bit_table(e)
+            full = ctx.evaluate_range(t, 0, n)
+            full_ex = ctx.evaluate_exact(t, words)
+            q.put((summed.cpu().numpy().view(np.complex128), det.cpu().numpy().view(np.complex128), full,
+                   ex.cpu().numpy(), full_ex))
+        dist.barrier()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_term_split_gpu_partials_over_gloo(world):
+    """dist.gpu_partial_fn + combine_partials (all-reduce and deterministic
+    all-gather) and gpu_exact_partial_fn + combine_exact_partials with
+    gpu_exact_sum_fn, `world` ranks on cuda:0: equal to the unsplit table."""
+    import torch.multiprocessing as mp
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.SimpleQueue()
+    mp.start_processes(_rank_worker, args=(world, _free_port(), q), nprocs=world, join=True, start_method="spawn")
+    summed, det, full, ex, full_ex = q.get()
+    scale = np.abs(full).max()
+    assert np.max(np.abs(summed - full)) <= 1e-12 * scale
+    assert np.max(np.abs(det - full)) <= 1e-12 * scale
+    assert np.array_equal(ex, full_ex)
