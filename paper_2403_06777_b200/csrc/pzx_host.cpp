@@ -1094,6 +1094,19 @@ pzx_status pzx_create(int device, pzx_ctx** out) {
     if ((st = cuda_err(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device), "device query"))) return st;
     c->n_sm = nsm > 0 ? nsm : 148;
     if ((st = cuda_err(c.get(), cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream"))) return st;
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    if ((st = cuda_err(c.get(), cudaMemPoolCreate(&c->pool, &pp), "scratch pool"))) {
+        cudaStreamDestroy(c->stream);
+        return st;
+    }
+    // keep freed scratch in the pool across synchronisations (a C2 call takes
+    // ~0.6 GB of term-chunk partials; re-mapping it every call would cost ms)
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
     *out = c.release();
     return PZX_OK;
 }
@@ -1105,6 +1118,9 @@ void pzx_destroy(pzx_ctx* ctx) {
     for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg, ctx->d_sort, ctx->d_xout})
         if (p) cudaFree(p);
     cudaStreamDestroy(ctx->stream);
+    // pending stream-ordered frees on callers' streams: the driver releases
+    // the pool once they have completed
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
 }
 
