@@ -1020,7 +1020,7 @@ __device__ __forceinline__ uint32_t planes_parity(uint32_t mask, uint32_t plane_
 // table C * w^j (8 entries) is built once per warp, then every live
 // assignment adds C * w^j' * (stuff from S, A, B) into its fp64 accumulator in
 // shared memory.
-template <bool P64, bool RAND, int NT, bool TM = false>
+template <bool P64, bool RAND, int NT, bool TM = false, bool DBG = false>
 __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t, const LaunchReq r) {
     static_assert(!TM || NT == 128, "TMEM accumulators: one warp per TMEM lane quarter");
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         if (code & kSlicePiFlag) K.bump_a(vpi);
                         if (code & kSlicePipFlag) K.bump_b(vpip);
                         if (code & kEndFlag) {
-                            if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
+                            if constexpr (DBG) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                             slice_term_epilogue<NT, TM, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                         }
                     }
@@ -1153,7 +1153,7 @@ __global__ void __launch_bounds__(NT, TM ? 4 : 1) k_eval_slice(const DevTable t,
                         if (code & kSlicePiFlag) K.bump_a(vpi);
                         if (code & kSlicePipFlag) K.bump_b(vpip);
                         if (code & kEndFlag) {
-                            if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
+                            if constexpr (DBG) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                             slice_term_epilogue<NT, TM>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                         }
                     }
@@ -1193,7 +1193,7 @@ size_t slicewc_smem_bytes(const DevTable& t) {
     return b > kTmemCtaSmem ? b : kTmemCtaSmem;
 }
 
-template <bool P64>
+template <bool P64, bool DBG = false>
 __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTable t, const LaunchReq r) {
     constexpr int NT = kSliceThreads;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1275,7 +1275,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
                     if (code & kEndFlag) {
-                        if (r.d_dbg5) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
+                        if constexpr (DBG) debug_dump_codes<NT, false>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                         slice_term_epilogue<NT, true, true>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                     }
                 }
@@ -1450,7 +1450,7 @@ size_t sorted_smem_bytes(const DevTable& t) {
 }
 
 
-template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads>
+template <bool TM = false, int G = kSortedGroups, int NT = kSliceThreads, bool DBG = false>
 __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1) k_eval_sorted(const DevTable t,
                                                                                              const LaunchReq r) {
     static_assert(!TM || NT == 128 || NT == 256, "TMEM: 4 or 8 warps per CTA");
@@ -1560,7 +1560,7 @@ __global__ void __launch_bounds__(NT, TM ? (NT > 128 ? 2 : (G > 4 ? 3 : 4)) : 1)
                     if (code & kSlicePiFlag) K.bump_a(vpi);
                     if (code & kSlicePipFlag) K.bump_b(vpip);
                     if (code & kEndFlag) {
-                        if (r.d_dbg5) debug_dump_codes<NT, (NT > 128)>(r, tc.next - 2, off, J0, J1, J2, Z, K);
+                        if constexpr (DBG) debug_dump_codes<NT, (NT > 128)>(r, tc.next - 2, off, J0, J1, J2, Z, K);
                         slice_term_epilogue<NT, TM, true, (NT > 128)>(tc, t.sterm_c, L, crot, acc, J0, J1, J2, Z, K);
                     }
                 }
@@ -1687,6 +1687,10 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
                                : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
         auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide, 256> : k_eval_sorted<false, kSortedGroupsWide>)
                          : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
+        if (r.d_dbg5) {  // plane-dump variant (pzx_debug_slice_codes): TMEM builds only
+            if (!tm) return cudaErrorNotSupported;
+            kern = wide ? k_eval_sorted<true, kSortedGroupsWide, 256, true> : k_eval_sorted<true, kSortedGroups, 128, true>;
+        }
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         kern<<<grid, sorted_threads(r.sorted_groups), sm, r.stream>>>(t, r);
@@ -1694,9 +1698,10 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
     }
     if (kc == KC_SLICEWC) {
         const size_t sm = slicewc_smem_bytes<P64>(t);
-        cudaError_t e = cudaFuncSetAttribute(k_eval_slice_wc<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        auto kern = r.d_dbg5 ? k_eval_slice_wc<P64, true> : k_eval_slice_wc<P64>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
-        k_eval_slice_wc<P64><<<dim3(grid.x, grid.y / kWarpChunks), kSliceThreads, sm, r.stream>>>(t, r);
+        kern<<<dim3(grid.x, grid.y / kWarpChunks), kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     if (kc == KC_SLICE2) {
@@ -1717,6 +1722,10 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
                   : small ? k_eval_slice<P64, false, 32>
                   : tm    ? k_eval_slice<P64, false, 128, true>
                           : k_eval_slice<P64, false, 128>;
+        if (r.d_dbg5) {  // plane-dump variant (pzx_debug_slice_codes): the 128-thread TMEM kernel only
+            if (rnd || small || !tm) return cudaErrorNotSupported;
+            kern = k_eval_slice<P64, false, 128, true, true>;
+        }
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         kern<<<grid, small ? 32 : 128, sm, r.stream>>>(t, r);
