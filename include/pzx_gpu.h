@@ -312,6 +312,36 @@ pzx_status pzx_debug_slice_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_
                                  uint64_t n, uint64_t term_begin, uint64_t term_end, uint32_t flags,
                                  pzx_term_code* out);
 
+/* ---- host parametric reducer (SPEC zx-core S:67-84,
+ * rewrite-engine S:131-244, decomposer S:246-317) ------------------------
+ * A Clifford+T circuit (gate set of SPEC Circuit) is turned into a
+ * closed polar-parameterised ZX diagram, Clifford-simplified (local
+ * complementation, pivoting, state copy, identity removal -- parameter-
+ * agnostic, emitting Node / PhasePair / HalfPi / PiPair subterms) and
+ * stabiliser-decomposed into the leaf-term list pzx_table_upload_expr takes:
+ * the reference's leaf form (diagram.hpp:70-77: scalar_ x pending_). Runs on
+ * all host threads; the term order is deterministic. */
+enum { PZX_G_H = 0, PZX_G_X, PZX_G_Z, PZX_G_S, PZX_G_SDG, PZX_G_T, PZX_G_TDG, PZX_G_CNOT, PZX_G_CZ,
+       PZX_G_RZ /* k * pi/4 */ };
+typedef struct { uint8_t op, q0, q1, k; } pzx_gate;
+/* mode: PZX_REDUCE_AMPLITUDE: <out| U |in>; PZX_REDUCE_DOUBLED: the doubled
+ * marginal <in| U^dag (|a><a| (x) I) U |in> (SPEC double_diagram).
+ * in_spec / out_spec per qubit: 0 / 1 a fixed bit, 2 + p parameter p (bit p
+ * of the assignment word), -1 (out_spec, doubled mode only) an unmeasured
+ * (traced) qubit; in_spec NULL = |0...0>. max_terms: PZX_E_CAPACITY beyond
+ * (0 = 2^26). Without parameters the leaves are summed exactly into ONE
+ * constant term (the non-parametric path: one amplitude per reduction). */
+enum { PZX_REDUCE_AMPLITUDE = 0, PZX_REDUCE_DOUBLED = 1 };
+typedef struct pzx_expr pzx_expr;
+pzx_status pzx_circuit_reduce(uint32_t n_qubits, const pzx_gate* gates, uint64_t n_gates, const int32_t* in_spec,
+                              const int32_t* out_spec, uint32_t mode, uint64_t max_terms, pzx_expr** out);
+/* the expression as a pzx_expr_view; the pointers stay valid until pzx_expr_free */
+pzx_status pzx_expr_get_view(const pzx_expr* e, pzx_expr_view* view);
+/* T-count of the input, T-like spiders left after the first Clifford
+ * simplification, wall seconds of the reduction */
+pzx_status pzx_expr_info(const pzx_expr* e, uint32_t* t_count, uint32_t* t_after_simp, double* seconds);
+void pzx_expr_free(pzx_expr* e);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,8 @@ EXPORTS = (
     "pzx_group_create", "pzx_group_destroy", "pzx_group_last_error", "pzx_group_upload_expr", "pzx_group_table_free",
     "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex", "pzx_evaluate_exact",
     "pzx_evaluate_exact_range", "pzx_ringquad_sum", "pzx_ringquad_sum_device", "pzx_table_slice_stats",
-    "pzx_last_kernel", "pzx_debug_slice_codes",
+    "pzx_last_kernel", "pzx_debug_slice_codes", "pzx_circuit_reduce", "pzx_expr_get_view", "pzx_expr_info",
+    "pzx_expr_free",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -128,6 +129,12 @@ def lib() -> C.CDLL:
     L.pzx_last_kernel.argtypes = [vp, i32p, i32p, i32p]
     L.pzx_debug_slice_codes.argtypes = [vp, vp, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
                                         C.POINTER(TermCode)]
+    L.pzx_circuit_reduce.argtypes = [C.c_uint32, vp, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                     C.c_uint32, C.c_uint64, C.POINTER(vp)]
+    L.pzx_expr_get_view.argtypes = [vp, C.POINTER(ExprView)]
+    L.pzx_expr_info.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+    L.pzx_expr_free.argtypes = [vp]
+    L.pzx_expr_free.restype = None
     _lib = L
     return L
 

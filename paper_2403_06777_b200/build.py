@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES_CU = ["pzx_kernels.cu", "pzx_microbench.cu"]
-SOURCES_CPP = ["pzx_host.cpp", "pzx_group.cpp"]
+SOURCES_CPP = ["pzx_host.cpp", "pzx_group.cpp", "pzx_reduce.cpp"]
 HEADERS = ["pzx_internal.h", "pzx_math.hpp", "pzx_classes.h", "pzx_slice_dispatch.inc"]
 
 

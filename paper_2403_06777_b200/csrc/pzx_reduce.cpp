@@ -400,9 +400,63 @@ Ph spec_phase(int32_t s) {  // 0 / 1 fixed bit, 2 + p parameter p
     return Ph{0, uint64_t(1) << (s - 2)};
 }
 
+// ---------------------------------------------------------- expressions ----
+// exact sum of leaf scalars (parameter-free reductions: the non-parametric
+// path needs only the value), value = sum_i c_i w^i * 2^e
+struct ExactSum {
+    i128 c[4] = {0, 0, 0, 0};
+    int e = 0;
+    bool any = false, ok = true;
+    static bool shl(i128& v, int s) {
+        for (; s > 0; --s) {
+            if (v > (i128(1) << 120) || v < -(i128(1) << 120)) return false;
+            v *= 2;
+        }
+        return true;
+    }
+    void add(const Scalar& x) {
+        if (x.num.zero()) return;
+        Zw n = x.num;
+        int s2 = x.s2;
+        if (s2 & 1) { n = zw_mul(n, zw(0, 1, 0, -1)); s2 -= 1; }
+        const int h = s2 / 2;
+        i128 v[4] = {n.c[0], n.c[1], n.c[2], n.c[3]};
+        if (!any) { for (int i = 0; i < 4; ++i) c[i] = v[i]; e = h; any = true; return; }
+        if (h < e) {
+            for (int i = 0; i < 4; ++i) ok = ok && shl(c[i], e - h);
+            e = h;
+        }
+        for (int i = 0; i < 4; ++i) {
+            ok = ok && shl(v[i], h - e);
+            c[i] += v[i];
+        }
+    }
+    void merge(const ExactSum& o) {
+        if (!o.any) return;
+        ok = ok && o.ok;
+        Scalar tmp;  // add o term by term at its own exponent
+        if (!any) { *this = o; return; }
+        const int h = o.e;
+        i128 v[4] = {o.c[0], o.c[1], o.c[2], o.c[3]};
+        if (h < e) {
+            for (int i = 0; i < 4; ++i) ok = ok && shl(c[i], e - h);
+            e = h;
+        }
+        for (int i = 0; i < 4; ++i) {
+            ok = ok && shl(v[i], h - e);
+            c[i] += v[i];
+        }
+        (void)tmp;
+    }
+    // (c0 + c1 w + c2 w^2 + c3 w^3) 2^e = (2c0 + (c1 - c3) sqrt2 + i(2c2 + (c1 + c3) sqrt2)) / 2^(1 - e)
+    bool to_quad(Quad& q) const {
+        if (!any) { q = Quad{}; return true; }
+        return ok && quad_canon(2 * c[0], c[1] - c[3], 2 * c[2], c[1] + c[3], int64_t(1) - e, q);
+    }
+};
+
 }  // namespace
 
-// ---------------------------------------------------------- expressions ----
 struct pzx_expr {
     uint32_t n_params = 0;
     std::vector<uint64_t> off{0};
@@ -412,6 +466,8 @@ struct pzx_expr {
     uint32_t t_count = 0, t_after_simp = 0;
     double seconds = 0;
     std::string err;
+    bool sum_only = false;  // no parameters: leaves are summed into one exact scalar
+    ExactSum total;
 };
 
 namespace {
@@ -430,6 +486,11 @@ int decompose(Dg d, pzx_expr& ex, uint64_t cap, std::string& err) {
         if (!g.simp()) continue;
         if (!g.sc.ok) { err = "scalar out of int64"; return PZX_E_OVERFLOW; }
         if (g.n_alive == 0) {
+            if (ex.sum_only) {
+                ex.total.add(g.sc);
+                if (!ex.total.ok) { err = "leaf sum out of range"; return PZX_E_OVERFLOW; }
+                continue;
+            }
             Quad q;
             if (!g.sc.to_quad(q)) { err = "leaf scalar out of RingQuad range"; return PZX_E_OVERFLOW; }
             if (q.a == 0 && q.b == 0 && q.c == 0 && q.d == 0) continue;
@@ -514,6 +575,7 @@ int decompose_parallel(Dg root, pzx_expr& ex, uint64_t cap, std::string& err) {
     }
     const size_t nw = frontier.size();
     std::vector<pzx_expr> parts(nw);
+    for (auto& p : parts) p.sum_only = ex.sum_only;
     std::vector<int> st(nw, PZX_OK);
     std::vector<std::string> errs(nw);
     std::atomic<size_t> next_job{0};
@@ -530,6 +592,11 @@ int decompose_parallel(Dg root, pzx_expr& ex, uint64_t cap, std::string& err) {
     for (auto& t : th) t.join();
     for (size_t j = 0; j < nw; ++j) {
         if (st[j]) { err = errs[j]; return st[j]; }
+        if (ex.sum_only) {
+            ex.total.merge(parts[j].total);
+            if (!ex.total.ok) { err = "leaf sum out of range"; return PZX_E_OVERFLOW; }
+            continue;
+        }
         const uint64_t base = ex.kind.size();
         for (size_t i = 1; i < parts[j].off.size(); ++i) ex.off.push_back(base + parts[j].off[i]);
         auto app = [](auto& dst, const auto& src) { dst.insert(dst.end(), src.begin(), src.end()); };
@@ -603,9 +670,19 @@ pzx_status pzx_circuit_reduce(uint32_t n_qubits, const pzx_gate* gates, uint64_t
         st = PZX_OK;  // the whole value is 0: the empty expression
     } else {
         ex->t_after_simp = uint32_t(d.tcount());
-        st = decompose_parallel(std::move(d), *ex, max_terms ? max_terms : (uint64_t(1) << 30), ex->err);
+        ex->sum_only = np == 0;
+        st = decompose_parallel(std::move(d), *ex, max_terms ? max_terms : (uint64_t(1) << 26), ex->err);
     }
     if (st) return pzx_status(st);
+    if (ex->sum_only && ex->total.any) {  // one constant term: the exact value
+        Quad q;
+        if (!ex->total.to_quad(q)) return PZX_E_OVERFLOW;
+        if (q.a || q.b || q.c || q.d) {
+            const int64_t v[5] = {q.a, q.b, q.c, q.d, q.e};
+            ex->scal.assign(v, v + 5);
+            ex->off.assign({0, 0});
+        }
+    }
     ex->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = ex.release();
     return PZX_OK;

@@ -41,11 +41,23 @@ class Config:
     prob_real: bool = False
     mix: str = "general"
     exp_cap: int | None = None  # cap on the scalar's 2^-exp: keeps the reference's int64 ring_add in range
+    # (n_qubits, T-count, seed): the table is the host reducer's output for
+    # circuit.random_circuit (every output bit a parameter) instead of a
+    # synthetic term list; n_terms / n_lo / n_hi are then unused
+    circuit: tuple | None = None
 
 
 CONFIGS = {
-    "c1": Config(1, "C1: P=8, all 2^8 amplitudes (8 qubits, T=20)", 8, 1 << 10, 8, 24, 1 << 8, True),
+    # C1 (BASELINE configs[0]): the real reduction of an 8-qubit, T-count-20
+    # random circuit; all 2^8 amplitudes
+    "c1": Config(1, "C1: 8-qubit T=20 random Clifford+T circuit, all 2^8 amplitudes via parametric reduction",
+                 8, 0, 0, 0, 1 << 8, True, circuit=(8, 20, 20261018 + 1)),
     "c2": Config(2, "C2: P=20, all 2^20 amplitudes (20 qubits, T=40)", 20, 1 << 17, 16, 48, 1 << 20, True),
+    # C2 on the real reduction of a 20-qubit, T-count-40 random circuit
+    "c2r": Config(12, "C2r: 20-qubit T=40 random Clifford+T circuit, all 2^20 amplitudes via parametric reduction",
+                  20, 0, 0, 0, 1 << 20, True, circuit=(20, 40, 20261018 + 2)),
+    # the round-1 synthetic C1-shaped table (kept for the kernel tests)
+    "c1s": Config(1, "C1s: P=8 synthetic 1024-term table, all 2^8 amplitudes", 8, 1 << 10, 8, 24, 1 << 8, True),
     "c3": Config(3, "C3: P=30, 2^24 sampled probabilities (30 qubits, T=60)", 30, 1 << 18, 24, 56, 1 << 24, False,
                  exp_cap=40),
     "c4": Config(4, "C4: P=10 doubled-diagram marginals, 2^10 params (term split)", 10, 1 << 22, 32, 64, 1 << 10,
@@ -137,7 +149,10 @@ def generate_config(cfg: Config, n_terms: int | None = None, chunks: range | Non
                     workers: int | None = None) -> ScalarExpression:
     """The config's term list. Above CHUNK_TERMS terms it is the concatenation of
     chunks seeded (seed, chunk index), so a term-split rank can generate just its
-    own chunks (`chunks`) and big tables generate on several threads."""
+    own chunks (`chunks`) and big tables generate on several threads. Circuit
+    configs run the host reducer (circuit.py) on their random circuit."""
+    if cfg.circuit is not None:
+        return circuit_reduction(cfg).expr
     n = cfg.n_terms if n_terms is None else n_terms
     seed = 20261018 + cfg.cid
     if n <= CHUNK_TERMS and chunks is None:
@@ -155,11 +170,32 @@ def generate_config(cfg: Config, n_terms: int | None = None, chunks: range | Non
     return concat(parts)
 
 
+def config_circuit(cfg: Config):
+    from .circuit import random_circuit
+    n, t, seed = cfg.circuit
+    return random_circuit(n, t, seed)
+
+
+_REDUCTIONS: dict = {}
+
+
+def circuit_reduction(cfg: Config):
+    """The parametric reduction of a circuit config (cached per process): every
+    output bit q is parameter q, so the table yields all 2^n amplitudes."""
+    from .circuit import param, reduce_amplitudes
+    if cfg.name not in _REDUCTIONS:
+        c = config_circuit(cfg)
+        _REDUCTIONS[cfg.name] = reduce_amplitudes(c, [param(q) for q in range(c.n_qubits)])
+    return _REDUCTIONS[cfg.name]
+
+
 def term_row_offsets(cfg: Config) -> np.ndarray:
     """Subterm offsets [m + 1] of the whole config table without generating it:
     the term sizes are the first draw of every (chunk) generator, so this is
     cheap even for C5's 2^24 terms. Used to cut row-balanced term ranges
     (dist.term_ranges) for the term split before any rank builds its table."""
+    if cfg.circuit is not None:
+        return np.asarray(generate_config(cfg).term_offset, np.uint64) - np.uint64(0)
     seed = 20261018 + cfg.cid
     n = cfg.n_terms
     if n <= CHUNK_TERMS:
@@ -175,7 +211,7 @@ def term_row_offsets(cfg: Config) -> np.ndarray:
 def generate_config_terms(cfg: Config, t0: int, t1: int) -> ScalarExpression:
     """Terms [t0, t1) of the config table (only the chunks that overlap the
     range are generated), rebased so the slice starts at subterm 0."""
-    if cfg.n_terms <= CHUNK_TERMS:
+    if cfg.circuit is not None or cfg.n_terms <= CHUNK_TERMS:
         full = generate_config(cfg)
         c0 = 0
     else:

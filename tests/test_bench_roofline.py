@@ -36,7 +36,7 @@ def test_row_minimum_per_class_is_pinned():
 
 
 def test_c1_table_minimum_regression():
-    cfg = synth.CONFIGS["c1"]
+    cfg = synth.CONFIGS["c1s"]
     h = P.HostTable(synth.generate_config(cfg))
     ops, kinds = h.slice_stats()
     assert int(ops.sum()) == h.n_rows and int(kinds.sum()) == h.n_terms
@@ -46,7 +46,7 @@ def test_c1_table_minimum_regression():
 
 
 def test_frac_is_bounded_and_shard_invariant():
-    cfg = synth.CONFIGS["c1"]
+    cfg = synth.CONFIGS["c1s"]
     h = P.HostTable(synth.generate_config(cfg))
     ops, kinds = h.slice_stats()
     c = RL.min_counts(ops, kinds, 1 << 20)

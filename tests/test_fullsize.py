@@ -72,10 +72,13 @@ def check_slice_codes(ctx, e, t, terms, words, codes):
             assert got == ZQ.from_quad(O.term_value(oe, term, int(w), impl=IMPL)), (term, int(w))
 
 
-def test_c1_full_all_amplitudes(ctx):
-    """C1: the 1024-term table, all 256 amplitudes (warp-chunk kernel) against
-    the reference on every assignment, and bit-exact against the integer kernel."""
-    cfg = synth.CONFIGS["c1"]
+@pytest.mark.parametrize("cid", ["c1", "c1s"])
+def test_c1_full_all_amplitudes(ctx, cid):
+    """C1: the real reduction of the 8-qubit T=20 circuit (and the round-1
+    synthetic 1024-term table), all 256 amplitudes (warp-chunk kernel) against
+    the reference on every assignment, bit-exact against the integer kernel,
+    and -- for the circuit -- against the dense statevector."""
+    cfg = synth.CONFIGS[cid]
     e = synth.generate_config(cfg)
     t = ctx.compile_bit_table(e)
     amp, prob = ctx.evaluate_range(t, 0, cfg.n_assign, prob=True)
@@ -85,6 +88,9 @@ def test_c1_full_all_amplitudes(ctx):
     assert_close(amp, want)
     assert_close(prob, np.abs(want) ** 2, 2 * TOL)
     assert np.array_equal(ctx.evaluate_exact_range(t, 0, cfg.n_assign), ex)
+    if cfg.circuit is not None:
+        import statevector as SV
+        assert np.max(np.abs(amp - SV.run(synth.config_circuit(cfg)))) <= 1e-12
     # the kernel's own per-term planes, every term at 16 assignments
     pick = np.arange(0, 256, 16, dtype=np.uint64)
     codes = ctx.debug_slice_codes(t, first=0, n=cfg.n_assign)
@@ -115,6 +121,26 @@ def test_c2_full_headline_kernel(ctx):
         codes = ctx.debug_slice_codes(t, first=0, n=N, term_begin=t0, term_end=t0 + 6)
         sub = pick[::16]
         check_slice_codes(ctx, e, t, range(t0, t0 + 6), sub, codes[:, sub.astype(np.int64)])
+
+
+def test_c2r_real_circuit_all_amplitudes(ctx):
+    """C2r: the real reduction of the 20-qubit T=40 circuit, all 2^20 amplitudes
+    on the headline kernel against the dense 2^20 statevector (every amplitude),
+    the integer kernel (every amplitude) and the reference (64)."""
+    import statevector as SV
+    cfg = synth.CONFIGS["c2r"]
+    e = synth.generate_config(cfg)
+    t = ctx.compile_bit_table(e)
+    N = cfg.n_assign
+    amp = ctx.evaluate_range(t, 0, N)
+    assert ctx.last_kernel()["kernel"] == "slice"
+    sv = SV.run(synth.config_circuit(cfg))
+    assert np.max(np.abs(amp - sv)) <= 1e-12 * np.sqrt(np.mean(np.abs(sv) ** 2)) * 1e3
+    ex = ctx.evaluate_exact_range(t, 0, N)
+    assert_close(amp, exact_to_complex(ex))
+    pick = np.random.default_rng(5).choice(N, 64, replace=False).astype(np.uint64)
+    ex_ref, want = O.eval_batch(e, pick, THREADS, impl=IMPL)
+    assert np.array_equal(ex[pick.astype(np.int64)], ex_ref)
 
 
 def test_c4_full_marginal_kernel(ctx):
@@ -170,7 +196,8 @@ def test_c5_full_term_split(ctx):
                         flags=P.ACCUMULATE, stream=st)
     torch.cuda.synchronize()
     assert_close(acc.cpu().numpy().view(np.complex128), amp, 1e-13, 1.0)
-    codes = ctx.debug_slice_codes(t, sub[:256], term_begin=t.n_terms - 3, term_end=t.n_terms)
+    codes = ctx.debug_slice_codes(t, words, term_begin=t.n_terms - 3, term_end=t.n_terms)  # the bench batch
+    assert ctx.last_kernel()["kernel"] == "sorted"
     check_slice_codes(ctx, oe, t, range(t.n_terms - 3, t.n_terms), sub[:8], codes[:, :8])
     t.free()
     # exact halves on their own tables, summed on the device

@@ -167,7 +167,7 @@ def test_no_device_means_no_evaluation():
 
 
 def test_synth_is_deterministic_and_within_invariants():
-    cfg = synth.CONFIGS["c1"]
+    cfg = synth.CONFIGS["c1s"]
     a = synth.generate_config(cfg)
     b = synth.generate_config(cfg)
     for f in ("term_offset", "term_scalar", "kind", "psi_k", "psi_mask", "phi_k", "phi_mask"):
