@@ -79,7 +79,8 @@ enum {
     PZX_KERNEL_SLICE = 1u << 10,  /* force the bit-sliced enumerated kernel        */
     PZX_KERNEL_SLICE_RAND = 1u << 11, /* force the plane-XOR bit-sliced kernel for any word list */
     PZX_KERNEL_SORTED = 1u << 12, /* force sort + bit-sliced Four-Russians kernel (any word list) */
-    PZX_KERNEL_SLICE2 = 1u << 13  /* force the two-slice (64 assignments / thread) enumerated kernel */
+    PZX_KERNEL_SLICE2 = 1u << 13, /* force the two-slice (64 assignments / thread) enumerated kernel */
+    PZX_KERNEL_PAGE = 1u << 14    /* force the page-layout enumerated kernel (branch-free row families) */
 };
 
 typedef struct pzx_ctx pzx_ctx;
@@ -165,6 +166,13 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
  * row), term_kinds = terms whose epilogue is kind-free / lambda-only / with a
  * pi or pi' row. Either pointer may be NULL. */
 pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]);
+/* Host-only tables (pzx_table_compile_host): the page layout of the
+ * enumerated page kernel -- *n_slots 32-byte records (8 x u32 each; slots may
+ * be NULL to query the size), the header slot of every term, the w^j folded
+ * into each term's page constant, and the rows per family {constraint,
+ * generic, dispatch, dropped}. PZX_E_CAPACITY: the table has no page layout. */
+pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* n_slots, uint32_t* term_slot,
+                                 uint8_t* jfold, uint64_t family_rows[4]);
 /* Folded exact constant C'_t (a,b,c,d,exp), sqrt2 exponent E_t and the count
  * nLM_t of lambda/mu rows of term t (see pzx_term_code). */
 pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],

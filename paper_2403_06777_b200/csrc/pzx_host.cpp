@@ -167,6 +167,17 @@ struct HostTable {
     uint64_t term_kinds[3] = {};            // terms by epilogue: kind-free, lambda only, with pi / pi'
     bool want_srows = true;                 // build the bit-sliced layout (enumerated batches)
     bool want_qrows = true;                 // build the sorted-batch layout (word lists, n_params <= 32)
+    // page layout of the enumerated page kernel (n_params <= 32):
+    // kPageSlots-slot pages of 32-byte records, terms never straddle a page
+    bool want_prows = true;
+    std::vector<uint4> prows;               // 2 x uint4 per slot
+    std::vector<uint32_t> term_slot;        // header slot of every term
+    std::vector<uint8_t> jp_t;              // per term: the j offset folded into its page constant
+    struct PendRow { uint64_t psi, phi; uint32_t op; };
+    std::vector<PendRow> pend;              // rows of the open term
+    uint32_t page_fill = 0;                 // slots used in the open page
+    int64_t last_hdr = -1;                  // slot of the last header written
+    uint64_t page_rows[4] = {};             // rows by family: constraint, G, dispatch, dropped
     bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
@@ -221,6 +232,7 @@ void choose_layouts(HostTable& h, uint64_t rows_est) {
     else sl = rows_est <= (uint64_t(1) << 28), so = true;
     h.want_srows = sl;
     h.want_qrows = so && h.n_params <= 32;
+    h.want_prows = sl && h.n_params <= 32 && std::getenv("PZX_NO_PAGES") == nullptr;
 }
 
 void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, uint32_t pat, uint8_t sw,
@@ -237,6 +249,7 @@ void push_device_row(HostTable& h, uint64_t psi, uint64_t phi, uint32_t code, ui
     const uint32_t op = unit ? uint32_t(kSliceUnitOp) : cls * 2u + (phi == 0 ? 1u : 0u);
     h.jb_term += kSliceJbase[op];
     h.op_rows[op] += 1;
+    if (h.want_prows && !unit) h.pend.push_back(HostTable::PendRow{psi, phi, op});
     h.kinds_term |= uint32_t(kSliceKindFlags[op]);
     const uint32_t scode = op | uint32_t(kSliceKindFlags[op]);
     if (h.want_srows) {
@@ -272,6 +285,137 @@ void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
     push_device_row(h, pr.psi, pr.phi, uint32_t(cls) * 16u, walsh_pattern(pr.psi, pr.phi), sw, 0);
 }
 
+// ---- page layout (enumerated page kernel) -------------------
+// Every row of a term is put in one of three families by the values of its
+// reachable variants (p, q) = parities of (psi, phi) (pzx_classes.h):
+//   C (constraint): one parity, one variant zero           -> Z |= X
+//   G (generic monomial): value w^(c0 + (k + 4p')(q' ^ inv)) sqrt2^e g, g constant
+//       (every class with ka or kb in {0,4}: 28 of 64, ~83 % of the rows of the
+//       BASELINE tables)                                   -> branch-free J += (k + 4p')q~
+//   D (dispatch): zero-pair / lambda / pi / pi' rows       -> the generated class bodies
+// and rows whose reachable variants are equal are dropped (their w^j goes
+// into the term constant like every c0; their sqrt2^e and mu are already in
+// E_t / nLM_t). Records (8 x u32):
+//   header: {C_page (double2), counts nc | ng << 8 | nd << 16 | last_in_page << 24, 0, 0, 0}
+//   C: {W ^ zc, ~(W ^ zc), 0, 0, 0, 0, psi, 0}
+//   G: {A = W(x) ^ K2, ~A, B = W(y) ^ INV, ~B, K0, K1, x-mask, y-mask}
+//   D: {W(psi), ~W(psi), W(phi), ~W(phi), op | kind flags, op, psi, phi}
+// W = Walsh32 of the mask (bit g = parity(mask & g)); Kc = all ones when bit c of k is set.
+struct PageRec { int fam; uint32_t w[8]; int jfold; };
+
+PageRec classify_page_row(uint64_t psi, uint64_t phi, uint32_t op) {
+    PageRec r{3, {0, 0, 0, 0, 0, 0, 0, 0}, 0};
+    const SliceOp so = slice_op(int(op));
+    const bool single = phi == 0;
+    const int kinds = so.lam_tt | so.pi_tt | so.pip_tt;
+    auto jv = [&](int v) { return (so.jbase + so.w[v]) & 7; };
+    const uint32_t Wp = walsh32(psi), Wq = walsh32(phi);
+    auto dispatch = [&] {
+        r.fam = 3;
+        r.w[0] = Wp; r.w[1] = ~Wp; r.w[2] = Wq; r.w[3] = ~Wq;
+        r.w[4] = op | uint32_t(kSliceKindFlags[op]); r.w[5] = op; r.w[6] = uint32_t(psi); r.w[7] = uint32_t(phi);
+        r.jfold = so.jbase;
+        return r;
+    };
+    if (kinds) return dispatch();
+    if (single) {
+        const int z = so.zero_tt & 3;
+        if (z == 1 || z == 2) {  // the other variant survives: its w^j is a constant
+            const uint32_t zc = z == 2 ? 0u : ~0u;  // Z |= X (variant 1 zero) or ~X (variant 0 zero)
+            r.fam = 0;
+            r.w[0] = Wp ^ zc; r.w[1] = ~(Wp ^ zc); r.w[6] = uint32_t(psi);
+            r.jfold = jv(z == 2 ? 0 : 1);
+            return r;
+        }
+        if (z) return dispatch();
+        if (jv(0) == jv(1)) { r.fam = 4; r.jfold = jv(0); return r; }  // assignment-independent
+        const int k = (jv(1) - jv(0)) & 7;  // J += k * p: a G row with x = 0, q~ = p
+        r.fam = 1;
+        const uint32_t K2 = (k & 4) ? ~0u : 0u;
+        r.w[0] = K2; r.w[1] = K2; r.w[2] = Wp; r.w[3] = ~Wp;
+        r.w[4] = (k & 1) ? ~0u : 0u; r.w[5] = (k & 2) ? ~0u : 0u; r.w[6] = 0; r.w[7] = uint32_t(psi);
+        r.jfold = jv(0);
+        return r;
+    }
+    if (so.zero_tt) return dispatch();
+    // j(p, q) = c0 + (k + 4p')(q' ^ inv), (p', q') = swap ? (q, p) : (p, q)
+    for (int sw = 0; sw < 2; ++sw)
+        for (int inv = 0; inv < 2; ++inv)
+            for (int k = 0; k < 8; ++k) {
+                const int c0 = (jv(0) - k * inv) & 7;  // (p, q) = (0, 0): p' = 0, q' = 0
+                bool ok = true;
+                for (int v = 0; v < 4 && ok; ++v) {
+                    const int p = v & 1, q = v >> 1;
+                    const int pp = sw ? q : p, qq = (sw ? p : q) ^ inv;
+                    ok = jv(v) == ((c0 + (k + 4 * pp) * qq) & 7);
+                }
+                if (!ok) continue;
+                const uint64_t xm = sw ? phi : psi, ym = sw ? psi : phi;
+                const uint32_t K2 = (k & 4) ? ~0u : 0u, INV = inv ? ~0u : 0u;
+                r.fam = 1;
+                r.w[0] = walsh32(xm) ^ K2; r.w[1] = ~r.w[0];
+                r.w[2] = walsh32(ym) ^ INV; r.w[3] = ~r.w[2];
+                r.w[4] = (k & 1) ? ~0u : 0u; r.w[5] = (k & 2) ? ~0u : 0u;
+                r.w[6] = uint32_t(xm); r.w[7] = uint32_t(ym);
+                r.jfold = c0;
+                return r;
+            }
+    return dispatch();
+}
+
+void page_pad(HostTable& h) {
+    if (h.page_fill == 0) return;
+    if (h.last_hdr >= 0) h.prows[2 * size_t(h.last_hdr) + 1].x |= 1u << 24;  // last term of its page
+    while (h.page_fill < uint32_t(kPageSlots)) {
+        h.prows.push_back(make_uint4(0, 0, 0, 0));
+        h.prows.push_back(make_uint4(0, 0, 0, 0));
+        ++h.page_fill;
+    }
+    h.page_fill = 0;
+}
+
+// the open term's rows -> one header + C, G, D records; returns its j fold
+int page_term(HostTable& h, const C128& cpp) {
+    std::vector<PageRec> fam[3];
+    int jf = 0;
+    for (const auto& pr : h.pend) {
+        const PageRec r = classify_page_row(pr.psi, pr.phi, pr.op);
+        jf += r.jfold;
+        if (r.fam == 4) { h.page_rows[3] += 1; continue; }
+        const int f = r.fam == 0 ? 0 : r.fam == 1 ? 1 : 2;
+        h.page_rows[f] += 1;
+        fam[f].push_back(r);
+    }
+    h.pend.clear();
+    const uint32_t n = uint32_t(1 + fam[0].size() + fam[1].size() + fam[2].size());
+    if (n > uint32_t(kPageSlots)) {  // a term must fit one page: no page layout for this table
+        h.want_prows = false;
+        std::vector<uint4>().swap(h.prows);
+        std::vector<uint32_t>().swap(h.term_slot);
+        return jf & 7;
+    }
+    if (h.page_fill + n > uint32_t(kPageSlots)) page_pad(h);
+    const C128 wj = zw_to_c128(zw_pow_w(jf & 7));
+    const C128 c = cmul(cpp, wj);
+    const double re = double(c.re), im = double(c.im);
+    uint32_t q[4];
+    std::memcpy(q, &re, 8);
+    std::memcpy(q + 2, &im, 8);
+    h.term_slot.push_back(uint32_t(h.prows.size() / 2));
+    h.last_hdr = int64_t(h.prows.size() / 2);
+    h.prows.push_back(make_uint4(q[0], q[1], q[2], q[3]));
+    h.prows.push_back(make_uint4(uint32_t(fam[0].size()) | uint32_t(fam[1].size()) << 8 |
+                                     uint32_t(fam[2].size()) << 16, 0, 0, 0));
+    for (int f = 0; f < 3; ++f)
+        for (const PageRec& r : fam[f]) {
+            h.prows.push_back(make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]));
+            h.prows.push_back(make_uint4(r.w[4], r.w[5], r.w[6], r.w[7]));
+        }
+    h.page_fill += n;
+    if (h.page_fill == uint32_t(kPageSlots)) page_pad(h);
+    return jf & 7;
+}
+
 uint32_t& code_word(HostTable& h, uint64_t i) { return h.n_params <= 32 ? h.rows[i].z : h.rows[2 * i + 1].x; }
 
 // Close a term: a term without assignment-dependent rows gets one unit row
@@ -304,6 +448,7 @@ int finish_term(HostTable& h, const Quad& c, int e, int lm, uint64_t row0) {
     h.term_c.push_back(double(v.re));
     h.term_c.push_back(double(v.im));
     h.jb_t.push_back(uint8_t(h.jb_term & 7));
+    if (h.want_prows) h.jp_t.push_back(uint8_t(page_term(h, v)));
     const C128 wj = zw_to_c128(zw_pow_w(h.jb_term & 7));  // slice kernel: w^(sum of row jbase)
     const C128 vs = cmul(v, wj);
     h.sterm_c.push_back(double(vs.re));
@@ -462,6 +607,21 @@ void merge_into(HostTable& h, HostTable& part) {
     app(h.unit, part.unit);
     h.max_rows = std::max(h.max_rows, part.max_rows);
     for (int i = 0; i < kSliceOps; ++i) h.op_rows[i] += part.op_rows[i];
+    // pages: both sides padded to whole pages, the part's slots rebased
+    if (h.want_prows && part.want_prows) {
+        page_pad(h);
+        page_pad(part);
+        const uint32_t base_slot = uint32_t(h.prows.size() / 2);
+        for (uint32_t ts : part.term_slot) h.term_slot.push_back(base_slot + ts);
+        app(h.prows, part.prows);
+        app(h.jp_t, part.jp_t);
+        if (part.last_hdr >= 0) h.last_hdr = int64_t(base_slot) + part.last_hdr;
+        for (int i = 0; i < 4; ++i) h.page_rows[i] += part.page_rows[i];
+    } else if (h.want_prows) {
+        h.want_prows = false;
+        std::vector<uint4>().swap(h.prows);
+        std::vector<uint32_t>().swap(h.term_slot);
+    }
     for (int i = 0; i < 3; ++i) h.term_kinds[i] += part.term_kinds[i];
 }
 
@@ -475,7 +635,11 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
     choose_layouts(h, rows_est);
     unsigned nth = std::max(1u, std::thread::hardware_concurrency());
     nth = unsigned(std::min<uint64_t>(nth, std::max<uint64_t>(1, m / 2048)));
-    if (nth <= 1) return compile_expr_range(v, 0, m, h, err);
+    if (nth <= 1) {
+        const int st = compile_expr_range(v, 0, m, h, err);
+        if (!st && h.want_prows) page_pad(h);
+        return st;
+    }
     std::vector<HostTable> parts(nth);
     std::vector<int> st(nth, PZX_OK);
     std::vector<std::string> errs(nth);
@@ -484,6 +648,7 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
         parts[i].n_params = h.n_params;
         parts[i].want_srows = h.want_srows;
         parts[i].want_qrows = h.want_qrows;
+        parts[i].want_prows = h.want_prows;
         parts[i].simplify = h.simplify;
         th.emplace_back([&, i] {
             st[i] = compile_expr_range(v, m * i / nth, m * (i + 1) / nth, parts[i], errs[i]);
@@ -492,7 +657,11 @@ int compile_expr(const pzx_expr_view* v, HostTable& h, std::string& err) {
     for (auto& x : th) x.join();
     for (unsigned i = 0; i < nth; ++i)
         if (st[i]) { err = errs[i]; return st[i]; }
-    for (unsigned i = 0; i < nth; ++i) merge_into(h, parts[i]);
+    for (unsigned i = 0; i < nth; ++i) {
+        if (i == 0) h.want_prows = parts[0].want_prows;
+        merge_into(h, parts[i]);
+    }
+    if (h.want_prows) page_pad(h);
     return PZX_OK;
 }
 
@@ -521,6 +690,7 @@ int compile_rows(const pzx_table_view* v, HostTable& h, std::string& err) {
         int st = finish_term(h, c, e, lm, row0);
         if (st) { err = "term has more rows than supported"; return st; }
     }
+    if (h.want_prows) page_pad(h);
     return PZX_OK;
 }
 
@@ -618,6 +788,8 @@ struct pzx_table {
     void* d_srows = nullptr;
     void* d_sterm_c = nullptr;
     void* d_qrows = nullptr;
+    void* d_prows = nullptr;
+    void* d_term_slot = nullptr;
     void* d_exact = nullptr;  // exact-evaluation tables (built on first pzx_evaluate_exact)
     ExactDev exact;
 };
@@ -668,6 +840,9 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     if ((slice_ok || sorted_ok) &&
         (st = cuda_err(ctx, upload_vec(&t->d_sterm_c, h.sterm_c), "upload slice constants"))) return st;
     if (sorted_ok && (st = cuda_err(ctx, upload_vec(&t->d_qrows, h.qrows), "upload sorted-kernel rows"))) return st;
+    const bool page_ok = slice_ok && h.want_prows && !h.prows.empty() && h.term_slot.size() == h.coef.size();
+    if (page_ok && (st = cuda_err(ctx, upload_vec(&t->d_prows, h.prows), "upload page rows"))) return st;
+    if (page_ok && (st = cuda_err(ctx, upload_vec(&t->d_term_slot, h.term_slot), "upload term slots"))) return st;
     LutLayout L;
     std::vector<unsigned char> blob = build_lut(h.max_rows, L);
     if ((st = cuda_err(ctx, upload_vec(&t->d_lut, blob), "upload lut"))) return st;
@@ -687,12 +862,17 @@ pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table*
     d.sterm_c = static_cast<const double2*>(t->d_sterm_c);
     d.sorted_ok = sorted_ok ? 1 : 0;
     d.qrows = static_cast<const uint4*>(t->d_qrows);
+    d.page_ok = page_ok ? 1 : 0;
+    d.prows = static_cast<const uint4*>(t->d_prows);
+    d.term_slot = static_cast<const uint32_t*>(t->d_term_slot);
+    d.n_pages = page_ok ? h.prows.size() / (2 * size_t(kPageSlots)) : 0;
     t->ctx = ctx;
     t->device = ctx->device;
     // the device owns the row layouts now; keep only what host-side queries use
     std::vector<uint4>().swap(h.rows);
     std::vector<uint4>().swap(h.srows);
     std::vector<uint4>().swap(h.qrows);
+    std::vector<uint4>().swap(h.prows);
     std::vector<double>().swap(h.term_c);
     std::vector<double>().swap(h.sterm_c);
     *out = t.release();
@@ -778,6 +958,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
              : (flags & PZX_KERNEL_SLICE_RAND) ? KC_SLICER
              : (flags & PZX_KERNEL_SORTED)  ? KC_SORTED
              : (flags & PZX_KERNEL_SLICE2)  ? KC_SLICE2
+             : (flags & PZX_KERNEL_PAGE)    ? KC_PAGE
                                             : KC_AUTO;
     if (r.kernel != KC_AUTO && !kernel_supported(t->dev, r, r.kernel))
         return set_err(ctx, PZX_E_INVALID, "requested kernel does not support this batch / table "
@@ -1440,7 +1621,8 @@ void pzx_table_free(pzx_table* t) {
     if (!t) return;
     if (t->device < 0) { delete t; return; }
     cudaSetDevice(t->device);
-    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows, t->d_exact})
+    for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows, t->d_exact,
+                    t->d_prows, t->d_term_slot})
         if (p) cudaFree(p);
     delete t;
 }
@@ -1452,6 +1634,21 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
     if (n_terms) *n_terms = t->dev.n_terms;
     if (n_rows) *n_rows = t->host.genuine_rows();
     if (max_term_rows) *max_term_rows = t->host.max_rows;
+    return PZX_OK;
+}
+
+pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* n_slots, uint32_t* term_slot,
+                                 uint8_t* jfold, uint64_t family_rows[4]) {
+    if (!t || !n_slots) return PZX_E_INVALID;
+    const HostTable& h = t->host;
+    if (!h.want_prows || h.term_slot.size() != h.coef.size()) { *n_slots = 0; return PZX_E_CAPACITY; }
+    if (family_rows)
+        for (int i = 0; i < 4; ++i) family_rows[i] = h.page_rows[i];
+    if (h.prows.empty() && t->device >= 0) { *n_slots = 0; return PZX_E_INVALID; }  // uploaded: host copy released
+    *n_slots = h.prows.size() / 2;
+    if (slots) std::memcpy(slots, h.prows.data(), h.prows.size() * 16);
+    if (term_slot) std::memcpy(term_slot, h.term_slot.data(), h.term_slot.size() * 4);
+    if (jfold) std::memcpy(jfold, h.jp_t.data(), h.jp_t.size());
     return PZX_OK;
 }
 
@@ -1784,12 +1981,13 @@ pzx_status pzx_debug_slice_codes(pzx_ctx* ctx, const pzx_table* t, const uint64_
     r.dbg_n = n;
     if ((st = run_eval(ctx, t, r, flags))) return st;
     const int k = ctx->last_kernel;
-    if (k != KC_SLICE && k != KC_SLICER && k != KC_SLICEWC && k != KC_SORTED)
+    if (k != KC_SLICE && k != KC_SLICER && k != KC_SLICEWC && k != KC_SORTED && k != KC_PAGE)
         return set_err(ctx, PZX_E_INVALID, "debug_slice_codes: the batch did not run on a bit-sliced kernel");
+    const std::vector<uint8_t>& jfold = k == KC_PAGE ? t->host.jp_t : t->host.jb_t;
     if ((st = cuda_err(ctx, cudaMemcpyAsync(out, ctx->d_dbg, M * n * 20, cudaMemcpyDeviceToHost, ctx->stream), "D2H"))) return st;
     if ((st = cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "debug slice codes"))) return st;
     for (uint64_t tt = 0; tt < M; ++tt) {  // the slice kernels count w' relative to each row's jbase
-        const uint32_t jb = t->host.jb_t[term_begin + tt];
+        const uint32_t jb = jfold[term_begin + tt];
         for (uint64_t i = 0; i < n; ++i) {
             pzx_term_code& c = out[tt * n + i];
             if (c.j != 0xFFFFFFFFu) c.j = (c.j + jb) & 7u;

@@ -76,14 +76,24 @@ struct DevTable {
     // of a 128-thread CTA (256-thread CTAs double them)
     const uint4* qrows = nullptr;
     int sorted_ok = 0;
+    // page layout: pages of kPageSlots x 32 B records (terms never straddle a
+    // page) and the header slot of every term (pzx_host.cpp, page_term)
+    const uint4* prows = nullptr;
+    const uint32_t* term_slot = nullptr;
+    uint64_t n_pages = 0;
+    int page_ok = 0;
 };
+
+// page layout (enumerated page kernel): pages of kPageSlots 32-byte records
+constexpr int kPageSlots = 256;
 
 constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables (dense batches)
 constexpr int kSortedGroupsWide = 6;          // parameters 0..23 via tables (sparse batches, e.g. 2^16 of 2^32)
 constexpr int kSortedLowBits = 4 * kSortedGroups;
 
 enum KernelChoice { KC_AUTO = 0, KC_GENERAL = 1, KC_GRAY = 2, KC_SLICE = 3, KC_SLICER = 4, KC_SORTED = 5, KC_SLICE2 = 6,
-                    KC_SLICEWC = 7 /* small enumerated batches: 4 warps x 4 term chunks per CTA (auto only) */ };
+                    KC_SLICEWC = 7 /* small enumerated batches: 4 warps x 4 term chunks per CTA (auto only) */,
+                    KC_PAGE = 8 /* enumerated batches on the page layout (C / G / D row families) */ };
 constexpr int kWarpChunksHost = 4;  // term chunks per CTA of the warp-chunk kernel
 
 struct LaunchReq {

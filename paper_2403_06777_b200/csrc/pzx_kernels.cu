@@ -47,6 +47,12 @@ namespace {
 
 constexpr int kTileRows = 256;
 
+// Term epilogue decode: 1 = byte-lane bit transposes (slice_epilogue_tr), 0 =
+// the round-1 nibble-spread decode (A/B builds: -DPZX_EPI_TRANSPOSE=0)
+#ifndef PZX_EPI_TRANSPOSE
+#define PZX_EPI_TRANSPOSE 1
+#endif
+
 // ------------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -818,6 +824,92 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
     }
 }
 
+// 8 bit planes -> per-assignment keys: an 8 x 8 bit transpose inside every
+// byte lane (three delta-swap stages). Before: P[c] bit (8m + k) = plane c of
+// assignment 8m + k. After: P[k] byte m bit c = plane c of assignment 8m + k,
+// i.e. byte m of P[k] is assignment 8m + k's 8-bit key. ~60 LOP3/SHF for all
+// 32 assignments x 8 planes (the nibble-spread decode it replaces took 0.75
+// instructions per plane and assignment, i.e. 192).
+__device__ __forceinline__ void transpose8_bytes(uint32_t (&P)[8]) {
+#pragma unroll
+    for (int s = 4; s > 0; s >>= 1) {
+        const uint32_t m = s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (c & s) continue;
+            const uint32_t t = ((P[c] >> s) ^ P[c + s]) & m;
+            P[c + s] ^= t;
+            P[c] ^= t << s;
+        }
+    }
+}
+
+// Term epilogue fast path, TMEM accumulators, transposed decode:
+// planes {J0 J1 J2 Z S0..S3} -> key byte (j | z << 3 | s << 4) per assignment,
+// {A0 A1 B0 B1} -> (a | b << 2). Per assignment: the key byte, C w^j from the
+// warp's crot table (zeros for Z-marked assignments) and
+//   KIND 0 (kind-free term):   acc += C w^j                     (1 LDS, 2 DADD)
+//   KIND 1 (lambda rows only): acc += C w^j (sqrt2-1)^s          (2 LDS, 2 DFMA)
+//   KIND 2 (pi / pi' rows):    acc += C w^j (sqrt2-1)^s pi^a pi'^b (2 LDS, 4 DFMA)
+// Groups of 4 consecutive assignments (16 TMEM columns) are loaded / stored
+// together; assignment 8m + 4h + r is byte m of key word 4h + r.
+template <int NT, int KIND, bool LC>
+__device__ __forceinline__ void slice_epilogue_tr(const SmemLut& L, const double2* crot, SliceAcc<NT, true>& acc,
+                                                  uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
+                                                  const KindCounters<NT, LC>& K) {
+    uint32_t Q[8] = {J0, J1, J2, Z, 0u, 0u, 0u, 0u};
+    if constexpr (KIND >= 1) {
+        Q[4] = K.S[0]; Q[5] = K.S[1]; Q[6] = K.S[2]; Q[7] = K.S[3];
+    }
+    transpose8_bytes(Q);
+    uint32_t R[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if constexpr (KIND == 2) {
+        R[0] = K.A[0]; R[1] = K.A[1]; R[2] = K.B[0]; R[3] = K.B[1];
+        transpose8_bytes(R);
+    }
+    tmem_wait_st();  // the previous term's stores have landed
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t sh = 8u * uint32_t(m);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t v[16];
+            tmem_ld16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+            double2 c[4];
+            double2 f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t b = Q[4 * h + r] >> sh;
+                c[r] = crot[b & 15u];
+                if constexpr (KIND == 1) {
+                    f[r].x = L.u[(b >> 4) & 15u];
+                } else if constexpr (KIND == 2) {
+                    f[r] = L.sab[((b >> 4) & 15u) | (((R[4 * h + r] >> sh) & 15u) << 4)];
+                }
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double2 o = v2d(v + 4 * r);
+                if constexpr (KIND == 0) {
+                    o.x += c[r].x;
+                    o.y += c[r].y;
+                } else if constexpr (KIND == 1) {
+                    o.x = fma(c[r].x, f[r].x, o.x);
+                    o.y = fma(c[r].y, f[r].x, o.y);
+                } else {
+                    o.x = fma(c[r].x, f[r].x, o.x);
+                    o.y = fma(c[r].x, f[r].y, o.y);
+                    o.x = fma(-c[r].y, f[r].y, o.x);
+                    o.y = fma(c[r].y, f[r].x, o.y);
+                }
+                d2v(o, v + 4 * r);
+            }
+            tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+        }
+    }
+}
+
 // Any counter widths: one assignment's term value (0 when Z-marked).
 template <int NT, bool LC = false>
 __device__ __forceinline__ double2 slice_value_slow(const SmemLut& L, const double2* crot, uint32_t J0, uint32_t J1,
@@ -872,6 +964,22 @@ __device__ __forceinline__ void slice_epilogue_apply(const SmemLut& L, const dou
         J2 ^= w2 ^ c1;
     }
     const bool kinds = K.any();
+#if PZX_EPI_TRANSPOSE
+    if constexpr (TM) {
+        if (!kinds) {
+            slice_epilogue_tr<NT, 0, LC>(L, crot, acc, J0, J1, J2, Z, K);
+            J0 = J1 = J2 = Z = 0;
+            return;
+        }
+        if (K.fits_fast()) {
+            if (!K.has_pi()) slice_epilogue_tr<NT, 1, LC>(L, crot, acc, J0, J1, J2, Z, K);
+            else slice_epilogue_tr<NT, 2, LC>(L, crot, acc, J0, J1, J2, Z, K);
+            J0 = J1 = J2 = Z = 0;
+            K.reset();
+            return;
+        }
+    }
+#endif
     if (!kinds) {
         slice_epilogue_fast<NT, TM, false, ROLL, 2, LC>(L, crot, acc, J0, J1, J2, Z, K);
     } else if (K.fits_fast()) {
@@ -1303,6 +1411,171 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
     tmem_free_cta(tmem_base_of(acc.taddr));
 }
 
+// ---------------------------------------------------------- page kernel ----
+// Enumerated batches (all 2^P amplitudes, contiguous sweeps; n_params <= 32) on
+// the PAGE layout (pzx_host.cpp, page_term): pages of
+// kPageSlots 32-byte records, terms never straddling a page, each term a
+// header (its constant) + constraint (C), generic (G) and dispatch (D) rows.
+// A thread owns 32 assignments (bit-sliced as in k_eval_slice), a warp 1024
+// consecutive ones, base_w + 32 lane + g. Per page and warp, a pre-pass
+// resolves the parity of every row mask against the warp's high bits ONCE per
+// row (one POPC per row and warp, spread over the lanes) into a lane word
+//   M = LW(mask bits 5..9) ^ -parity(mask & base_w)     (bit l: lane l's parity)
+// so the row loops form X = parity ? ~W : W with a predicate test of M and a
+// SEL -- no per-thread POPC. Per row and warp:
+//   C: Z |= X                                            (6 instructions)
+//   G: J += (k + 4p)q~, branch-free ripple add           (~16, no jump)
+//   D: the generated class body through the jump table   (the slice kernel's)
+// After a term's C rows a warp whose 1024 assignments are all zero skips the
+// rest of the term (constraint-first order, PAPER "Conclusions").
+__host__ __device__ constexpr uint32_t page_lut_offset() { return 2 * kPageSlots * 32 + 16; }
+
+size_t page_smem_bytes(const DevTable& t) {
+    const uint32_t amp_off = (page_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    const size_t b = amp_off + 4 * kCrot * 16 + 4 * size_t(kPageSlots) * 8 + size_t(kHiPlanes) * kSliceThreads * 4;
+    return b > kTmemCtaSmem ? b : kTmemCtaSmem;
+}
+
+template <bool DBG = false>
+__global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t, const LaunchReq r) {
+    constexpr int NT = kSliceThreads;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ uint32_t lw_s[32];  // lw_s[v] bit l = parity(v & l): lane bits 5..9 of the assignment
+    if (threadIdx.x < 32) {
+        uint32_t w = 0;
+        for (uint32_t l = 0; l < 32; ++l) w |= uint32_t(__popc(threadIdx.x & l) & 1) << l;
+        lw_s[threadIdx.x] = w;
+    }
+    const SmemLut L = kernel_prologue(t, smem, page_lut_offset());  // (its __syncthreads covers lw_s)
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t amp_off = (page_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
+    double2* crot = reinterpret_cast<double2*>(smem + amp_off) + warp * kCrot;
+    uint2* Mw = reinterpret_cast<uint2*>(smem + amp_off + 4 * kCrot * 16) + warp * kPageSlots;
+    uint32_t* hi_planes = reinterpret_cast<uint32_t*>(smem + amp_off + 4 * kCrot * 16 + 4 * kPageSlots * 8);
+    SliceAcc<NT, true> acc{nullptr, 0u};
+    acc.taddr = tmem_alloc_cta(&tmem_base_s);
+    acc.zero();
+
+    uint64_t tb, te;
+    term_range(r, tb, te);
+    const uint64_t off = (uint64_t(blockIdx.x) * NT + threadIdx.x) * kSliceG;
+    const uint32_t wbase = uint32_t(r.first + (uint64_t(blockIdx.x) * NT + warp * 32u) * kSliceG);
+    const uint32_t lanebit = 1u << lane;
+    uint32_t J0 = 0, J1 = 0, J2 = 0, Z = 0;
+    KindCounters<NT> K;
+    K.init(hi_planes + threadIdx.x);
+
+    if (tb < te) {
+        uint4* pages = reinterpret_cast<uint4*>(smem);
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kPageSlots * 32);
+        const uint32_t s0 = t.term_slot[tb];
+        const uint32_t p0 = s0 / uint32_t(kPageSlots), np = t.term_slot[te - 1] / uint32_t(kPageSlots) - p0 + 1;
+        auto issue = [&](uint32_t i) {
+            uint64_t* bar = &bars[i & 1];
+            mbar_expect_tx(bar, kPageSlots * 32);
+            tma_load_1d(pages + (i & 1) * kPageSlots * 2, t.prows + uint64_t(p0 + i) * kPageSlots * 2,
+                        kPageSlots * 32, bar);
+        };
+        if (threadIdx.x == 0) {
+            issue(0);
+            if (np > 1) issue(1);
+        }
+        uint64_t term = tb;
+        uint32_t s = s0 % uint32_t(kPageSlots);
+        for (uint32_t i = 0; i < np; ++i) {
+            mbar_wait(&bars[i & 1], (i >> 1) & 1u);
+            const uint4* pg = pages + (i & 1) * kPageSlots * 2;
+            // pre-pass: this warp's lane-parity words of every slot of the page
+#pragma unroll 4
+            for (uint32_t q = lane; q < uint32_t(kPageSlots); q += 32) {
+                const uint4 rec = pg[2 * q + 1];
+                const uint32_t mx = lw_s[(rec.z >> 5) & 31u] ^ (0u - (uint32_t(__popc(rec.z & wbase)) & 1u));
+                const uint32_t my = lw_s[(rec.w >> 5) & 31u] ^ (0u - (uint32_t(__popc(rec.w & wbase)) & 1u));
+                Mw[q] = make_uint2(mx, my);
+            }
+            __syncwarp();
+            while (term < te) {
+                const uint4 h0 = pg[2 * s], h1 = pg[2 * s + 1];
+                const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu;
+                uint32_t q = s + 1;
+                // C rows: parity constraints
+                for (const uint32_t e = q + nc; q < e; ++q) {
+                    const uint4 a = pg[2 * q];
+                    Z |= (Mw[q].x & lanebit) ? a.y : a.x;
+                }
+                const bool dead = nc != 0 && __all_sync(0xFFFFFFFFu, Z == 0xFFFFFFFFu);
+                if (dead) {
+                    q += ng + nd;
+                } else {
+                    // G rows: J += (k + 4p) q~ with X = p ^ K2, Y = q~, K0 / K1 the low bits of k
+#pragma unroll 2
+                    for (const uint32_t e = q + ng; q < e; ++q) {
+                        const uint4 a = pg[2 * q], b = pg[2 * q + 1];
+                        const uint2 m = Mw[q];
+                        const uint32_t X = (m.x & lanebit) ? a.y : a.x;
+                        const uint32_t Y = (m.y & lanebit) ? a.w : a.z;
+                        const uint32_t v0 = Y & b.x, v1 = Y & b.y, v2 = Y & X;
+                        const uint32_t c0 = J0 & v0;
+                        J0 ^= v0;
+                        const uint32_t c1 = (J1 & (v1 | c0)) | (v1 & c0);
+                        J1 ^= v1 ^ c0;
+                        J2 ^= v2 ^ c1;
+                    }
+                    // D rows: the class bodies of the bit-sliced kernels (generated PTX)
+                    for (const uint32_t e = q + nd; q < e; ++q) {
+                        const uint4 a = pg[2 * q], b = pg[2 * q + 1];
+                        const uint2 m = Mw[q];
+                        const uint32_t X = (m.x & lanebit) ? a.y : a.x;
+                        const uint32_t Y = (m.y & lanebit) ? a.w : a.z;
+                        const uint32_t code = b.x, op = b.y;
+                        uint32_t vl, vpi, vpip;
+                        asm(PZX_SLICE_DISPATCH_ASM_XY
+                            : "+r"(J0), "+r"(J1), "+r"(J2), "+r"(Z), "=r"(vl), "=r"(vpi), "=r"(vpip)
+                            : "r"(X), "r"(op), "r"(Y));
+                        if (code & (kSliceLamFlag | kSlicePiFlag | kSlicePipFlag)) {
+                            if (code & kSliceLamFlag) K.bump_s(vl);
+                            if (code & kSlicePiFlag) K.bump_a(vpi);
+                            if (code & kSlicePipFlag) K.bump_b(vpip);
+                        }
+                    }
+                }
+                if constexpr (DBG) debug_dump_codes<NT, false>(r, term, off, J0, J1, J2, Z, K);
+                if (!dead) {
+                    __syncwarp();  // the previous term's epilogue is done with crot
+                    if (lane < uint32_t(kCrot)) {
+                        double2 v = make_double2(0.0, 0.0);
+                        if (lane < 8) {
+                            const double2 C = make_double2(__hiloint2double(int(h0.y), int(h0.x)),
+                                                           __hiloint2double(int(h0.w), int(h0.z)));
+                            const double2 w = L.om[lane];
+                            v = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+                        }
+                        crot[lane] = v;
+                    }
+                    __syncwarp();
+                    slice_epilogue_apply<NT, true, true>(L, crot, acc, J0, J1, J2, Z, K);
+                } else {
+                    J0 = J1 = J2 = Z = 0;
+                    if (K.any()) K.reset();
+                }
+                ++term;
+                s = q;
+                if ((h1.x >> 24) & 1u) {  // last term of this page
+                    s = 0;
+                    break;
+                }
+            }
+            __syncthreads();  // every warp is done with buffer (i & 1)
+            if (threadIdx.x == 0 && i + 2 < np) {
+                fence_proxy_async();
+                issue(i + 2);
+            }
+        }
+    }
+    slice_store_results<NT, true>(r, off, acc);
+}
+
 // ---------------------------------------------------- two-slice kernel ----
 // Enumerated batches, 64 assignments per thread: slice a = base + g, slice b
 // = base + 32 + g (base % 64 == 0). Both slices share the row load, the
@@ -1704,6 +1977,14 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
         kern<<<dim3(grid.x, grid.y / kWarpChunks), kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
+    if (kc == KC_PAGE) {
+        const size_t sm = page_smem_bytes(t);
+        auto kern = r.d_dbg5 ? k_eval_page<true> : k_eval_page<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
+        return cudaGetLastError();
+    }
     if (kc == KC_SLICE2) {
         const size_t sm = slice2_smem_bytes<P64>(t);
         cudaError_t e = cudaFuncSetAttribute(k_eval_slice2<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -1740,12 +2021,20 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
 
 // ------------------------------------------------------------------ host ----
 
+// the page kernel: 128-thread TMEM CTAs, warps of 1024 consecutive assignments
+// (lane bits = assignment bits 5..9), tables with the page layout (P <= 32)
+bool page_kernel_ok(const DevTable& t, const LaunchReq& r) {
+    static const bool off = std::getenv("PZX_NO_PAGES") != nullptr;  // A/B knob
+    return !off && t.page_ok && tmem_accumulators() && slice_threads(r) == kSliceThreads && (r.first % 1024) == 0;
+}
+
 KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
     if (r.kernel != KC_AUTO) return r.kernel;
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (enumerated && t.slice_ok && (r.first % (2 * kSliceG)) == 0 && slice_threads(r) == kSliceThreads &&
         tmem_accumulators() && slice2_enabled())
         return KC_SLICE2;
+    if (enumerated && page_kernel_ok(t, r)) return KC_PAGE;
     if (enumerated && t.slice_ok && (r.first % kSliceG) == 0)
         return (slice_threads(r) == 32 && tmem_accumulators()) ? KC_SLICEWC : KC_SLICE;
     if (enumerated && (r.first % kGray) == 0) return KC_GRAY;
@@ -1758,6 +2047,7 @@ KernelChoice choose_kernel(const DevTable& t, const LaunchReq& r) {
 bool kernel_supported(const DevTable& t, const LaunchReq& r, KernelChoice kc) {
     const bool enumerated = r.d_asg == nullptr || r.words_contiguous;
     if (kc == KC_SLICE) return enumerated && t.slice_ok && (r.first % kSliceG) == 0;
+    if (kc == KC_PAGE) return enumerated && t.page_ok && tmem_accumulators() && (r.first % 1024) == 0;
     if (kc == KC_SLICE2) return enumerated && t.slice_ok && (r.first % (2 * kSliceG)) == 0;
     if (kc == KC_SLICER) return t.slice_ok != 0;
     if (kc == KC_SORTED) return t.sorted_ok != 0 && r.d_asg != nullptr;
@@ -1783,6 +2073,7 @@ int grid_assign_blocks(const DevTable&, const LaunchReq& r, KernelChoice kc) {
                        : kc == KC_SLICE2                   ? uint64_t(kSliceThreads) * 2 * kSliceG
                        : kc == KC_SORTED                   ? uint64_t(sorted_threads(r.sorted_groups)) * kSliceG
                        : (kc == KC_SLICE || kc == KC_SLICER) ? uint64_t(slice_threads(r)) * kSliceG
+                       : kc == KC_PAGE                     ? uint64_t(kSliceThreads) * kSliceG
                        : kc == KC_GRAY  ? uint64_t(kThreads) * kGray
                                         : uint64_t(kThreads) * kGeneralK;
     return int((r.n + per - 1) / per);
@@ -1801,6 +2092,10 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
         auto kern = t.p64 ? k_eval_slice_wc<true> : k_eval_slice_wc<false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+    } else if (kc == KC_PAGE) {
+        sm = page_smem_bytes(t);
+        cudaFuncSetAttribute(k_eval_page<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_page<false>, kSliceThreads, sm);
     } else if (kc == KC_SLICE2) {
         sm = t.p64 ? slice2_smem_bytes<true>(t) : slice2_smem_bytes<false>(t);
         auto kern = t.p64 ? k_eval_slice2<true> : k_eval_slice2<false>;

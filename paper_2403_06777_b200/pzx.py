@@ -301,6 +301,7 @@ KERNEL_SLICE_RAND = 1 << 11
 ACCUMULATE = 1 << 2
 KERNEL_SORTED = 1 << 12
 KERNEL_SLICE2 = 1 << 13
+KERNEL_PAGE = 1 << 14
 
 
 class DeviceTable:
@@ -372,7 +373,7 @@ class Context:
     def launch_count(self) -> int:
         return int(N.lib().pzx_launch_count(self.handle))
 
-    KERNEL_NAMES = {1: "popc", 2: "gray", 3: "slice", 4: "slice_rand", 5: "sorted", 6: "slice2", 7: "slice_wc"}
+    KERNEL_NAMES = {1: "popc", 2: "gray", 3: "slice", 4: "slice_rand", 5: "sorted", 6: "slice2", 7: "slice_wc", 8: "page"}
 
     def last_kernel(self) -> dict:
         """The evaluation kernel the last evaluate* call chose (pzx_last_kernel)."""
@@ -580,6 +581,23 @@ class HostTable:
 
     term_info = DeviceTable.term_info
     slice_stats = DeviceTable.slice_stats
+
+    def page_layout(self):
+        """(slots uint32 [n, 8], term_slot [m], jfold [m], family_rows [4]) of the
+        page kernel's layout (pzx_table_page_layout), or None without one."""
+        L = N.lib()
+        n = C.c_uint64()
+        fam = np.zeros(4, np.uint64)
+        st = L.pzx_table_page_layout(self.handle, None, C.byref(n), None, None, N.ptr(fam, C.c_uint64))
+        if st == 6:
+            return None
+        _check(st)
+        slots = np.zeros((max(n.value, 1), 8), np.uint32)
+        ts = np.zeros(max(self.n_terms, 1), np.uint32)
+        jf = np.zeros(max(self.n_terms, 1), np.uint8)
+        _check(L.pzx_table_page_layout(self.handle, slots.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(n),
+                                       ts.ctypes.data_as(C.POINTER(C.c_uint32)), N.ptr(jf, C.c_uint8), None))
+        return slots[:n.value], ts[:self.n_terms], jf[:self.n_terms], fam
     free = DeviceTable.free
     __del__ = DeviceTable.__del__
 
@@ -806,6 +824,6 @@ __all__ = [
     "kMaxParams", "ParamAssignment", "ParamPhase", "phase_add", "SubtermKind", "Subterm", "RingQuad",
     "ScalarExpression", "DeviceTable", "HostTable", "class_table", "Context", "compile_bit_table", "evaluate_batch", "evaluate",
     "Group", "GroupTable", "REPLICATE", "SPLIT_TERMS", "PhaseTable", "encode_pzx1", "decode_pzx1", "pzx1_to_json", "pzx1_from_json",
-    "PROB_ABS2", "PROB_REAL", "ACCUMULATE", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "slice_op_table",
+    "PROB_ABS2", "PROB_REAL", "ACCUMULATE", "KERNEL_GENERAL", "KERNEL_GRAY", "KERNEL_SLICE", "KERNEL_SLICE_RAND", "KERNEL_SORTED", "KERNEL_SLICE2", "KERNEL_PAGE", "slice_op_table",
 ]
 _ = builtins

@@ -108,9 +108,11 @@ def test_c2_full_headline_kernel(ctx):
     N = cfg.n_assign
     amp = ctx.evaluate_range(t, 0, N)
     kinfo = ctx.last_kernel()
-    assert kinfo["kernel"] == "slice" and kinfo["term_chunks"] > 1
+    assert kinfo["kernel"] == "page" and kinfo["term_chunks"] > 1
     ex = ctx.evaluate_exact_range(t, 0, N)
     assert_close(amp, exact_to_complex(ex))
+    # the round-1 bit-sliced kernel (srows layout) on the same batch
+    assert_close(ctx.evaluate_range(t, 0, N, flags=P.KERNEL_SLICE), amp, 1e-13, 1.0)
     rng = np.random.default_rng(2)
     pick = np.sort(rng.choice(N, 256, replace=False)).astype(np.uint64)
     ex_ref, want = O.eval_batch(e, pick, THREADS, impl=IMPL)
@@ -133,7 +135,7 @@ def test_c2r_real_circuit_all_amplitudes(ctx):
     t = ctx.compile_bit_table(e)
     N = cfg.n_assign
     amp = ctx.evaluate_range(t, 0, N)
-    assert ctx.last_kernel()["kernel"] == "slice"
+    assert ctx.last_kernel()["kernel"] == "page"
     sv = SV.run(synth.config_circuit(cfg))
     assert np.max(np.abs(amp - sv)) <= 1e-12 * np.sqrt(np.mean(np.abs(sv) ** 2)) * 1e3
     ex = ctx.evaluate_exact_range(t, 0, N)
@@ -213,7 +215,7 @@ def test_c5_full_term_split(ctx):
     assert_close(amp[:4], want)
 
 
-@pytest.mark.parametrize("kernel", ["slice", "sorted"])
+@pytest.mark.parametrize("kernel", ["slice", "page", "sorted"])
 def test_slice_codes_goldens_and_random(ctx, kernel):
     """Per-term planes of the production kernels on the reference-generated
     goldens and random tables (P up to 32 for sorted, 64 for slice)."""
@@ -228,13 +230,15 @@ def test_slice_codes_goldens_and_random(ctx, kernel):
     cases += [synth.generate(p, 200, 1, 60, 8800 + p) for p in (9, 20, 31)]
     for e in cases:
         t = ctx.compile_bit_table(e)
-        if t.max_term_rows > 127 or (kernel == "sorted" and e.n_params > 32):
+        if t.max_term_rows > 127 or (kernel in ("sorted", "page") and e.n_params > 32):
             continue
         rng = np.random.default_rng(e.n_params)
-        if kernel == "slice":
+        if kernel in ("slice", "page"):
             n = 1 << 14                       # 128-thread TMEM variant (>= 16K assignments)
             first = 0 if e.n_params <= 14 else int(rng.integers(0, 1 << min(e.n_params - 14, 40))) << 14
-            codes = ctx.debug_slice_codes(t, first=first, n=n, term_end=min(t.n_terms, 24), flags=P.KERNEL_SLICE)
+            fl = P.KERNEL_SLICE if kernel == "slice" else P.KERNEL_PAGE
+            codes = ctx.debug_slice_codes(t, first=first, n=n, term_end=min(t.n_terms, 24), flags=fl)
+            assert ctx.last_kernel()["kernel"] == kernel
             idx = rng.choice(n, 24, replace=False)
             check_slice_codes(ctx, e, t, range(min(t.n_terms, 24)), np.uint64(first) + idx.astype(np.uint64),
                               codes[:, idx])

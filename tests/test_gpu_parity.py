@@ -120,6 +120,44 @@ def test_slice_kernel_vs_oracle(ctx, P_):
     assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_GENERAL), 1e-13)
 
 
+@pytest.mark.parametrize("P_", [10, 14, 20, 27, 32])
+def test_page_kernel_vs_oracle(ctx, P_):
+    """Page-layout kernel (C / G / D row families, lane-parity pre-pass, zero
+    skip) on enumerated batches: against the reference oracle and the
+    round-1 bit-sliced kernel, both row mixes, ragged batch ends, term chunks."""
+    for mix in ("general", "clifford"):
+        e = synth.generate(P_, 900, 0, 60, 1700 + P_, mix)
+        t = ctx.compile_bit_table(e)
+        n = (1 << min(P_, 16)) - 77
+        first = 0 if P_ <= 16 else 1024 * 37
+        amp = ctx.evaluate_range(t, first, n, flags=P.KERNEL_PAGE)
+        assert ctx.last_kernel()["kernel"] == "page"
+        words = np.arange(first, first + n, dtype=np.uint64)
+        idx = np.random.default_rng(P_).choice(n, 64, replace=False)
+        _, want = O.eval_batch(e, words[idx], 8, impl="ref" if O.have_ref() else "port")
+        assert_close(amp[idx], want)
+        assert_close(amp, ctx.evaluate_range(t, first, n, flags=P.KERNEL_SLICE), 1e-13)
+        assert_close(ctx.evaluate_range(t, first, n), amp, 1e-13)   # auto
+
+
+def test_page_kernel_zero_skip(ctx):
+    """Terms whose constraint rows kill every assignment of a warp are skipped
+    (the skip is exact: the skipped terms are zero there)."""
+    R = P.RingQuad
+    nd = lambda k, m: P.Subterm.node(P.ParamPhase(k, m))  # noqa: E731
+    pp = lambda a, m1, b, m2: P.Subterm.phase_pair(P.ParamPhase(a, m1), P.ParamPhase(b, m2))  # noqa: E731
+    terms = []
+    for i in range(300):
+        # (1 + (-1)^{a_15}) kills every assignment with bit 15 set; bits 10..14 vary per warp
+        rows = [nd(0, 1 << 15), pp(1, (i % 7 + 1) << 3, 3, 0b101), nd(1, 0b11 | 1 << (10 + i % 5))]
+        terms.append((R.make(i % 5 + 1, 1, 0, 0, 2), rows))
+    e = P.ScalarExpression.from_terms(16, terms)
+    t = ctx.compile_bit_table(e)
+    amp = ctx.evaluate_range(t, 0, 1 << 16, flags=P.KERNEL_PAGE)
+    assert np.all(amp[1 << 15:] == 0)
+    assert_close(amp, ctx.evaluate_range(t, 0, 1 << 16, flags=P.KERNEL_GENERAL), 1e-13)
+
+
 @pytest.mark.parametrize("P_", [3, 6, 12, 20, 33, 64])
 def test_slice2_kernel_vs_oracle(ctx, P_):
     """Two-slice (64 assignments / thread, TMEM accumulators) enumerated kernel."""
