@@ -465,8 +465,9 @@ def run_ours(args):
     kinfo = ctx.last_kernel()
     op_rows, term_kinds = table.slice_stats()
     from paper_2403_06777_b200 import roofline as RL
-    model = "sorted" if kinfo["kernel"] == "sorted" else "slice"
-    roof = RL.roofline(op_rows, term_kinds, N, mean_ms / 1e3, f_mhz, model, kinfo["sorted_groups"] or 4)
+    model = kinfo["kernel"] if kinfo["kernel"] in ("sorted", "page") else "slice"
+    roof = RL.roofline(op_rows, term_kinds, N, mean_ms / 1e3, f_mhz, model, kinfo["sorted_groups"] or 4,
+                       page_stats=table.page_stats() if model == "page" else None)
     # BASELINE's naive int-op count (8 ops per row-eval), kept for reference
     w_row = 8 if cfg.n_params <= 32 else 12
     work = N * (w_row * R + 16 * m)

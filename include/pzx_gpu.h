@@ -166,6 +166,10 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
  * row), term_kinds = terms whose epilogue is kind-free / lambda-only / with a
  * pi or pi' row. Either pointer may be NULL. */
 pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]);
+/* Rows per page family {constraint, generic, dispatch, dropped} and the
+ * dispatch rows per op (bench.py's roofline of the page kernel); any table
+ * with a page layout, PZX_E_CAPACITY otherwise. */
+pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[4], uint64_t d_op_rows[129]);
 /* Host-only tables (pzx_table_compile_host): the page layout of the
  * enumerated page kernel -- *n_slots 32-byte records (8 x u32 each; slots may
  * be NULL to query the size), the header slot of every term, the w^j folded

@@ -24,7 +24,7 @@ EXPORTS = (
     "pzx_group_evaluate", "pzx_microbench", "pzx_table_upload_expr_ex", "pzx_evaluate_exact",
     "pzx_evaluate_exact_range", "pzx_ringquad_sum", "pzx_ringquad_sum_device", "pzx_table_slice_stats",
     "pzx_last_kernel", "pzx_debug_slice_codes", "pzx_circuit_reduce", "pzx_expr_get_view", "pzx_expr_info",
-    "pzx_expr_free", "pzx_table_page_layout",
+    "pzx_expr_free", "pzx_table_page_layout", "pzx_table_page_stats",
 )
 
 u8p = C.POINTER(C.c_uint8)
@@ -134,6 +134,7 @@ def lib() -> C.CDLL:
     L.pzx_expr_get_view.argtypes = [vp, C.POINTER(ExprView)]
     L.pzx_expr_info.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
     L.pzx_table_page_layout.argtypes = [vp, C.POINTER(C.c_uint32), u64p, C.POINTER(C.c_uint32), u8p, u64p]
+    L.pzx_table_page_stats.argtypes = [vp, u64p, u64p]
     L.pzx_expr_free.argtypes = [vp]
     L.pzx_expr_free.restype = None
     _lib = L

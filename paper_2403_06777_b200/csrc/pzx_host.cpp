@@ -178,6 +178,7 @@ struct HostTable {
     uint32_t page_fill = 0;                 // slots used in the open page
     int64_t last_hdr = -1;                  // slot of the last header written
     uint64_t page_rows[4] = {};             // rows by family: constraint, G, dispatch, dropped
+    uint64_t page_d_ops[kSliceOps] = {};    // dispatch-family rows per op (the roofline's D bodies)
     bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
     uint64_t n_dev_rows() const { return unit.size(); }
     uint64_t genuine_rows() const { return unit.size() - uint64_t(std::count(unit.begin(), unit.end(), 1)); }
@@ -384,6 +385,7 @@ int page_term(HostTable& h, const C128& cpp) {
         if (r.fam == 4) { h.page_rows[3] += 1; continue; }
         const int f = r.fam == 0 ? 0 : r.fam == 1 ? 1 : 2;
         h.page_rows[f] += 1;
+        if (f == 2) h.page_d_ops[pr.op] += 1;
         fam[f].push_back(r);
     }
     h.pend.clear();
@@ -617,6 +619,7 @@ void merge_into(HostTable& h, HostTable& part) {
         app(h.jp_t, part.jp_t);
         if (part.last_hdr >= 0) h.last_hdr = int64_t(base_slot) + part.last_hdr;
         for (int i = 0; i < 4; ++i) h.page_rows[i] += part.page_rows[i];
+        for (int i = 0; i < kSliceOps; ++i) h.page_d_ops[i] += part.page_d_ops[i];
     } else if (h.want_prows) {
         h.want_prows = false;
         std::vector<uint4>().swap(h.prows);
@@ -1649,6 +1652,17 @@ pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* 
     if (slots) std::memcpy(slots, h.prows.data(), h.prows.size() * 16);
     if (term_slot) std::memcpy(term_slot, h.term_slot.data(), h.term_slot.size() * 4);
     if (jfold) std::memcpy(jfold, h.jp_t.data(), h.jp_t.size());
+    return PZX_OK;
+}
+
+pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[4], uint64_t d_op_rows[129]) {
+    if (!t) return PZX_E_INVALID;
+    const HostTable& h = t->host;
+    if (!h.want_prows || h.term_slot.size() != h.coef.size()) return PZX_E_CAPACITY;
+    if (family_rows)
+        for (int i = 0; i < 4; ++i) family_rows[i] = h.page_rows[i];
+    if (d_op_rows)
+        for (int i = 0; i < kSliceOps; ++i) d_op_rows[i] = h.page_d_ops[i];
     return PZX_OK;
 }
 

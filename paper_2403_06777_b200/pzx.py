@@ -330,6 +330,17 @@ class DeviceTable:
         _check(N.lib().pzx_table_slice_stats(self.handle, N.ptr(ops, C.c_uint64), N.ptr(kinds, C.c_uint64)))
         return ops, kinds
 
+    def page_stats(self):
+        """(family_rows [C, G, D, dropped], dispatch rows per op [129]) of the page
+        layout, or None when the table has none (pzx_table_page_stats)."""
+        fam = np.zeros(4, np.uint64)
+        ops = np.zeros(129, np.uint64)
+        st = N.lib().pzx_table_page_stats(self.handle, N.ptr(fam, C.c_uint64), N.ptr(ops, C.c_uint64))
+        if st == 6:
+            return None
+        _check(st)
+        return fam, ops
+
     def free(self) -> None:
         if self.handle:
             N.lib().pzx_table_free(self.handle)
@@ -581,6 +592,7 @@ class HostTable:
 
     term_info = DeviceTable.term_info
     slice_stats = DeviceTable.slice_stats
+    page_stats = DeviceTable.page_stats
 
     def page_layout(self):
         """(slots uint32 [n, 8], term_slot [m], jfold [m], family_rows [4]) of the

@@ -25,9 +25,18 @@ Per term and warp (the epilogue, 32 assignments per thread), per assignment:
 
 For word-list batches the sorted kernel forms each parity vector from G
 Four-Russians table words: G LDS + G XOR + AND + POPC + 1 = 2G + 3 per parity
-(G = 4 dense, 6 sparse batches). Loop control, row prefetch, TMA waits,
-counter decode, TMEM traffic and the chunk reduction are implementation
-overhead and are NOT in the minimum, so frac <= 1 by construction.
+(G = 4 dense, 6 sparse batches).
+
+The page kernel (enumerated batches, page layout) resolves the high-bit
+parities once per row and WARP in a pre-pass (2 POPC per row, spread over the
+lanes: (1 LDS + 2 x (index, LDS, AND, POPC, XOR) + 1 STS) / 32 per row and
+warp), then per row and warp:
+    C row: 2 LDS (record, lane word) + LOP3->P + SEL + OR                      = 5
+    G row: 3 LDS (record halves, lane words) + 2 x (LOP3->P + SEL) + 7 LOP3   = 14
+    D row: 3 LDS + 2 x (LOP3->P + SEL) + the class's LOP3 chain
+Loop control, row prefetch, TMA waits, counter decode, TMEM traffic and the
+chunk reduction are implementation overhead and are NOT in the minimum, so
+frac <= 1 by construction.
 """
 from __future__ import annotations
 
@@ -65,11 +74,31 @@ def min_counts(op_rows, term_kinds, n_assign: int, kernel: str = "slice", sorted
             "per_term_per_warp": term_inst / max(float(np.sum(kinds)), 1.0)}
 
 
+def min_counts_page(family_rows, d_op_rows, term_kinds, n_assign: int) -> dict:
+    """Minimum warp-instructions / warp-POPCs of one page-kernel launch."""
+    body, _ = _op_table()
+    c, g, d, _dropped = (float(x) for x in family_rows)
+    d_ops = np.asarray(d_op_rows, np.float64)
+    rows = c + g + d
+    pre = rows * (1 + 2 * 5 + 1) / 32.0
+    row_inst = pre + 5 * c + 14 * g + float(np.sum(d_ops * (3 + 4 + body)))
+    kinds = np.asarray(term_kinds, np.float64)
+    term_inst = float(np.sum(kinds * 32 * np.array(EPI_PER_ASSIGN)))
+    warps = n_assign / 1024.0
+    return {"warp_instructions": warps * (row_inst + term_inst), "warp_popc": warps * rows * 2 / 32.0,
+            "row_share": row_inst / max(row_inst + term_inst, 1.0),
+            "per_row_per_warp": row_inst / max(rows, 1.0),
+            "per_term_per_warp": term_inst / max(float(np.sum(kinds)), 1.0)}
+
+
 def roofline(op_rows, term_kinds, n_assign: int, seconds: float, f_mhz: float, kernel: str = "slice",
-             sorted_groups: int = 4) -> dict:
+             sorted_groups: int = 4, page_stats=None) -> dict:
     """The bench's `roofline` object: the binding resource of the algorithm's
     minimum work (issue slots or the POPC pipe) against the measured launch time."""
-    c = min_counts(op_rows, term_kinds, n_assign, kernel, sorted_groups)
+    if kernel == "page" and page_stats is not None:
+        c = min_counts_page(page_stats[0], page_stats[1], term_kinds, n_assign)
+    else:
+        c = min_counts(op_rows, term_kinds, n_assign, kernel, sorted_groups)
     hz = f_mhz * 1e6
     t_issue = c["warp_instructions"] / (N_SM * ISSUE_PER_SM * hz)
     t_xu = c["warp_popc"] * 32 / (N_SM * POPC_LANES_PER_SM * hz)
