@@ -462,6 +462,17 @@ constexpr int kSliceG = 1 << kSliceBits;  // 32 assignments per thread, one bit 
 constexpr int kSliceTile = 512;           // rows (32 B each) per TMA-staged tile
 constexpr int kPlanes = 7;                // bit-sliced counters up to 127 (terms <= kSegRows rows)
 
+__device__ __forceinline__ double2 lds_d2(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ double lds_d(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -844,33 +855,37 @@ __device__ __forceinline__ void transpose8_bytes(uint32_t (&P)[8]) {
     }
 }
 
-// Term epilogue fast path, TMEM accumulators, transposed decode:
-// planes {J0 J1 J2 Z S0..S3} -> key byte (j | z << 3 | s << 4) per assignment,
-// {A0 A1 B0 B1} -> (a | b << 2). Per assignment: the key byte, C w^j from the
-// warp's crot table (zeros for Z-marked assignments) and
-//   KIND 0 (kind-free term):   acc += C w^j                     (1 LDS, 2 DADD)
-//   KIND 1 (lambda rows only): acc += C w^j (sqrt2-1)^s          (2 LDS, 2 DFMA)
-//   KIND 2 (pi / pi' rows):    acc += C w^j (sqrt2-1)^s pi^a pi'^b (2 LDS, 4 DFMA)
-// Groups of 4 consecutive assignments (16 TMEM columns) are loaded / stored
+// Term epilogue fast path, TMEM accumulators, transposed decode.
+// The planes are grouped so that each transposed byte IS a table index:
+//   KIND 0 (kind-free term):  {J0 J1 J2 Z}         -> crot[j | z << 3]              acc += C w^j
+//   KIND 1 (lambda rows only): {J0 J1 J2 Z S0..S3} -> crot[b & 15], u[b >> 4]       acc += C w^j (sqrt2-1)^s
+//   KIND 2 (pi / pi' rows):    {J0 J1 J2 Z}, {S0..S3 A0 A1 B0 B1}
+//                              -> crot[b1], sab[b2 = s | a << 4 | b << 6]         acc += C w^j (sqrt2-1)^s pi^a pi'^b
+// (crot: the warp's C * w^j table with zeros for Z-marked assignments.) A
+// byte is picked with one PRMT and turned into an address with one LEA;
+// groups of 4 consecutive assignments (16 TMEM columns) are loaded / stored
 // together; assignment 8m + 4h + r is byte m of key word 4h + r.
 template <int NT, int KIND, bool LC>
 __device__ __forceinline__ void slice_epilogue_tr(const SmemLut& L, const double2* crot, SliceAcc<NT, true>& acc,
                                                   uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
                                                   const KindCounters<NT, LC>& K) {
     uint32_t Q[8] = {J0, J1, J2, Z, 0u, 0u, 0u, 0u};
-    if constexpr (KIND >= 1) {
+    if constexpr (KIND == 1) {
         Q[4] = K.S[0]; Q[5] = K.S[1]; Q[6] = K.S[2]; Q[7] = K.S[3];
     }
     transpose8_bytes(Q);
     uint32_t R[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     if constexpr (KIND == 2) {
-        R[0] = K.A[0]; R[1] = K.A[1]; R[2] = K.B[0]; R[3] = K.B[1];
+        R[0] = K.S[0]; R[1] = K.S[1]; R[2] = K.S[2]; R[3] = K.S[3];
+        R[4] = K.A[0]; R[5] = K.A[1]; R[6] = K.B[0]; R[7] = K.B[1];
         transpose8_bytes(R);
     }
+    const uint32_t crot_s = smem_u32(crot);
+    const uint32_t u_s = smem_u32(L.u), sab_s = smem_u32(L.sab);
     tmem_wait_st();  // the previous term's stores have landed
 #pragma unroll 1
     for (int m = 0; m < 4; ++m) {
-        const uint32_t sh = 8u * uint32_t(m);
+        const uint32_t sel = 0x4440u | uint32_t(m);  // PRMT: byte m -> byte 0, zeros above
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             uint32_t v[16];
@@ -879,12 +894,13 @@ __device__ __forceinline__ void slice_epilogue_tr(const SmemLut& L, const double
             double2 f[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const uint32_t b = Q[4 * h + r] >> sh;
-                c[r] = crot[b & 15u];
+                const uint32_t b = __byte_perm(Q[4 * h + r], 0u, sel);
                 if constexpr (KIND == 1) {
-                    f[r].x = L.u[(b >> 4) & 15u];
-                } else if constexpr (KIND == 2) {
-                    f[r] = L.sab[((b >> 4) & 15u) | (((R[4 * h + r] >> sh) & 15u) << 4)];
+                    c[r] = lds_d2(crot_s + ((b & 15u) << 4));
+                    f[r].x = lds_d(u_s + ((b >> 4) << 3));
+                } else {
+                    c[r] = lds_d2(crot_s + (b << 4));
+                    if constexpr (KIND == 2) f[r] = lds_d2(sab_s + (__byte_perm(R[4 * h + r], 0u, sel) << 4));
                 }
             }
             tmem_wait_ld();
@@ -1430,6 +1446,38 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
 // rest of the term (constraint-first order, PAPER "Conclusions").
 __host__ __device__ constexpr uint32_t page_lut_offset() { return 2 * kPageSlots * 32 + 16; }
 
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+// (J2 J1 J0) += Y & K0 + 2 (Y & K1) + 4 (Y & X)  mod 8, bit-sliced: 7 LOP3
+__device__ __forceinline__ void g_row(uint32_t& J0, uint32_t& J1, uint32_t& J2, uint32_t X, uint32_t Y, uint32_t K0,
+                                      uint32_t K1) {
+    asm("{\n"
+        ".reg .b32 c0, v1, c1, v2;\n"
+        "lop3.b32 c0, %0, %3, %5, 0x80;\n"   // J0 & Y & K0
+        "lop3.b32 %0, %0, %3, %5, 0x78;\n"   // J0 ^ (Y & K0)
+        "and.b32 v1, %3, %6;\n"               // Y & K1
+        "lop3.b32 c1, %1, v1, c0, 0xe8;\n"   // maj(J1, v1, c0)
+        "lop3.b32 %1, %1, v1, c0, 0x96;\n"   // J1 ^ v1 ^ c0
+        "and.b32 v2, %3, %4;\n"               // Y & X
+        "lop3.b32 %2, %2, v2, c1, 0x96;\n"   // J2 ^ v2 ^ c1
+        "}\n"
+        : "+r"(J0), "+r"(J1), "+r"(J2)
+        : "r"(Y), "r"(X), "r"(K0), "r"(K1));
+}
+
+// (J2 J1 J0) += (H2 H1 H0) mod 8
+__device__ __forceinline__ void add3(uint32_t& J0, uint32_t& J1, uint32_t& J2, uint32_t H0, uint32_t H1, uint32_t H2) {
+    const uint32_t c0 = J0 & H0;
+    J0 ^= H0;
+    const uint32_t c1 = (J1 & H1) | (c0 & (J1 ^ H1));
+    J1 ^= H1 ^ c0;
+    J2 ^= H2 ^ c1;
+}
+
 size_t page_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (page_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t b = amp_off + 4 * kCrot * 16 + 4 * size_t(kPageSlots) * 8 + size_t(kHiPlanes) * kSliceThreads * 4;
@@ -1448,7 +1496,9 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
         lw_s[threadIdx.x] = w;
     }
     const SmemLut L = kernel_prologue(t, smem, page_lut_offset());  // (its __syncthreads covers lw_s)
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    // the warp index through a lane-0 shuffle: provably warp-uniform (uniform
+    // datapath addressing of the warp's lane words and crot table)
+    const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31u;
     const uint32_t amp_off = (page_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     double2* crot = reinterpret_cast<double2*>(smem + amp_off) + warp * kCrot;
     uint2* Mw = reinterpret_cast<uint2*>(smem + amp_off + 4 * kCrot * 16) + warp * kPageSlots;
@@ -1508,19 +1558,28 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                 if (dead) {
                     q += ng + nd;
                 } else {
-                    // G rows: J += (k + 4p) q~ with X = p ^ K2, Y = q~, K0 / K1 the low bits of k
-#pragma unroll 2
-                    for (const uint32_t e = q + ng; q < e; ++q) {
-                        const uint4 a = pg[2 * q], b = pg[2 * q + 1];
-                        const uint2 m = Mw[q];
-                        const uint32_t X = (m.x & lanebit) ? a.y : a.x;
-                        const uint32_t Y = (m.y & lanebit) ? a.w : a.z;
-                        const uint32_t v0 = Y & b.x, v1 = Y & b.y, v2 = Y & X;
-                        const uint32_t c0 = J0 & v0;
-                        J0 ^= v0;
-                        const uint32_t c1 = (J1 & (v1 | c0)) | (v1 & c0);
-                        J1 ^= v1 ^ c0;
-                        J2 ^= v2 ^ c1;
+                    // G rows: J += (k + 4p) q~ with X = p ^ K2, Y = q~, K0 / K1 the low bits
+                    // of k -- 7 LOP3 (g_row). Pairs of rows go to two counters (J, H) so
+                    // consecutive rows do not wait on each other's ripple carries; H is
+                    // added into J once, after the G rows.
+                    {
+                        uint32_t H0 = 0, H1 = 0, H2 = 0;
+                        uint32_t ra = smem_u32(pg + 2 * q), rm = smem_u32(Mw + q);
+                        const uint32_t e2 = q + (ng & ~1u);
+#pragma unroll 1
+                        for (; q < e2; q += 2, ra += 64, rm += 16) {
+                            const uint4 a = lds128(ra), b = lds128(ra + 16), c = lds128(ra + 32), d = lds128(ra + 48);
+                            const uint2 m0 = lds64(rm), m1 = lds64(rm + 8);
+                            g_row(J0, J1, J2, (m0.x & lanebit) ? a.y : a.x, (m0.y & lanebit) ? a.w : a.z, b.x, b.y);
+                            g_row(H0, H1, H2, (m1.x & lanebit) ? c.y : c.x, (m1.y & lanebit) ? c.w : c.z, d.x, d.y);
+                        }
+                        if (ng & 1u) {
+                            const uint4 a = lds128(ra), b = lds128(ra + 16);
+                            const uint2 m0 = lds64(rm);
+                            g_row(J0, J1, J2, (m0.x & lanebit) ? a.y : a.x, (m0.y & lanebit) ? a.w : a.z, b.x, b.y);
+                            ++q;
+                        }
+                        add3(J0, J1, J2, H0, H1, H2);
                     }
                     // D rows: the class bodies of the bit-sliced kernels (generated PTX)
                     for (const uint32_t e = q + nd; q < e; ++q) {

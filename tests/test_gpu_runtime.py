@@ -75,6 +75,9 @@ def _sanitize(tool, code, env=None, timeout=900):
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
                          env={**os.environ, **(env or {})})
     out = res.stdout + res.stderr
+    if "compute-sanitizer is closed on this pool" in out:
+        pytest.skip("compute-sanitizer is disabled on this GPU pool (runs under it left GPUs needing a "
+                    "reset); tests/test_gpu_runtime.py::test_guard_canaries checks out-of-bounds writes instead")
     assert res.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
     return out
@@ -110,6 +113,45 @@ def test_sanitizer_racecheck_smem_variants():
 def test_sanitizer_memcheck_smem_variants():
     out = _sanitize("memcheck", SMALL, env={"PZX_ACC": "smem"})
     assert "small ok" in out
+
+
+@pytest.mark.parametrize("kernel", ["auto", "page", "slice", "sorted", "general", "gray", "small"])
+def test_guard_canaries(ctx, kernel):
+    """Out-of-bounds writes without compute-sanitizer: every kernel writes its
+    results into the middle of a buffer whose guard regions on both sides are
+    filled with a canary; the guards must come back untouched and the results
+    must equal the POPC kernel's (ragged batch sizes, term-chunked grids)."""
+    import torch
+    e = synth.generate(18, 2500, 4, 60, 77)
+    t = ctx.compile_bit_table(e)
+    n = {"small": 1000, "gray": 20000 + 16, "sorted": 30000 + 5}.get(kernel, 40000 + 1024)
+    fl = {"auto": 0, "page": P.KERNEL_PAGE, "slice": P.KERNEL_SLICE, "sorted": P.KERNEL_SORTED,
+          "general": P.KERNEL_GENERAL, "gray": P.KERNEL_GRAY, "small": 0}[kernel]
+    G = 4096
+    canary = -1.2345e300
+    amp = torch.full((2 * (n + 2 * G),), canary, dtype=torch.float64, device="cuda:0")
+    prob = torch.full((n + 2 * G,), canary, dtype=torch.float64, device="cuda:0")
+    st = torch.cuda.current_stream().cuda_stream
+    words = None
+    if kernel == "sorted":
+        w = np.random.default_rng(1).integers(0, 1 << 18, n, dtype=np.uint64)
+        words = torch.from_numpy(w.view(np.int64)).cuda()
+    ctx.evaluate_device(t, n, d_assignments=words.data_ptr() if words is not None else 0, first=0,
+                        d_amp=amp.data_ptr() + 16 * G, d_prob=prob.data_ptr() + 8 * G, flags=fl | P.PROB_ABS2,
+                        stream=st)
+    torch.cuda.synchronize()
+    a = amp.cpu().numpy()
+    p = prob.cpu().numpy()
+    assert np.all(a[:2 * G] == canary) and np.all(a[2 * (G + n):] == canary)
+    assert np.all(p[:G] == canary) and np.all(p[G + n:] == canary)
+    got = a[2 * G:2 * (G + n)].view(np.complex128)
+    if words is not None:
+        want = ctx.evaluate_batch(t, w, flags=P.KERNEL_GENERAL)
+    else:
+        want = ctx.evaluate_range(t, 0, n, flags=P.KERNEL_GENERAL)
+    scale = np.abs(want).max()
+    assert np.max(np.abs(got - want)) <= 1e-12 * scale
+    assert np.max(np.abs(p[G:G + n] - np.abs(want) ** 2)) <= 1e-11 * scale ** 2
 
 
 # ---------------------------------------------------------------------------
@@ -163,8 +205,12 @@ def test_term_split_gpu_partials_over_gloo(world):
     import torch.multiprocessing as mp
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.SimpleQueue()
-    mp.start_processes(_rank_worker, args=(world, _free_port(), q), nprocs=world, join=True, start_method="spawn")
+    # read the result BEFORE joining: rank 0 blocks in put() until the parent reads
+    pc = mp.start_processes(_rank_worker, args=(world, _free_port(), q), nprocs=world, join=False,
+                            start_method="spawn")
     summed, det, full, ex, full_ex = q.get()
+    while not pc.join():
+        pass
     scale = np.abs(full).max()
     assert np.max(np.abs(summed - full)) <= 1e-12 * scale
     assert np.max(np.abs(det - full)) <= 1e-12 * scale
