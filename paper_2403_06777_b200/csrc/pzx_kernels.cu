@@ -1566,12 +1566,37 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                         uint32_t H0 = 0, H1 = 0, H2 = 0;
                         uint32_t ra = smem_u32(pg + 2 * q), rm = smem_u32(Mw + q);
                         const uint32_t e2 = q + (ng & ~1u);
+                        if (q < e2) {
+                            // software-pipelined one pair ahead: the next pair's six shared
+                            // loads are in flight while this pair's 14 LOP3 run (the read
+                            // past the last pair stays inside the CTA's shared window and
+                            // is never used)
+                            // two register sets alternate (no copies on the back edge)
+                            struct Pair { uint4 a, c; uint2 b, d, m0, m1; };
+                            auto load = [&](Pair& p, uint32_t r_, uint32_t m_) {
+                                p.a = lds128(r_); p.c = lds128(r_ + 32);
+                                p.b = lds64(r_ + 16); p.d = lds64(r_ + 48);
+                                p.m0 = lds64(m_); p.m1 = lds64(m_ + 8);
+                            };
+                            auto rows2 = [&](const Pair& p) {
+                                g_row(J0, J1, J2, (p.m0.x & lanebit) ? p.a.y : p.a.x, (p.m0.y & lanebit) ? p.a.w : p.a.z,
+                                      p.b.x, p.b.y);
+                                g_row(H0, H1, H2, (p.m1.x & lanebit) ? p.c.y : p.c.x, (p.m1.y & lanebit) ? p.c.w : p.c.z,
+                                      p.d.x, p.d.y);
+                            };
+                            Pair P0, P1;
+                            load(P0, ra, rm);
 #pragma unroll 1
-                        for (; q < e2; q += 2, ra += 64, rm += 16) {
-                            const uint4 a = lds128(ra), b = lds128(ra + 16), c = lds128(ra + 32), d = lds128(ra + 48);
-                            const uint2 m0 = lds64(rm), m1 = lds64(rm + 8);
-                            g_row(J0, J1, J2, (m0.x & lanebit) ? a.y : a.x, (m0.y & lanebit) ? a.w : a.z, b.x, b.y);
-                            g_row(H0, H1, H2, (m1.x & lanebit) ? c.y : c.x, (m1.y & lanebit) ? c.w : c.z, d.x, d.y);
+                            for (;;) {
+                                load(P1, ra + 64, rm + 16);
+                                rows2(P0);
+                                q += 2; ra += 64; rm += 16;
+                                if (q >= e2) break;
+                                load(P0, ra + 64, rm + 16);
+                                rows2(P1);
+                                q += 2; ra += 64; rm += 16;
+                                if (q >= e2) break;
+                            }
                         }
                         if (ng & 1u) {
                             const uint4 a = lds128(ra), b = lds128(ra + 16);
