@@ -735,7 +735,11 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
         b = cmul(b, pip);
     }
     // (sqrt2-1)^s pi^a pi'^b for s < 16, a, b < 4 (slice-kernel fast path),
-    // index s | a << 4 | b << 6, each rounded once from f128
+    // each rounded once from f128, at index sab_index(s, a, b): the low three
+    // bits of s XOR (a | b0 << 2), so that assignments with the same s but
+    // different pi counts read different shared-memory bank groups (the
+    // kernels form that index for free by XOR-ing the bit planes); a = b = 0
+    // keeps index s
     double* sab = reinterpret_cast<double*>(blob.data() + L.sab_off);
     for (int is = 0; is < 16; ++is)
         for (int ia = 0; ia < 4; ++ia)
@@ -744,7 +748,7 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
                 for (int k = 0; k < ia; ++k) v = cmul(v, pi);
                 for (int k = 0; k < ib; ++k) v = cmul(v, pip);
                 for (int k = 0; k < is; ++k) v = cmul(v, C128{f128_sqrt2() - 1, 0});
-                const int i = is | (ia << 4) | (ib << 6);
+                const int i = ((is & 7) ^ (ia | ((ib & 1) << 2))) | (is & 8) | (ia << 4) | (ib << 6);
                 sab[2 * i] = double(v.re);
                 sab[2 * i + 1] = double(v.im);
             }

@@ -779,7 +779,8 @@ __device__ __forceinline__ void slice_epilogue_fast(const SmemLut& L, const doub
         for (int r = 0; r < 4; ++r) {
             c[r] = crot[__byte_perm(kj, 0u, 0x4440u | uint32_t(r))];
             if constexpr (KINDS && AB > 0) {
-                f[r] = L.sab[__byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
+                const uint32_t k = __byte_perm(ks, 0u, 0x4440u | uint32_t(r));
+                f[r] = L.sab[k ^ ((k >> 4) & 3u) ^ (((k >> 6) & 1u) << 2)];  // the table's bank swizzle
             } else if constexpr (KINDS) {
                 f[r].x = reinterpret_cast<const double*>(L.sab)[2 * __byte_perm(ks, 0u, 0x4440u | uint32_t(r))];
                 f[r].y = 0.0;
@@ -869,14 +870,16 @@ template <int NT, int KIND, bool LC>
 __device__ __forceinline__ void slice_epilogue_tr(const SmemLut& L, const double2* crot, SliceAcc<NT, true>& acc,
                                                   uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
                                                   const KindCounters<NT, LC>& K) {
-    uint32_t Q[8] = {J0, J1, J2, Z, 0u, 0u, 0u, 0u};
+    // Z-marked assignments all read crot[15] (zero): OR-ing Z into the j planes
+    // keeps the dead lanes off the live entries' bank groups
+    uint32_t Q[8] = {J0 | Z, J1 | Z, J2 | Z, Z, 0u, 0u, 0u, 0u};
     if constexpr (KIND == 1) {
         Q[4] = K.S[0]; Q[5] = K.S[1]; Q[6] = K.S[2]; Q[7] = K.S[3];
     }
     transpose8_bytes(Q);
     uint32_t R[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    if constexpr (KIND == 2) {
-        R[0] = K.S[0]; R[1] = K.S[1]; R[2] = K.S[2]; R[3] = K.S[3];
+    if constexpr (KIND == 2) {  // key = sab_index(s, a, b): low s bits XOR (a | b0 << 2), the table's swizzle
+        R[0] = K.S[0] ^ K.A[0]; R[1] = K.S[1] ^ K.A[1]; R[2] = K.S[2] ^ K.B[0]; R[3] = K.S[3];
         R[4] = K.A[0]; R[5] = K.A[1]; R[6] = K.B[0]; R[7] = K.B[1];
         transpose8_bytes(R);
     }
