@@ -27,8 +27,18 @@
 #include "pzx_internal.h"
 #include "pzx_slice_dispatch.inc"
 #include "pzx_math.hpp"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a tool (nsys / ncu) is attached
 
 using namespace pzxb;
+
+namespace {
+// NVTX range scoped to a C-ABI call (SURVEY §5 tracing: upload / evaluate /
+// exact / reduce phases show up by name on an nsys or ncu timeline)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 // ------------------------------------------------------------ class table ----
 namespace {
@@ -834,6 +844,7 @@ cudaError_t upload_vec(void** dst, const std::vector<T>& v) {
 }
 
 pzx_status finish_upload(pzx_ctx* ctx, std::unique_ptr<pzx_table>& t, pzx_table** out) {
+    NvtxRange nv("pzx.table_upload");
     HostTable& h = t->host;
     pzx_status st;
     if ((st = cuda_err(ctx, cudaSetDevice(ctx->device), "cudaSetDevice"))) return st;
@@ -954,6 +965,7 @@ struct CallScratch {
 };
 
 pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t flags) {
+    NvtxRange nv("pzx.evaluate");
     if (!ctx || !t) return PZX_E_INVALID;
     if (t->device < 0) return set_err(ctx, PZX_E_INVALID, "host-only table (pzx_table_compile_host)");
     if (t->device != ctx->device) return set_err(ctx, PZX_E_INVALID, "table belongs to another device");
@@ -1196,6 +1208,7 @@ pzx_status build_exact(pzx_ctx* ctx, pzx_table* t) {
 }
 
 pzx_status exact_host(pzx_ctx* ctx, pzx_table* t, const uint64_t* asg, uint64_t first, uint64_t n, int64_t* out) {
+    NvtxRange nv("pzx.evaluate_exact");
     if (!ctx || !t || (n && !out)) return PZX_E_INVALID;
     if (t->device < 0 || !t->dev.rows) return set_err(ctx, PZX_E_INVALID, "evaluate_exact: host-only table");
     if (n == 0) return PZX_OK;
@@ -1689,7 +1702,14 @@ pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5
     return PZX_OK;
 }
 
+static pzx_status eval_host_impl(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
+                                 uint64_t n, double* amp, double* prob, uint32_t flags);
 static pzx_status eval_host(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
+                            uint64_t n, double* amp, double* prob, uint32_t flags) {
+    NvtxRange nv("pzx.evaluate_host (H2D + kernels + D2H)");
+    return eval_host_impl(ctx, t, asg, first, n, amp, prob, flags);
+}
+static pzx_status eval_host_impl(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
                             uint64_t n, double* amp, double* prob, uint32_t flags) {
     if (!ctx || !t) return PZX_E_INVALID;
     if (n == 0) return PZX_OK;

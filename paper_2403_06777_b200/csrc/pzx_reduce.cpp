@@ -45,6 +45,7 @@
 
 #include "pzx_gpu.h"
 #include "pzx_math.hpp"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace pzxb;
 
@@ -618,6 +619,8 @@ extern "C" {
 pzx_status pzx_circuit_reduce(uint32_t n_qubits, const pzx_gate* gates, uint64_t n_gates, const int32_t* in_spec,
                               const int32_t* out_spec, uint32_t mode, uint64_t max_terms, pzx_expr** out) {
     if (!out || (n_gates && !gates) || !out_spec || n_qubits == 0 || n_qubits > 4096) return PZX_E_INVALID;
+    nvtxRangePushA("pzx.circuit_reduce");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_exit;
     *out = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     std::unique_ptr<pzx_expr> ex(new (std::nothrow) pzx_expr);
