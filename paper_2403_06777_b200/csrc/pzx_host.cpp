@@ -17,8 +17,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <new>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -809,6 +812,11 @@ struct pzx_table {
     void* d_term_slot = nullptr;
     void* d_exact = nullptr;  // exact-evaluation tables (built on first pzx_evaluate_exact)
     ExactDev exact;
+    // device copies of term-chunk bounds, keyed by (term range, chunk count):
+    // immutable once written, so any stream may read them; saves a pageable
+    // H2D copy per call (it dominates small, launch-bound batches)
+    std::mutex chunk_mu;
+    std::map<std::tuple<uint64_t, uint64_t, int>, void*> chunk_cache;
 };
 
 namespace {
@@ -1068,13 +1076,31 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     if (kc == KC_SLICEWC) chunks *= kWarpChunksHost;  // 4 warp chunks per CTA row, always partials
     r.n_chunks = chunks;
     if (chunks > 1) {
-        std::vector<uint64_t> b;
-        chunk_bounds(t->host, r.term_begin, r.term_end, chunks, b);
         void* d_b = nullptr;
         void* d_p = nullptr;
-        if ((st = scratch.alloc(b.size() * 8, &d_b))) return st;
-        // pageable source: staged by the driver before the call returns, so `b` may go
-        if ((st = cuda_err(ctx, cudaMemcpyAsync(d_b, b.data(), b.size() * 8, cudaMemcpyHostToDevice, r.stream), "copy chunks"))) return st;
+        {
+            pzx_table* mt = const_cast<pzx_table*>(t);
+            std::lock_guard<std::mutex> lock(mt->chunk_mu);
+            const auto key = std::make_tuple(r.term_begin, r.term_end, chunks);
+            auto it = mt->chunk_cache.find(key);
+            if (it != mt->chunk_cache.end()) {
+                d_b = it->second;
+            } else {
+                std::vector<uint64_t> b;
+                chunk_bounds(t->host, r.term_begin, r.term_end, chunks, b);
+                if ((st = cuda_err(ctx, cudaMalloc(&d_b, b.size() * 8), "alloc chunks"))) return st;
+                if ((st = cuda_err(ctx, cudaMemcpy(d_b, b.data(), b.size() * 8, cudaMemcpyHostToDevice), "copy chunks"))) {
+                    cudaFree(d_b);
+                    return st;
+                }
+                if (mt->chunk_cache.size() >= 64) {  // bounded: term ranges vary in split runs
+                    cudaDeviceSynchronize();  // no call in flight may still read an evicted bound
+                    for (auto& kv : mt->chunk_cache) cudaFree(kv.second);
+                    mt->chunk_cache.clear();
+                }
+                mt->chunk_cache.emplace(key, d_b);
+            }
+        }
         if ((st = scratch.alloc(size_t(chunks) * r.n * 16, &d_p))) return st;
         r.d_chunk_terms = static_cast<const uint64_t*>(d_b);
         r.d_partial = static_cast<double2*>(d_p);
@@ -1644,6 +1670,7 @@ void pzx_table_free(pzx_table* t) {
     for (void* p : {t->d_rows, t->d_term_row, t->d_term_c, t->d_lut, t->d_srows, t->d_sterm_c, t->d_qrows, t->d_exact,
                     t->d_prows, t->d_term_slot})
         if (p) cudaFree(p);
+    for (auto& kv : t->chunk_cache) cudaFree(kv.second);
     delete t;
 }
 

@@ -32,6 +32,55 @@
 #include "pzx_internal.h"
 #include "pzx_slice_dispatch.inc"
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
+namespace {
+// Per-launch host overhead matters for small batches (C1: ~0.1 ms steps), so
+// the two driver queries every launch used to make are cached per device:
+// the dynamic shared-memory opt-in (cudaFuncSetAttribute only when a kernel
+// needs more than it was last granted) and the occupancy per (kernel, block
+// size, shared memory).
+std::mutex g_attr_mu;
+std::map<std::tuple<int, const void*>, size_t> g_smem_set;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+
+int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+template <class K>
+cudaError_t set_max_smem(K* kern, size_t smem) {
+    const auto key = std::make_tuple(cur_device(), reinterpret_cast<const void*>(kern));
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    auto it = g_smem_set.find(key);
+    if (it != g_smem_set.end() && it->second >= smem) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e == cudaSuccess) g_smem_set[key] = smem;
+    return e;
+}
+
+template <class K>
+cudaError_t cached_occupancy(int* nb, K* kern, int threads, size_t smem) {
+    const auto key = std::make_tuple(cur_device(), reinterpret_cast<const void*>(kern), threads, smem);
+    {
+        std::lock_guard<std::mutex> lock(g_attr_mu);
+        auto it = g_occ.find(key);
+        if (it != g_occ.end()) { *nb = it->second; return cudaSuccess; }
+    }
+    cudaError_t e = set_max_smem(kern, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, kern, threads, smem);
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lock(g_attr_mu);
+        g_occ[key] = *nb;
+    }
+    return e;
+}
+}  // namespace
+
 namespace pzxb {
 
 // PZX_ACC=smem keeps the accumulators in shared memory (A/B comparisons)
@@ -2029,7 +2078,7 @@ template <class KernelT>
 cudaError_t launch_one(KernelT kern, dim3 grid, size_t smem, cudaStream_t s, const DevTable& t,
                        const LaunchReq& r) {
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e = set_max_smem(kern, smem);
         if (e != cudaSuccess) return e;
     }
     kern<<<grid, kThreads, smem, s>>>(t, r);
@@ -2051,7 +2100,7 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
             if (!tm) return cudaErrorNotSupported;
             kern = wide ? k_eval_sorted<true, kSortedGroupsWide, 256, true> : k_eval_sorted<true, kSortedGroups, 128, true>;
         }
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(kern, sm);
         if (e != cudaSuccess) return e;
         kern<<<grid, sorted_threads(r.sorted_groups), sm, r.stream>>>(t, r);
         return cudaGetLastError();
@@ -2059,7 +2108,7 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
     if (kc == KC_SLICEWC) {
         const size_t sm = slicewc_smem_bytes<P64>(t);
         auto kern = r.d_dbg5 ? k_eval_slice_wc<P64, true> : k_eval_slice_wc<P64>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(kern, sm);
         if (e != cudaSuccess) return e;
         kern<<<dim3(grid.x, grid.y / kWarpChunks), kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
@@ -2067,14 +2116,14 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
     if (kc == KC_PAGE) {
         const size_t sm = page_smem_bytes(t);
         auto kern = r.d_dbg5 ? k_eval_page<true> : k_eval_page<false>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(kern, sm);
         if (e != cudaSuccess) return e;
         kern<<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
     }
     if (kc == KC_SLICE2) {
         const size_t sm = slice2_smem_bytes<P64>(t);
-        cudaError_t e = cudaFuncSetAttribute(k_eval_slice2<P64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(k_eval_slice2<P64>, sm);
         if (e != cudaSuccess) return e;
         k_eval_slice2<P64><<<grid, kSliceThreads, sm, r.stream>>>(t, r);
         return cudaGetLastError();
@@ -2094,7 +2143,7 @@ cudaError_t launch_typed(const DevTable& t, const LaunchReq& r, KernelChoice kc,
             if (rnd || small || !tm) return cudaErrorNotSupported;
             kern = k_eval_slice<P64, false, 128, true, true>;
         }
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(kern, sm);
         if (e != cudaSuccess) return e;
         kern<<<grid, small ? 32 : 128, sm, r.stream>>>(t, r);
         return cudaGetLastError();
@@ -2172,30 +2221,26 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
     int nb = 0;
     size_t sm = (t.p64 ? smem_lut_offset<true>() : smem_lut_offset<false>()) + t.lut_layout.bytes;
     cudaError_t e;
-#define PZX_OCC(K) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, K, kThreads, sm)
+#define PZX_OCC(K) e = cached_occupancy(&nb, K, kThreads, sm)
     const bool tm = tmem_accumulators();
     if (kc == KC_SLICEWC) {
         sm = t.p64 ? slicewc_smem_bytes<true>(t) : slicewc_smem_bytes<false>(t);
         auto kern = t.p64 ? k_eval_slice_wc<true> : k_eval_slice_wc<false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+        e = cached_occupancy(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_PAGE) {
         sm = page_smem_bytes(t);
-        cudaFuncSetAttribute(k_eval_page<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_page<false>, kSliceThreads, sm);
+        e = cached_occupancy(&nb, k_eval_page<false>, kSliceThreads, sm);
     } else if (kc == KC_SLICE2) {
         sm = t.p64 ? slice2_smem_bytes<true>(t) : slice2_smem_bytes<false>(t);
         auto kern = t.p64 ? k_eval_slice2<true> : k_eval_slice2<false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSliceThreads, sm);
+        e = cached_occupancy(&nb, kern, kSliceThreads, sm);
     } else if (kc == KC_SORTED) {
         const bool wide = sorted_groups > kSortedGroups;
         sm = wide ? (tm ? sorted_smem_bytes<true, kSortedGroupsWide, 256>(t) : sorted_smem_bytes<false, kSortedGroupsWide>(t))
                   : (tm ? sorted_smem_bytes<true>(t) : sorted_smem_bytes<false>(t));
         auto kern = wide ? (tm ? k_eval_sorted<true, kSortedGroupsWide, 256> : k_eval_sorted<false, kSortedGroupsWide>)
                          : (tm ? k_eval_sorted<true> : k_eval_sorted<false>);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, sorted_threads(sorted_groups), sm);
+        e = cached_occupancy(&nb, kern, sorted_threads(sorted_groups), sm);
     } else if (kc == KC_SLICE || kc == KC_SLICER) {
         const bool rnd = kc == KC_SLICER;
         if (nt == 32) {
@@ -2203,8 +2248,7 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
                               : (rnd ? k_eval_slice<false, true, 32> : k_eval_slice<false, false, 32>);
             sm = t.p64 ? (rnd ? slice_smem_bytes<true, true, 32>(t) : slice_smem_bytes<true, false, 32>(t))
                        : (rnd ? slice_smem_bytes<false, true, 32>(t) : slice_smem_bytes<false, false, 32>(t));
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, sm);
+            e = cached_occupancy(&nb, kern, 32, sm);
         } else {
             auto kern = t.p64 ? (rnd ? k_eval_slice<true, true, 128>
                                  : tm ? k_eval_slice<true, false, 128, true> : k_eval_slice<true, false, 128>)
@@ -2214,8 +2258,7 @@ int resident_ctas_per_sm(const DevTable& t, KernelChoice kc, int nt, int sorted_
                           : tm ? slice_smem_bytes<true, false, 128, true>(t) : slice_smem_bytes<true, false, 128>(t))
                        : (rnd ? slice_smem_bytes<false, true, 128>(t)
                           : tm ? slice_smem_bytes<false, false, 128, true>(t) : slice_smem_bytes<false, false, 128>(t));
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, sm);
+            e = cached_occupancy(&nb, kern, 128, sm);
         }
     } else if (kc == KC_GRAY) {
         if (t.p64) { if (lng) PZX_OCC((k_eval_gray<true, kGrayBits, true>)); else PZX_OCC((k_eval_gray<true, kGrayBits, false>)); }
@@ -2917,7 +2960,7 @@ cudaError_t launch_exact(const DevTable& t, const ExactDev& x, const uint64_t* d
               : kx == 1 ? (t.p64 ? k_eval_exact<true, 1> : k_eval_exact<false, 1>)
                         : (t.p64 ? k_eval_exact<true, 2> : k_eval_exact<false, 2>);
     if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_max_smem(kern, sm);
         if (e != cudaSuccess) return e;
     }
     const dim3 grid(unsigned((n + kExactThreads * kx - 1) / (kExactThreads * kx)), unsigned(n_chunks));
