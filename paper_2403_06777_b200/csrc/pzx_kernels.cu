@@ -2016,6 +2016,38 @@ __global__ void k_reduce_partials(const double2* __restrict__ partial, int n_chu
     if (prob) prob[i] = prob_mode == 2 ? s.x : s.x * s.x + s.y * s.y;
 }
 
+// Few assignments, many term chunks (C1: 256 x 592, C4: 1024 x 4736): one
+// warp per assignment, lane l sums chunks l, l + 32, ... in order, then a
+// fixed shuffle tree -- deterministic, and the chunk reads of an assignment
+// are spread over 32 lanes instead of one thread's serial chain.
+__global__ void k_reduce_partials_warp(const double2* __restrict__ partial, int n_chunks, uint64_t n,
+                                       double2* amp, double* prob, int prob_mode, int accumulate,
+                                       const uint32_t* __restrict__ perm) {
+    const uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (k >= n) return;
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = int(lane); c < n_chunks; c += 32) {
+        const double2 v = partial[uint64_t(c) * n + k];
+        s.x += v.x;
+        s.y += v.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_down_sync(0xFFFFFFFFu, s.x, o);
+        s.y += __shfl_down_sync(0xFFFFFFFFu, s.y, o);
+    }
+    if (lane != 0) return;
+    const uint64_t i = perm ? perm[k] : k;
+    if (i == 0xFFFFFFFFu) return;
+    if (accumulate) {
+        s.x += amp[i].x;
+        s.y += amp[i].y;
+    }
+    if (amp) amp[i] = s;
+    if (prob) prob[i] = prob_mode == 2 ? s.x : s.x * s.x + s.y * s.y;
+}
+
 __global__ void k_amp_to_prob(const double2* __restrict__ amp, uint64_t n, double* prob, int mode) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -2281,9 +2313,14 @@ cudaError_t launch_evaluate(const DevTable& t, const LaunchReq& r, KernelChoice 
     ++*launches;
     if (e != cudaSuccess || r.n_chunks <= 1) return e;
     const int tpb = 256;
-    k_reduce_partials<<<int((r.n + tpb - 1) / tpb), tpb, 0, r.stream>>>(r.d_partial, r.n_chunks, r.n, r.d_amp,
-                                                                        r.d_prob, r.prob_mode, r.accumulate,
-                                                                        r.d_perm);
+    if (r.n_chunks >= 64 && r.n * 32 <= uint64_t(1) << 22) {  // few assignments, many chunks
+        k_reduce_partials_warp<<<int((r.n * 32 + tpb - 1) / tpb), tpb, 0, r.stream>>>(
+            r.d_partial, r.n_chunks, r.n, r.d_amp, r.d_prob, r.prob_mode, r.accumulate, r.d_perm);
+    } else {
+        k_reduce_partials<<<int((r.n + tpb - 1) / tpb), tpb, 0, r.stream>>>(r.d_partial, r.n_chunks, r.n, r.d_amp,
+                                                                            r.d_prob, r.prob_mode, r.accumulate,
+                                                                            r.d_perm);
+    }
     ++*launches;
     return cudaGetLastError();
 }
