@@ -166,17 +166,20 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
  * row), term_kinds = terms whose epilogue is kind-free / lambda-only / with a
  * pi or pi' row. Either pointer may be NULL. */
 pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]);
-/* Rows per page family {constraint, generic, dispatch, dropped} and the
- * dispatch rows per op (bench.py's roofline of the page kernel); any table
- * with a page layout, PZX_E_CAPACITY otherwise. */
-pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[4], uint64_t d_op_rows[129]);
+/* Rows per page family: {constraint, generic, dispatch, dropped, lambda} and
+ * the generic rows by update class {S2, S6, E0, E2, GG} (pzx_host.cpp,
+ * page_term) -- PZX_PAGE_FAMILIES counts -- and the dispatch rows per op
+ * (bench.py's roofline of the page kernel); any table with a page layout,
+ * PZX_E_CAPACITY otherwise. */
+#define PZX_PAGE_FAMILIES 10
+pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[PZX_PAGE_FAMILIES], uint64_t d_op_rows[129]);
 /* Host-only tables (pzx_table_compile_host): the page layout of the
  * enumerated page kernel -- *n_slots 32-byte records (8 x u32 each; slots may
  * be NULL to query the size), the header slot of every term, the w^j folded
- * into each term's page constant, and the rows per family {constraint,
- * generic, dispatch, dropped}. PZX_E_CAPACITY: the table has no page layout. */
+ * into each term's page constant, and the rows per family (as
+ * pzx_table_page_stats). PZX_E_CAPACITY: the table has no page layout. */
 pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* n_slots, uint32_t* term_slot,
-                                 uint8_t* jfold, uint64_t family_rows[4]);
+                                 uint8_t* jfold, uint64_t family_rows[PZX_PAGE_FAMILIES]);
 /* Folded exact constant C'_t (a,b,c,d,exp), sqrt2 exponent E_t and the count
  * nLM_t of lambda/mu rows of term t (see pzx_term_code). */
 pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5],

@@ -190,7 +190,8 @@ struct HostTable {
     std::vector<PendRow> pend;              // rows of the open term
     uint32_t page_fill = 0;                 // slots used in the open page
     int64_t last_hdr = -1;                  // slot of the last header written
-    uint64_t page_rows[4] = {};             // rows by family: constraint, G, dispatch, dropped
+    uint64_t page_rows[5] = {};             // rows by family: constraint, G, dispatch, dropped, L
+    uint64_t page_gsub[5] = {};             // G rows by update class: S2, S6, E0, E2, GG
     uint64_t page_d_ops[kSliceOps] = {};    // dispatch-family rows per op (the roofline's D bodies)
     bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
     uint64_t n_dev_rows() const { return unit.size(); }
@@ -306,19 +307,24 @@ void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
 //   G (generic monomial): value w^(c0 + (k + 4p')(q' ^ inv)) sqrt2^e g, g constant
 //       (every class with ka or kb in {0,4}: 28 of 64, ~83 % of the rows of the
 //       BASELINE tables)                                   -> branch-free J += (k + 4p')q~
+//   L (lambda): one parity, no zero, exactly one lambda/mu variant
+//       (terms with < 16 lambda-capable rows)              -> J += k p, S += p ^ inv
 //   D (dispatch): zero-pair / lambda / pi / pi' rows       -> the generated class bodies
 // and rows whose reachable variants are equal are dropped (their w^j goes
 // into the term constant like every c0; their sqrt2^e and mu are already in
-// E_t / nLM_t). Records (8 x u32):
-//   header: {C_page (double2), counts nc | ng << 8 | nd << 16 | last_in_page << 24, 0, 0, 0}
+// E_t / nLM_t). Records (8 x u32), in the order header, C, G, L, D:
+//   header: {C_page (double2), nc | n_gg << 8 | nd << 16 | last_in_page << 24, nl,
+//            n_s2 | n_s6 << 8 | n_e0 << 16 | n_e2 << 24, 0}
+// with the G rows in the order S2, S6, E0, E2, GG (page_term: by update cost)
 //   C: {W ^ zc, ~(W ^ zc), 0, 0, 0, 0, psi, 0}
 //   G: {A = W(x) ^ K2, ~A, B = W(y) ^ INV, ~B, K0, K1, x-mask, y-mask}
+//   L: {W ^ INV, ~(W ^ INV), W, ~W, K0, K1, psi, K2}
 //   D: {W(psi), ~W(psi), W(phi), ~W(phi), op | kind flags, op, psi, phi}
 // W = Walsh32 of the mask (bit g = parity(mask & g)); Kc = all ones when bit c of k is set.
-struct PageRec { int fam; uint32_t w[8]; int jfold; };
+struct PageRec { int fam; uint32_t w[8]; int jfold; uint32_t dw[8]; int djfold; };  // dw / djfold: the D form of an L row
 
 PageRec classify_page_row(uint64_t psi, uint64_t phi, uint32_t op) {
-    PageRec r{3, {0, 0, 0, 0, 0, 0, 0, 0}, 0};
+    PageRec r{3, {0, 0, 0, 0, 0, 0, 0, 0}, 0, {0, 0, 0, 0, 0, 0, 0, 0}, 0};
     const SliceOp so = slice_op(int(op));
     const bool single = phi == 0;
     const int kinds = so.lam_tt | so.pi_tt | so.pip_tt;
@@ -331,6 +337,20 @@ PageRec classify_page_row(uint64_t psi, uint64_t phi, uint32_t op) {
         r.jfold = so.jbase;
         return r;
     };
+    // L (single-parity lambda/mu row, one lambda variant): J += k p, S += p ^ inv
+    if (single && so.lam_tt && !so.pi_tt && !so.pip_tt && !(so.zero_tt & 3) && (so.lam_tt & 3) != 3) {
+        dispatch();  // keep the D form: the term may have too many lambda rows for the fast counters
+        std::memcpy(r.dw, r.w, sizeof r.w);
+        r.djfold = r.jfold;
+        const int k = (jv(1) - jv(0)) & 7;
+        const uint32_t INV = (so.lam_tt & 1) ? ~0u : 0u;  // variant 0 is the lambda one: Lambda = ~p
+        r.fam = 5;
+        r.w[0] = Wp ^ INV; r.w[1] = ~(Wp ^ INV); r.w[2] = Wp; r.w[3] = ~Wp;
+        r.w[4] = (k & 1) ? ~0u : 0u; r.w[5] = (k & 2) ? ~0u : 0u; r.w[6] = uint32_t(psi);
+        r.w[7] = (k & 4) ? ~0u : 0u;
+        r.jfold = jv(0);
+        return r;
+    }
     if (kinds) return dispatch();
     if (single) {
         const int z = so.zero_tt & 3;
@@ -390,19 +410,50 @@ void page_pad(HostTable& h) {
 
 // the open term's rows -> one header + C, G, D records; returns its j fold
 int page_term(HostTable& h, const C128& cpp) {
-    std::vector<PageRec> fam[3];
-    int jf = 0;
+    // families in record order: 0 C, 1 G, 2 L, 3 D
+    std::vector<PageRec> recs;
+    recs.reserve(h.pend.size());
+    int n_lam = 0, n_l = 0;  // rows that can bump the lambda counter / L candidates
     for (const auto& pr : h.pend) {
-        const PageRec r = classify_page_row(pr.psi, pr.phi, pr.op);
+        recs.push_back(classify_page_row(pr.psi, pr.phi, pr.op));
+        n_l += recs.back().fam == 5;
+        n_lam += (kSliceKindFlags[pr.op] & int(kSliceLamFlag)) != 0;
+    }
+    // the L loop keeps the lambda counter in its 4 register planes: a term
+    // with >= 16 lambda-capable rows sends its L rows to the dispatch loop
+    const bool l_ok = n_lam < 16;
+    std::vector<PageRec> fam[4];
+    int jf = 0;
+    for (size_t i = 0; i < recs.size(); ++i) {
+        PageRec r = recs[i];
+        if (r.fam == 5 && !l_ok) {
+            std::memcpy(r.w, r.dw, sizeof r.w);
+            r.jfold = r.djfold;
+            r.fam = 3;
+        }
         jf += r.jfold;
         if (r.fam == 4) { h.page_rows[3] += 1; continue; }
-        const int f = r.fam == 0 ? 0 : r.fam == 1 ? 1 : 2;
-        h.page_rows[f] += 1;
-        if (f == 2) h.page_d_ops[pr.op] += 1;
+        const int f = r.fam == 0 ? 0 : r.fam == 1 ? 1 : r.fam == 5 ? 2 : 3;
+        h.page_rows[f == 2 ? 4 : f == 3 ? 2 : f] += 1;  // stats order: C, G, D, dropped, L
+        if (f == 3) h.page_d_ops[h.pend[i].op] += 1;
         fam[f].push_back(r);
     }
+    (void)n_l;
     h.pend.clear();
-    const uint32_t n = uint32_t(1 + fam[0].size() + fam[1].size() + fam[2].size());
+    // G rows by update cost (k = the record's K0 | K1 << 1; single rows have x-mask 0, X = K2):
+    //   0 S2: single, J += 2q        1 S6: single, J += 6q        (J2 ^= q & J1 (~J1); J1 ^= q)
+    //   2 E0: k = 0 (and single J += 4q)  J2 ^= X & Y
+    //   3 E2: k = 2                       J2 ^= Y & (J1 ^ X); J1 ^= Y
+    //   4 GG: odd k                       g_row
+    std::vector<PageRec> gsub[5];
+    for (const PageRec& r : fam[1]) {
+        const int k = (r.w[4] ? 1 : 0) | (r.w[5] ? 2 : 0);
+        const bool single = r.w[6] == 0;
+        const int sc = (single && k == 2) ? (r.w[0] ? 1 : 0) : k == 0 ? 2 : k == 2 ? 3 : 4;
+        gsub[sc].push_back(r);
+        h.page_gsub[sc] += 1;
+    }
+    const uint32_t n = uint32_t(1 + fam[0].size() + fam[1].size() + fam[2].size() + fam[3].size());
     if (n > uint32_t(kPageSlots)) {  // a term must fit one page: no page layout for this table
         h.want_prows = false;
         std::vector<uint4>().swap(h.prows);
@@ -419,13 +470,22 @@ int page_term(HostTable& h, const C128& cpp) {
     h.term_slot.push_back(uint32_t(h.prows.size() / 2));
     h.last_hdr = int64_t(h.prows.size() / 2);
     h.prows.push_back(make_uint4(q[0], q[1], q[2], q[3]));
-    h.prows.push_back(make_uint4(uint32_t(fam[0].size()) | uint32_t(fam[1].size()) << 8 |
-                                     uint32_t(fam[2].size()) << 16, 0, 0, 0));
-    for (int f = 0; f < 3; ++f)
-        for (const PageRec& r : fam[f]) {
+    h.prows.push_back(make_uint4(uint32_t(fam[0].size()) | uint32_t(gsub[4].size()) << 8 |
+                                     uint32_t(fam[3].size()) << 16,
+                                 uint32_t(fam[2].size()),
+                                 uint32_t(gsub[0].size()) | uint32_t(gsub[1].size()) << 8 |
+                                     uint32_t(gsub[2].size()) << 16 | uint32_t(gsub[3].size()) << 24,
+                                 0));
+    auto put = [&](const std::vector<PageRec>& v) {
+        for (const PageRec& r : v) {
             h.prows.push_back(make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]));
             h.prows.push_back(make_uint4(r.w[4], r.w[5], r.w[6], r.w[7]));
         }
+    };
+    put(fam[0]);
+    for (int sc = 0; sc < 5; ++sc) put(gsub[sc]);
+    put(fam[2]);
+    put(fam[3]);
     h.page_fill += n;
     if (h.page_fill == uint32_t(kPageSlots)) page_pad(h);
     return jf & 7;
@@ -631,7 +691,8 @@ void merge_into(HostTable& h, HostTable& part) {
         app(h.prows, part.prows);
         app(h.jp_t, part.jp_t);
         if (part.last_hdr >= 0) h.last_hdr = int64_t(base_slot) + part.last_hdr;
-        for (int i = 0; i < 4; ++i) h.page_rows[i] += part.page_rows[i];
+        for (int i = 0; i < 5; ++i) h.page_rows[i] += part.page_rows[i];
+        for (int i = 0; i < 5; ++i) h.page_gsub[i] += part.page_gsub[i];
         for (int i = 0; i < kSliceOps; ++i) h.page_d_ops[i] += part.page_d_ops[i];
     } else if (h.want_prows) {
         h.want_prows = false;
@@ -1685,12 +1746,14 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
 }
 
 pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* n_slots, uint32_t* term_slot,
-                                 uint8_t* jfold, uint64_t family_rows[4]) {
+                                 uint8_t* jfold, uint64_t family_rows[PZX_PAGE_FAMILIES]) {
     if (!t || !n_slots) return PZX_E_INVALID;
     const HostTable& h = t->host;
     if (!h.want_prows || h.term_slot.size() != h.coef.size()) { *n_slots = 0; return PZX_E_CAPACITY; }
-    if (family_rows)
-        for (int i = 0; i < 4; ++i) family_rows[i] = h.page_rows[i];
+    if (family_rows) {
+        for (int i = 0; i < 5; ++i) family_rows[i] = h.page_rows[i];
+        for (int i = 0; i < 5; ++i) family_rows[5 + i] = h.page_gsub[i];
+    }
     if (h.prows.empty() && t->device >= 0) { *n_slots = 0; return PZX_E_INVALID; }  // uploaded: host copy released
     *n_slots = h.prows.size() / 2;
     if (slots) std::memcpy(slots, h.prows.data(), h.prows.size() * 16);
@@ -1699,12 +1762,14 @@ pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* 
     return PZX_OK;
 }
 
-pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[4], uint64_t d_op_rows[129]) {
+pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[PZX_PAGE_FAMILIES], uint64_t d_op_rows[129]) {
     if (!t) return PZX_E_INVALID;
     const HostTable& h = t->host;
     if (!h.want_prows || h.term_slot.size() != h.coef.size()) return PZX_E_CAPACITY;
-    if (family_rows)
-        for (int i = 0; i < 4; ++i) family_rows[i] = h.page_rows[i];
+    if (family_rows) {
+        for (int i = 0; i < 5; ++i) family_rows[i] = h.page_rows[i];
+        for (int i = 0; i < 5; ++i) family_rows[5 + i] = h.page_gsub[i];
+    }
     if (d_op_rows)
         for (int i = 0; i < kSliceOps; ++i) d_op_rows[i] = h.page_d_ops[i];
     return PZX_OK;

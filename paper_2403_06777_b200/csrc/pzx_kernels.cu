@@ -1492,7 +1492,8 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
 // so the row loops form X = parity ? ~W : W with a predicate test of M and a
 // SEL -- no per-thread POPC. Per row and warp:
 //   C: Z |= X                                            (6 instructions)
-//   G: J += (k + 4p)q~, branch-free ripple add           (~16, no jump)
+//   G: J += (k + 4p)q~, branch-free, by update class     (~7-16, no jump)
+//   L: J += k p, S += p ^ inv (single-parity lambda rows) (~20, no jump)
 //   D: the generated class body through the jump table   (the slice kernel's)
 // After a term's C rows a warp whose 1024 assignments are all zero skips the
 // rest of the term (constraint-first order, PAPER "Conclusions").
@@ -1528,6 +1529,90 @@ __device__ __forceinline__ void add3(uint32_t& J0, uint32_t& J1, uint32_t& J2, u
     const uint32_t c1 = (J1 & H1) | (c0 & (J1 ^ H1));
     J1 ^= H1 ^ c0;
     J2 ^= H2 ^ c1;
+}
+
+// One class of G rows (records at shared address ra, lane words at rm; both
+// advanced past the n rows), software-pipelined one pair ahead: the next
+// pair's shared loads are in flight while this pair computes (two register
+// sets alternate, no copies on the back edge; the read past the last pair stays
+// inside the CTA's shared window and is never used). Per row, X / Y = the
+// record's word or its complement by this lane's parity bit:
+//   kGS : Y only;  J2 ^= Y & J1, J1 ^= Y                   (J += 2Y)
+//   kGE0: J2 ^= X & Y                                       (J += 4XY)
+//   kGE2: J2 ^= Y & (J1 ^ X), J1 ^= Y                       (J += 2Y + 4XY)
+//   kGG : g_row                                             (J += (k + 4X) Y)
+constexpr int kGS = 0, kGE0 = 1, kGE2 = 2, kGG = 3;
+
+template <int V>
+struct GRow {
+    uint4 a;
+    uint2 b, m;
+};
+
+template <int V>
+__device__ __forceinline__ void g_load(GRow<V>& r, uint32_t ra, uint32_t rm) {
+    if constexpr (V == kGS) {
+        const uint2 t = lds64(ra + 8);
+        r.a.z = t.x;
+        r.a.w = t.y;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.m.y) : "r"(rm + 4));
+    } else {
+        r.a = lds128(ra);
+        r.m = lds64(rm);
+        if constexpr (V == kGG) r.b = lds64(ra + 16);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void g_apply(const GRow<V>& r, uint32_t lanebit, uint32_t& J0, uint32_t& J1,
+                                        uint32_t& J2) {
+    const uint32_t Y = (r.m.y & lanebit) ? r.a.w : r.a.z;
+    if constexpr (V == kGS) {
+        J2 ^= Y & J1;
+        J1 ^= Y;
+    } else {
+        const uint32_t X = (r.m.x & lanebit) ? r.a.y : r.a.x;
+        if constexpr (V == kGE0) {
+            J2 ^= X & Y;
+        } else if constexpr (V == kGE2) {
+            J2 ^= Y & (J1 ^ X);
+            J1 ^= Y;
+        } else {
+            g_row(J0, J1, J2, X, Y, r.b.x, r.b.y);
+        }
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void g_loop(uint32_t& ra, uint32_t& rm, uint32_t n, uint32_t lanebit, uint32_t& J0,
+                                       uint32_t& J1, uint32_t& J2, uint32_t& H0, uint32_t& H1, uint32_t& H2) {
+    const uint32_t e2 = ra + 32u * (n & ~1u);
+    if (ra < e2) {
+        GRow<V> P0[2], P1[2];
+        g_load(P0[0], ra, rm);
+        g_load(P0[1], ra + 32, rm + 8);
+#pragma unroll 1
+        for (;;) {
+            g_load(P1[0], ra + 64, rm + 16);
+            g_load(P1[1], ra + 96, rm + 24);
+            g_apply(P0[0], lanebit, J0, J1, J2);
+            g_apply(P0[1], lanebit, H0, H1, H2);
+            ra += 64; rm += 16;
+            if (ra >= e2) break;
+            g_load(P0[0], ra + 64, rm + 16);
+            g_load(P0[1], ra + 96, rm + 24);
+            g_apply(P1[0], lanebit, J0, J1, J2);
+            g_apply(P1[1], lanebit, H0, H1, H2);
+            ra += 64; rm += 16;
+            if (ra >= e2) break;
+        }
+    }
+    if (n & 1u) {
+        GRow<V> r;
+        g_load(r, ra, rm);
+        g_apply(r, lanebit, J0, J1, J2);
+        ra += 32; rm += 8;
+    }
 }
 
 size_t page_smem_bytes(const DevTable& t) {
@@ -1599,7 +1684,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
             __syncwarp();
             while (term < te) {
                 const uint4 h0 = pg[2 * s], h1 = pg[2 * s + 1];
-                const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu;
+                const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu, nl = h1.y;
                 uint32_t q = s + 1;
                 // C rows: parity constraints
                 for (const uint32_t e = q + nc; q < e; ++q) {
@@ -1608,55 +1693,49 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                 }
                 const bool dead = nc != 0 && __all_sync(0xFFFFFFFFu, Z == 0xFFFFFFFFu);
                 if (dead) {
-                    q += ng + nd;
+                    q += ng + nl + nd + (h1.z & 0xFFu) + ((h1.z >> 8) & 0xFFu) + ((h1.z >> 16) & 0xFFu) + (h1.z >> 24);
                 } else {
-                    // G rows: J += (k + 4p) q~ with X = p ^ K2, Y = q~, K0 / K1 the low bits
-                    // of k -- 7 LOP3 (g_row). Pairs of rows go to two counters (J, H) so
-                    // consecutive rows do not wait on each other's ripple carries; H is
-                    // added into J once, after the G rows.
+                    // G rows, by update class (page_term): S2 / S6 (single parity, J += 2q / 6q),
+                    // E0 (J2 ^= X & Y), E2 (J += 2Y + 4XY), GG (any k: g_row, 7 LOP3). Pairs of
+                    // rows go to two counters (J, H) so consecutive rows do not wait on each
+                    // other's carries; H is added into J once, after the G rows.
                     {
                         uint32_t H0 = 0, H1 = 0, H2 = 0;
                         uint32_t ra = smem_u32(pg + 2 * q), rm = smem_u32(Mw + q);
-                        const uint32_t e2 = q + (ng & ~1u);
-                        if (q < e2) {
-                            // software-pipelined one pair ahead: the next pair's six shared
-                            // loads are in flight while this pair's 14 LOP3 run (the read
-                            // past the last pair stays inside the CTA's shared window and
-                            // is never used)
-                            // two register sets alternate (no copies on the back edge)
-                            struct Pair { uint4 a, c; uint2 b, d, m0, m1; };
-                            auto load = [&](Pair& p, uint32_t r_, uint32_t m_) {
-                                p.a = lds128(r_); p.c = lds128(r_ + 32);
-                                p.b = lds64(r_ + 16); p.d = lds64(r_ + 48);
-                                p.m0 = lds64(m_); p.m1 = lds64(m_ + 8);
-                            };
-                            auto rows2 = [&](const Pair& p) {
-                                g_row(J0, J1, J2, (p.m0.x & lanebit) ? p.a.y : p.a.x, (p.m0.y & lanebit) ? p.a.w : p.a.z,
-                                      p.b.x, p.b.y);
-                                g_row(H0, H1, H2, (p.m1.x & lanebit) ? p.c.y : p.c.x, (p.m1.y & lanebit) ? p.c.w : p.c.z,
-                                      p.d.x, p.d.y);
-                            };
-                            Pair P0, P1;
-                            load(P0, ra, rm);
-#pragma unroll 1
-                            for (;;) {
-                                load(P1, ra + 64, rm + 16);
-                                rows2(P0);
-                                q += 2; ra += 64; rm += 16;
-                                if (q >= e2) break;
-                                load(P0, ra + 64, rm + 16);
-                                rows2(P1);
-                                q += 2; ra += 64; rm += 16;
-                                if (q >= e2) break;
-                            }
+                        const uint32_t ns2 = h1.z & 0xFFu, ns6 = (h1.z >> 8) & 0xFFu, ne0 = (h1.z >> 16) & 0xFFu,
+                                       ne2 = h1.z >> 24;
+                        g_loop<kGS>(ra, rm, ns2, lanebit, J0, J1, J2, H0, H1, H2);
+                        if (ns6) {  // J += 6q: the S update on ~J1
+                            J1 = ~J1; H1 = ~H1;
+                            g_loop<kGS>(ra, rm, ns6, lanebit, J0, J1, J2, H0, H1, H2);
+                            J1 = ~J1; H1 = ~H1;
                         }
-                        if (ng & 1u) {
-                            const uint4 a = lds128(ra), b = lds128(ra + 16);
-                            const uint2 m0 = lds64(rm);
-                            g_row(J0, J1, J2, (m0.x & lanebit) ? a.y : a.x, (m0.y & lanebit) ? a.w : a.z, b.x, b.y);
-                            ++q;
-                        }
+                        g_loop<kGE0>(ra, rm, ne0, lanebit, J0, J1, J2, H0, H1, H2);
+                        g_loop<kGE2>(ra, rm, ne2, lanebit, J0, J1, J2, H0, H1, H2);
+                        g_loop<kGG>(ra, rm, ng, lanebit, J0, J1, J2, H0, H1, H2);
                         add3(J0, J1, J2, H0, H1, H2);
+                        q += ns2 + ns6 + ne0 + ne2 + ng;
+                    }
+                    // L rows (single-parity lambda / mu rows; the host sends them here only
+                    // when the term has < 16 lambda-capable rows, so S fits its 4 register
+                    // planes): J += k p, S += Lambda, Lambda = p ^ inv -- both from the x
+                    // parity word
+                    if (nl) {
+#pragma unroll 2
+                        for (const uint32_t e = q + nl; q < e; ++q) {
+                            const uint4 a = pg[2 * q], b = pg[2 * q + 1];
+                            const bool px = Mw[q].x & lanebit;
+                            const uint32_t lam = px ? a.y : a.x, p = px ? a.w : a.z;
+                            g_row(J0, J1, J2, b.w, p, b.x, b.y);
+                            const uint32_t c0 = K.S[0] & lam;
+                            K.S[0] ^= lam;
+                            const uint32_t c1 = K.S[1] & c0;
+                            K.S[1] ^= c0;
+                            const uint32_t c2 = K.S[2] & c1;
+                            K.S[2] ^= c1;
+                            K.S[3] ^= c2;
+                        }
+                        K.nS = nl;
                     }
                     // D rows: the class bodies of the bit-sliced kernels (generated PTX)
                     for (const uint32_t e = q + nd; q < e; ++q) {

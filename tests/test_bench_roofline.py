@@ -30,6 +30,8 @@ def test_row_minimum_per_class_is_pinned():
     c = RL.min_counts(ops, kinds, 1024)
     assert c["warp_instructions"] == 10 * 10 + 5 * 6 + 32 * (3 + 2 * 4 + 3 * 6)
     assert c["warp_popc"] == 10 * 2 + 5 * 1
+    # ALU pipe: per parity AND + LOP3->P + SEL, plus the body
+    assert c["warp_alu"] == 10 * (2 * 3 + 1) + 5 * (3 + 1)
     # the sorted kernel forms each parity from G table words: 2G + 3 per parity
     c4 = RL.min_counts(ops, kinds, 1024, "sorted", 4)
     assert c4["warp_instructions"] == 10 * (1 + 2 * 11 + 1) + 5 * (1 + 11 + 1) + 32 * 29
@@ -50,7 +52,8 @@ def test_frac_is_bounded_and_shard_invariant():
     h = P.HostTable(synth.generate_config(cfg))
     ops, kinds = h.slice_stats()
     c = RL.min_counts(ops, kinds, 1 << 20)
-    t_min = max(c["warp_instructions"] / (148 * 4 * 1965e6), c["warp_popc"] * 32 / (148 * 16 * 1965e6))
+    t_min = max(c["warp_instructions"] / (148 * 4 * 1965e6), c["warp_alu"] / (148 * 2 * 1965e6),
+                c["warp_popc"] * 32 / (148 * 16 * 1965e6))
     # a launch can never beat the minimum: at t = t_min the fraction is exactly 1
     r = RL.roofline(ops, kinds, 1 << 20, t_min, 1965.0)
     assert abs(r["frac"] - 1.0) < 1e-9
@@ -59,3 +62,29 @@ def test_frac_is_bounded_and_shard_invariant():
     # an 8-way assignment shard: each rank does 1/8 of the work in 1/8 of the time
     shard = RL.roofline(ops, kinds, (1 << 20) // 8, 3 * t_min / 8, 1965.0)
     assert abs(shard["frac"] - slow["frac"]) < 1e-9
+
+
+def test_page_minimum_by_family_and_class():
+    # C, G (all in the class split), D, dropped, L | S2, S6, E0, E2, GG
+    fam = [10, 40, 2, 5, 4, 8, 2, 10, 10, 10]
+    d_ops = np.zeros(129)
+    d_ops[0] = 2  # class (0,0) two-parity: body 1
+    c = RL.min_counts_page(fam, d_ops, np.array([1, 0, 0]), 1024)
+    rows = 10 + 40 + 2 + 4
+    pre = rows * 12 / 32
+    assert abs(c["warp_instructions"] - (pre + 5 * 10 + 6 * 10 + 7 * 10 + 9 * 10 + 14 * 10 + 20 * 4
+                                         + 2 * 8 + 32 * 3)) < 1e-9
+    assert abs(c["warp_alu"] - (rows * 6 / 32 + 3 * 10 + 4 * 10 + 5 * 10 + 7 * 10 + 11 * 10 + 17 * 4
+                                + 2 * 5)) < 1e-9
+    # a layout without the class split counts every G row as GG
+    old = RL.min_counts_page(fam[:5], d_ops, np.array([1, 0, 0]), 1024)
+    assert old["warp_alu"] > c["warp_alu"]
+
+
+def test_headline_table_is_alu_bound_and_classes_cover_g():
+    h = P.HostTable(synth.generate_config(synth.CONFIGS["c2"]))
+    fam, d_ops = h.page_stats()
+    assert int(fam[5:].sum()) == int(fam[1])
+    ops, kinds = h.slice_stats()
+    r = RL.roofline(ops, kinds, 1 << 20, 0.2, 1965.0, "page", page_stats=(fam, d_ops))
+    assert r["bound"] == "alu pipe" and 0 < r["frac"] < 1

@@ -1,7 +1,8 @@
 """CPU emulation of the page kernel's row families (pzx_table_page_layout):
 every record of the page layout is interpreted exactly as k_eval_page does
 (X = parity ? ~W : W via the record words, then C: Z |= X; G: J += (k + 4p)q~;
-D: the class op's w'(p, q) / zero / lambda / pi / pi' tables) and the per-term
+L: J += k p, S += p ^ inv; D: the class op's w'(p, q) / zero / lambda / pi /
+pi' tables) and the per-term
 exponent codes, with the term's folded j offset, must reconstruct the
 reference's instantiate_diagram value (diagram.cpp:149-165) bit for bit.
 No GPU: this pins the host classification the GPU tests then exercise."""
@@ -33,18 +34,47 @@ def emulate_term(slots, hdr, a):
         OPS = P.slice_op_table()
     cnt = int(slots[hdr, 4])
     nc, ng, nd = cnt & 0xFF, (cnt >> 8) & 0xFF, (cnt >> 16) & 0xFF
+    nl = int(slots[hdr, 5])
+    ng += sum((int(slots[hdr, 6]) >> (8 * i)) & 0xFF for i in range(4))  # S2, S6, E0, E2 + GG
     j = z = s1 = pa = pb = 0
     q = hdr + 1
     for _ in range(nc):
         w = slots[q]
         z |= vec(w[0], w[1], w[6], a)
         q += 1
-    for _ in range(ng):
+    cls = [0] * 4 + [ng]
+    for i in range(4):
+        cls[i] = (int(slots[hdr, 6]) >> (8 * i)) & 0xFF
+        cls[4] -= cls[i]
+    for c, n_c in enumerate(cls):          # S2, S6, E0, E2, GG: the kernel's per-class updates
+        for _ in range(n_c):
+            w = slots[q]
+            X = vec(w[0], w[1], w[6], a)
+            Y = vec(w[2], w[3], w[7], a)
+            k = (1 if w[4] else 0) + (2 if w[5] else 0)
+            if c == 0:
+                assert w[6] == 0 and k == 2 and w[0] == 0
+                j += 2 * Y
+            elif c == 1:
+                assert w[6] == 0 and k == 2 and w[0] == 0xFFFFFFFF
+                j += 6 * Y
+            elif c == 2:
+                assert k == 0
+                j += 4 * (X & Y)
+            elif c == 3:
+                assert k == 2
+                j += 2 * Y + 4 * (X & Y)
+            else:
+                assert k in (1, 3)
+                j += (k * Y + 4 * (X & Y))  # X = p ^ K2: v2 = Y & X carries k's bit 2
+            q += 1
+    for _ in range(nl):
         w = slots[q]
-        X = vec(w[0], w[1], w[6], a)
-        Y = vec(w[2], w[3], w[7], a)
-        k = (1 if w[4] else 0) + (2 if w[5] else 0)
-        j += (k * Y + 4 * (X & Y))          # X = p ^ K2: v2 = Y & X carries k's bit 2
+        lam = vec(w[0], w[1], w[6], a)      # Lambda = p ^ inv, from the x parity word
+        p_ = vec(w[2], w[3], w[6], a)
+        k = (1 if w[4] else 0) + (2 if w[5] else 0) + (4 if w[7] else 0)
+        j += k * p_
+        s1 += lam
         q += 1
     for _ in range(nd):
         w = slots[q]
@@ -78,11 +108,12 @@ def test_page_layout_reconstructs_reference_terms(case):
     lay = h.page_layout()
     assert lay is not None
     slots, tslot, jfold, fam = lay
-    assert slots.shape[0] % PAGE == 0 and int(fam[:3].sum()) <= h.n_rows
+    assert slots.shape[0] % PAGE == 0 and int(fam[:5].sum()) == h.n_rows and fam[5:].sum() == fam[1]
     # no term straddles a page; the last term of every used page is flagged
     for t in range(h.n_terms):
         cnt = int(slots[tslot[t], 4])
-        n = 1 + (cnt & 0xFF) + ((cnt >> 8) & 0xFF) + ((cnt >> 16) & 0xFF)
+        n = 1 + (cnt & 0xFF) + ((cnt >> 8) & 0xFF) + ((cnt >> 16) & 0xFF) + int(slots[tslot[t], 5])
+        n += sum((int(slots[tslot[t], 6]) >> (8 * i)) & 0xFF for i in range(4))
         assert tslot[t] // PAGE == (tslot[t] + n - 1) // PAGE
         nxt = tslot[t + 1] if t + 1 < h.n_terms else None
         if nxt is not None and nxt // PAGE != tslot[t] // PAGE:
@@ -103,6 +134,6 @@ def test_page_families_on_the_headline_table():
     """C2's rows: the generic (branch-free) family carries the bulk."""
     h = P.HostTable(synth.generate_config(synth.CONFIGS["c2"]))
     _, _, _, fam = h.page_layout()
-    c, g, d, dropped = (int(x) for x in fam)
-    assert c + g + d + dropped == h.n_rows
+    c, g, d, dropped, l_ = (int(x) for x in fam[:5])
+    assert c + g + d + dropped + l_ == h.n_rows
     assert g > 0.7 * h.n_rows and c > 0 and d > 0
