@@ -781,7 +781,8 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
     L.p3_off = align16(L.u_off + 8 * (M + 1));
     L.pd_off = align16(L.p3_off + 8 * (M / 2 + 1));
     L.sab_off = align16(L.pd_off + 16 * (2 * M + 1));
-    L.bytes = align16(L.sab_off + 16 * 256);
+    L.uz_off = align16(L.sab_off + 16 * 256);
+    L.bytes = align16(L.uz_off + 8 * 32);
     std::vector<unsigned char> blob(L.bytes, 0);
     uint32_t* codes = reinterpret_cast<uint32_t*>(blob.data() + L.codes_off);
     for (int c = 0; c < 64; ++c)
@@ -826,6 +827,10 @@ std::vector<unsigned char> build_lut(uint32_t max_rows, LutLayout& L) {
                 sab[2 * i] = double(v.re);
                 sab[2 * i + 1] = double(v.im);
             }
+    // (sqrt2-1)^s for s < 16 at s, zeros at 16..31 (Z-marked assignments: index s | 16)
+    double* uz = reinterpret_cast<double*>(blob.data() + L.uz_off);
+    x = 1;
+    for (int is = 0; is < 16; ++is) { uz[is] = double(x); x *= (f128_sqrt2() - 1); }
     return blob;
 }
 

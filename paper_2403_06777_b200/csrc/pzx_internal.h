@@ -41,6 +41,7 @@ struct LutLayout {
     uint32_t pd_off;     // double2 pi^d (d > 0) / pi'^-d (d < 0), d = -max_rows..max_rows
     uint32_t sab_off;    // double2 (sqrt2-1)^s pi^a pi'^b, s < 16, a, b < 4, index s | a << 4 | b << 6
                          // (bit-sliced kernels' epilogue fast path)
+    uint32_t uz_off;     // double uz[s | z << 4] = (sqrt2 - 1)^s (z = 0), 0 (z = 1); s < 16 (page kernel)
     uint32_t bytes;
     int32_t max_rows;
 };

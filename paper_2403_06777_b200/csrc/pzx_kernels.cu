@@ -101,6 +101,10 @@ constexpr int kTileRows = 256;
 #ifndef PZX_EPI_TRANSPOSE
 #define PZX_EPI_TRANSPOSE 1
 #endif
+// page kernel: pi terms through the per-warp T[j, a, b] table (page_epilogue_pi)
+#ifndef PZX_PI_TAB
+#define PZX_PI_TAB 1
+#endif
 
 // ------------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -153,6 +157,7 @@ struct SmemLut {
     const double* p3;
     const double2* pd;  // centred: pd[d], d in [-max_rows, max_rows]
     const double2* sab;  // (sqrt2-1)^s pi^a pi'^b, s < 16, a, b < 4, index s | a << 4 | b << 6
+    const double* uz;    // (sqrt2-1)^s at s < 16, 0 at s | 16 (page kernel, pi terms)
 };
 
 __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* dst_bytes) {
@@ -168,6 +173,7 @@ __device__ __forceinline__ SmemLut stage_lut(const DevTable& t, unsigned char* d
     L.p3 = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.p3_off);
     L.pd = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.pd_off) + t.lut_layout.max_rows;
     L.sab = reinterpret_cast<const double2*>(dst_bytes + t.lut_layout.sab_off);
+    L.uz = reinterpret_cast<const double*>(dst_bytes + t.lut_layout.uz_off);
     return L;
 }
 
@@ -1499,6 +1505,53 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
 // rest of the term (constraint-first order, PAPER "Conclusions").
 __host__ __device__ constexpr uint32_t page_lut_offset() { return 2 * kPageSlots * 32 + 16; }
 
+// Page-kernel epilogue of a term with pi / pi' rows (fast counters): the warp
+// has built T[pi_tab_index(j, a, b)] = C w^j pi^a pi'^b for the term, so each
+// assignment reads ONE complex entry and one real (sqrt2-1)^s (uz, zero for
+// Z-marked assignments) -- 2 DFMA -- instead of C w^j and (sqrt2-1)^s pi^a pi'^b
+// (two complex lookups, 4 DFMA; slice_epilogue_tr KIND 2). Index bytes from
+// two byte-lane transposes: {J0^A0, J1^A1, J2^B0, A0, A1, B0, B1} (dead
+// assignments OR-ed to one entry) and {S0..S3, Z} at bits 3..7 (= the uz byte
+// offset, no LEA).
+template <int NT, bool LC>
+__device__ __forceinline__ void page_epilogue_pi(const SmemLut& L, uint32_t tab_s, SliceAcc<NT, true>& acc,
+                                                 uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
+                                                 const KindCounters<NT, LC>& K) {
+    const uint32_t A0 = K.A[0] | Z, A1 = K.A[1] | Z, B0 = K.B[0] | Z, B1 = K.B[1] | Z;
+    uint32_t R[8] = {(J0 | Z) ^ A0, (J1 | Z) ^ A1, (J2 | Z) ^ B0, A0, A1, B0, B1, 0u};
+    transpose8_bytes(R);
+    // dead assignments: s = 15 | 16 -> uz[31] = 0, off the banks of the common small s
+    uint32_t Q[8] = {0u, 0u, 0u, K.S[0] | Z, K.S[1] | Z, K.S[2] | Z, K.S[3] | Z, Z};
+    transpose8_bytes(Q);
+    const uint32_t uz_s = smem_u32(L.uz);
+    tmem_wait_st();
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t sel = 0x4440u | uint32_t(m);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t v[16];
+            tmem_ld16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+            double2 c[4];
+            double f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                c[r] = lds_d2(tab_s + (__byte_perm(R[4 * h + r], 0u, sel) << 4));
+                f[r] = lds_d(uz_s + __byte_perm(Q[4 * h + r], 0u, sel));
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double2 o = v2d(v + 4 * r);
+                o.x = fma(c[r].x, f[r], o.x);
+                o.y = fma(c[r].y, f[r], o.y);
+                d2v(o, v + 4 * r);
+            }
+            tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+        }
+    }
+}
+
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
@@ -1615,10 +1668,17 @@ __device__ __forceinline__ void g_loop(uint32_t& ra, uint32_t& rm, uint32_t n, u
     }
 }
 
+// per-warp pi-term table T[j, a, b] = C w^j pi^a pi'^b (page_epilogue_pi)
+constexpr int kPiTab = 128;
+__host__ __device__ constexpr uint32_t pi_tab_index(uint32_t j, uint32_t a, uint32_t b) {
+    return (j ^ (a | ((b & 1u) << 2))) | (a << 3) | (b << 5);
+}
+
 size_t page_smem_bytes(const DevTable& t) {
     const uint32_t amp_off = (page_lut_offset() + t.lut_layout.bytes + 127u) & ~127u;
     const size_t b = amp_off + 4 * kCrot * 16 + 4 * size_t(kPageSlots) * 8 + size_t(kHiPlanes) * kSliceThreads * 4;
-    return b > kTmemCtaSmem ? b : kTmemCtaSmem;
+    constexpr size_t floor = kTmemCtaSmem - 4 * size_t(kPiTab) * 16;  // + the static pi tables: <= 4 CTAs / SM
+    return b > floor ? b : floor;
 }
 
 template <bool DBG = false>
@@ -1640,6 +1700,13 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
     double2* crot = reinterpret_cast<double2*>(smem + amp_off) + warp * kCrot;
     uint2* Mw = reinterpret_cast<uint2*>(smem + amp_off + 4 * kCrot * 16) + warp * kPageSlots;
     uint32_t* hi_planes = reinterpret_cast<uint32_t*>(smem + amp_off + 4 * kCrot * 16 + 4 * kPageSlots * 8);
+    // the warp's pi-term table in STATIC shared memory: its address is a link-time
+    // constant + warp * 2 KB, independent of the dynamic layout (a table addressed
+    // from the dynamic base shares subexpressions with the row loops' addresses and
+    // costs them their uniform-datapath addressing)
+    __shared__ __align__(16) double2 pitab_all[4 * kPiTab];
+    double2* pitab = pitab_all + warp * kPiTab;
+    for (uint32_t i = lane; i < uint32_t(kPiTab); i += 32) pitab[i] = make_double2(0.0, 0.0);  // finite for dead lanes
     SliceAcc<NT, true> acc{nullptr, 0u};
     acc.taddr = tmem_alloc_cta(&tmem_base_s);
     acc.zero();
@@ -1757,19 +1824,43 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                 }
                 if constexpr (DBG) debug_dump_codes<NT, false>(r, term, off, J0, J1, J2, Z, K);
                 if (!dead) {
-                    __syncwarp();  // the previous term's epilogue is done with crot
-                    if (lane < uint32_t(kCrot)) {
-                        double2 v = make_double2(0.0, 0.0);
-                        if (lane < 8) {
-                            const double2 C = make_double2(__hiloint2double(int(h0.y), int(h0.x)),
-                                                           __hiloint2double(int(h0.w), int(h0.z)));
-                            const double2 w = L.om[lane];
-                            v = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+                    __syncwarp();  // the previous term's epilogue is done with crot / pitab
+                    const double2 C = make_double2(__hiloint2double(int(h0.y), int(h0.x)),
+                                                   __hiloint2double(int(h0.w), int(h0.z)));
+                    if (PZX_PI_TAB && K.has_pi() && K.fits_fast()) {
+                        // T[j, a, b] = C w^j pi^a pi'^b for b <= nB: lane -> (j, a), one b per pass
+                        // (every lane writes: the entries with a > nA are finite and never read
+                        // by a live assignment)
+                        const uint32_t j = lane & 7u, a = lane >> 3;
+                        const double2 w = L.om[j];
+                        const double2 cw = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+                        for (uint32_t b = 0; b <= K.nB; ++b) {
+                            const double2 p = L.sab[(a | ((b & 1u) << 2)) | (a << 4) | (b << 6)];  // s = 0
+                            pitab[pi_tab_index(j, a, b)] =
+                                make_double2(cw.x * p.x - cw.y * p.y, cw.x * p.y + cw.y * p.x);
                         }
-                        crot[lane] = v;
+                        __syncwarp();
+                        if (K.nS) {  // (lambda/mu)^s1 = mu^.. w^(6 s1) (sqrt2-1)^s1: J += 6 s1
+                            const uint32_t w1 = K.S[0], w2 = K.S[0] ^ K.S[1];
+                            const uint32_t c1 = J1 & w1;
+                            J1 ^= w1;
+                            J2 ^= w2 ^ c1;
+                        }
+                        page_epilogue_pi<NT, false>(L, smem_u32(pitab), acc, J0, J1, J2, Z, K);
+                        J0 = J1 = J2 = Z = 0;
+                        K.reset();
+                    } else {
+                        if (lane < uint32_t(kCrot)) {
+                            double2 v = make_double2(0.0, 0.0);
+                            if (lane < 8) {
+                                const double2 w = L.om[lane];
+                                v = make_double2(C.x * w.x - C.y * w.y, C.x * w.y + C.y * w.x);
+                            }
+                            crot[lane] = v;
+                        }
+                        __syncwarp();
+                        slice_epilogue_apply<NT, true, true>(L, crot, acc, J0, J1, J2, Z, K);
                     }
-                    __syncwarp();
-                    slice_epilogue_apply<NT, true, true>(L, crot, acc, J0, J1, J2, Z, K);
                 } else {
                     J0 = J1 = J2 = Z = 0;
                     if (K.any()) K.reset();
