@@ -1668,6 +1668,50 @@ __device__ __forceinline__ void g_loop(uint32_t& ra, uint32_t& rm, uint32_t n, u
     }
 }
 
+// Page-kernel epilogue of a term with lambda / mu rows only (fast counters):
+// acc += crot[j] * uz[s | 16 z]. Two byte-lane transposes of mostly-zero
+// planes put j at bits 4..6 (the crot byte offset) and s | 16 z at bits 3..7
+// (the uz byte offset): no LEA, and dead assignments read crot[j] -- entries
+// 0..7 fill the 32 banks exactly, so no bank conflict -- times uz[31] = 0
+// (slice_epilogue_tr KIND 1 sends them to one zero entry that conflicts with
+// the live j = 7 reads).
+template <int NT, bool LC>
+__device__ __forceinline__ void page_epilogue_lam(const SmemLut& L, uint32_t crot_s, SliceAcc<NT, true>& acc,
+                                                  uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
+                                                  const KindCounters<NT, LC>& K) {
+    uint32_t R[8] = {0u, 0u, 0u, 0u, J0, J1, J2, 0u};
+    transpose8_bytes(R);
+    uint32_t Q[8] = {0u, 0u, 0u, K.S[0] | Z, K.S[1] | Z, K.S[2] | Z, K.S[3] | Z, Z};
+    transpose8_bytes(Q);
+    const uint32_t uz_s = smem_u32(L.uz);
+    tmem_wait_st();
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t sel = 0x4440u | uint32_t(m);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t v[16];
+            tmem_ld16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+            double2 c[4];
+            double f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                c[r] = lds_d2(crot_s + __byte_perm(R[4 * h + r], 0u, sel));
+                f[r] = lds_d(uz_s + __byte_perm(Q[4 * h + r], 0u, sel));
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double2 o = v2d(v + 4 * r);
+                o.x = fma(c[r].x, f[r], o.x);
+                o.y = fma(c[r].y, f[r], o.y);
+                d2v(o, v + 4 * r);
+            }
+            tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+        }
+    }
+}
+
 // per-warp pi-term table T[j, a, b] = C w^j pi^a pi'^b (page_epilogue_pi)
 constexpr int kPiTab = 128;
 __host__ __device__ constexpr uint32_t pi_tab_index(uint32_t j, uint32_t a, uint32_t b) {
@@ -1859,7 +1903,17 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                             crot[lane] = v;
                         }
                         __syncwarp();
-                        slice_epilogue_apply<NT, true, true>(L, crot, acc, J0, J1, J2, Z, K);
+                        if (PZX_PI_TAB && K.any() && K.fits_fast()) {  // lambda / mu rows only
+                            const uint32_t w1 = K.S[0], w2 = K.S[0] ^ K.S[1];  // J += 6 s1
+                            const uint32_t c1 = J1 & w1;
+                            J1 ^= w1;
+                            J2 ^= w2 ^ c1;
+                            page_epilogue_lam<NT, false>(L, smem_u32(crot), acc, J0, J1, J2, Z, K);
+                            J0 = J1 = J2 = Z = 0;
+                            K.reset();
+                        } else {
+                            slice_epilogue_apply<NT, true, true>(L, crot, acc, J0, J1, J2, Z, K);
+                        }
                     }
                 } else {
                     J0 = J1 = J2 = Z = 0;
