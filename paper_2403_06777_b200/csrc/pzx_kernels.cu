@@ -1511,14 +1511,15 @@ __host__ __device__ constexpr uint32_t page_lut_offset() { return 2 * kPageSlots
 // Z-marked assignments) -- 2 DFMA -- instead of C w^j and (sqrt2-1)^s pi^a pi'^b
 // (two complex lookups, 4 DFMA; slice_epilogue_tr KIND 2). Index bytes from
 // two byte-lane transposes: {J0^A0, J1^A1, J2^B0, A0, A1, B0, B1} (dead
-// assignments OR-ed to one entry) and {S0..S3, Z} at bits 3..7 (= the uz byte
-// offset, no LEA).
+// assignments masked to entry 0, which the live (j, a, b) = 0 lanes of its bank
+// group share) and {S0..S3, Z} at bits 3..7 (= the uz byte offset, no LEA).
 template <int NT, bool LC>
 __device__ __forceinline__ void page_epilogue_pi(const SmemLut& L, uint32_t tab_s, SliceAcc<NT, true>& acc,
                                                  uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
                                                  const KindCounters<NT, LC>& K) {
-    const uint32_t A0 = K.A[0] | Z, A1 = K.A[1] | Z, B0 = K.B[0] | Z, B1 = K.B[1] | Z;
-    uint32_t R[8] = {(J0 | Z) ^ A0, (J1 | Z) ^ A1, (J2 | Z) ^ B0, A0, A1, B0, B1, 0u};
+    // dead assignments read T[0, 0, 0] (the entry most live lanes of its bank group read)
+    const uint32_t A0 = K.A[0] & ~Z, A1 = K.A[1] & ~Z, B0 = K.B[0] & ~Z, B1 = K.B[1] & ~Z;
+    uint32_t R[8] = {(J0 & ~Z) ^ A0, (J1 & ~Z) ^ A1, (J2 & ~Z) ^ B0, A0, A1, B0, B1, 0u};
     transpose8_bytes(R);
     // dead assignments: s = 15 | 16 -> uz[31] = 0, off the banks of the common small s
     uint32_t Q[8] = {0u, 0u, 0u, K.S[0] | Z, K.S[1] | Z, K.S[2] | Z, K.S[3] | Z, Z};
