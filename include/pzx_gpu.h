@@ -167,11 +167,11 @@ pzx_status pzx_table_shape(const pzx_table* t, uint32_t* n_params, uint64_t* n_t
  * pi or pi' row. Either pointer may be NULL. */
 pzx_status pzx_table_slice_stats(const pzx_table* t, uint64_t op_rows[129], uint64_t term_kinds[3]);
 /* Rows per page family: {constraint, generic, dispatch, dropped, lambda} and
- * the generic rows by update class {S2, S6, E0, E2, GG} (pzx_host.cpp,
+ * the generic rows by update class {S2, S6, E0, E2, G1, G3} (pzx_host.cpp,
  * page_term) -- PZX_PAGE_FAMILIES counts -- and the dispatch rows per op
  * (bench.py's roofline of the page kernel); any table with a page layout,
  * PZX_E_CAPACITY otherwise. */
-#define PZX_PAGE_FAMILIES 10
+#define PZX_PAGE_FAMILIES 11
 pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[PZX_PAGE_FAMILIES], uint64_t d_op_rows[129]);
 /* Host-only tables (pzx_table_compile_host): the page layout of the
  * enumerated page kernel -- *n_slots 32-byte records (8 x u32 each; slots may

@@ -191,7 +191,7 @@ struct HostTable {
     uint32_t page_fill = 0;                 // slots used in the open page
     int64_t last_hdr = -1;                  // slot of the last header written
     uint64_t page_rows[5] = {};             // rows by family: constraint, G, dispatch, dropped, L
-    uint64_t page_gsub[5] = {};             // G rows by update class: S2, S6, E0, E2, GG
+    uint64_t page_gsub[kPageGClasses] = {};  // G rows by update class: S2, S6, E0, E2, G1, G3
     uint64_t page_d_ops[kSliceOps] = {};    // dispatch-family rows per op (the roofline's D bodies)
     bool simplify = false;                  // PZX_COMPILE_SIMPLIFY: fold assignment-independent row groups
     uint64_t n_dev_rows() const { return unit.size(); }
@@ -313,9 +313,9 @@ void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
 // and rows whose reachable variants are equal are dropped (their w^j goes
 // into the term constant like every c0; their sqrt2^e and mu are already in
 // E_t / nLM_t). Records (8 x u32), in the order header, C, G, L, D:
-//   header: {C_page (double2), nc | n_gg << 8 | nd << 16 | last_in_page << 24, nl,
-//            n_s2 | n_s6 << 8 | n_e0 << 16 | n_e2 << 24, 0}
-// with the G rows in the order S2, S6, E0, E2, GG (page_term: by update cost)
+//   header: {C_page (double2), nc | n_g1 << 8 | nd << 16 | last_in_page << 24, nl,
+//            n_s2 | n_s6 << 8 | n_e0 << 16 | n_e2 << 24, n_g3}
+// with the G rows in the order S2, S6, E0, E2, G1, G3 (page_term: by update cost)
 //   C: {W ^ zc, ~(W ^ zc), 0, 0, 0, 0, psi, 0}
 //   G: {A = W(x) ^ K2, ~A, B = W(y) ^ INV, ~B, K0, K1, x-mask, y-mask}
 //   L: {W ^ INV, ~(W ^ INV), W, ~W, K0, K1, psi, K2}
@@ -444,12 +444,14 @@ int page_term(HostTable& h, const C128& cpp) {
     //   0 S2: single, J += 2q        1 S6: single, J += 6q        (J2 ^= q & J1 (~J1); J1 ^= q)
     //   2 E0: k = 0 (and single J += 4q)  J2 ^= X & Y
     //   3 E2: k = 2                       J2 ^= Y & (J1 ^ X); J1 ^= Y
-    //   4 GG: odd k                       g_row
-    std::vector<PageRec> gsub[5];
-    for (const PageRec& r : fam[1]) {
+    //   4 G1: k = 1                       J += Y + 4XY (5 LOP3)
+    //   5 G3: k = 3, stored with X' = ~X  J -= Y, J += 4X'Y: the G1 update on ~J
+    std::vector<PageRec> gsub[kPageGClasses];
+    for (PageRec r : fam[1]) {
         const int k = (r.w[4] ? 1 : 0) | (r.w[5] ? 2 : 0);
         const bool single = r.w[6] == 0;
-        const int sc = (single && k == 2) ? (r.w[0] ? 1 : 0) : k == 0 ? 2 : k == 2 ? 3 : 4;
+        const int sc = (single && k == 2) ? (r.w[0] ? 1 : 0) : k == 0 ? 2 : k == 2 ? 3 : k == 1 ? 4 : 5;
+        if (sc == 5) std::swap(r.w[0], r.w[1]);  // X' = ~X
         gsub[sc].push_back(r);
         h.page_gsub[sc] += 1;
     }
@@ -475,7 +477,7 @@ int page_term(HostTable& h, const C128& cpp) {
                                  uint32_t(fam[2].size()),
                                  uint32_t(gsub[0].size()) | uint32_t(gsub[1].size()) << 8 |
                                      uint32_t(gsub[2].size()) << 16 | uint32_t(gsub[3].size()) << 24,
-                                 0));
+                                 uint32_t(gsub[5].size())));
     auto put = [&](const std::vector<PageRec>& v) {
         for (const PageRec& r : v) {
             h.prows.push_back(make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]));
@@ -483,7 +485,7 @@ int page_term(HostTable& h, const C128& cpp) {
         }
     };
     put(fam[0]);
-    for (int sc = 0; sc < 5; ++sc) put(gsub[sc]);
+    for (int sc = 0; sc < kPageGClasses; ++sc) put(gsub[sc]);
     put(fam[2]);
     put(fam[3]);
     h.page_fill += n;
@@ -692,7 +694,7 @@ void merge_into(HostTable& h, HostTable& part) {
         app(h.jp_t, part.jp_t);
         if (part.last_hdr >= 0) h.last_hdr = int64_t(base_slot) + part.last_hdr;
         for (int i = 0; i < 5; ++i) h.page_rows[i] += part.page_rows[i];
-        for (int i = 0; i < 5; ++i) h.page_gsub[i] += part.page_gsub[i];
+        for (int i = 0; i < kPageGClasses; ++i) h.page_gsub[i] += part.page_gsub[i];
         for (int i = 0; i < kSliceOps; ++i) h.page_d_ops[i] += part.page_d_ops[i];
     } else if (h.want_prows) {
         h.want_prows = false;
@@ -1757,7 +1759,7 @@ pzx_status pzx_table_page_layout(const pzx_table* t, uint32_t* slots, uint64_t* 
     if (!h.want_prows || h.term_slot.size() != h.coef.size()) { *n_slots = 0; return PZX_E_CAPACITY; }
     if (family_rows) {
         for (int i = 0; i < 5; ++i) family_rows[i] = h.page_rows[i];
-        for (int i = 0; i < 5; ++i) family_rows[5 + i] = h.page_gsub[i];
+        for (int i = 0; i < kPageGClasses; ++i) family_rows[5 + i] = h.page_gsub[i];
     }
     if (h.prows.empty() && t->device >= 0) { *n_slots = 0; return PZX_E_INVALID; }  // uploaded: host copy released
     *n_slots = h.prows.size() / 2;
@@ -1773,7 +1775,7 @@ pzx_status pzx_table_page_stats(const pzx_table* t, uint64_t family_rows[PZX_PAG
     if (!h.want_prows || h.term_slot.size() != h.coef.size()) return PZX_E_CAPACITY;
     if (family_rows) {
         for (int i = 0; i < 5; ++i) family_rows[i] = h.page_rows[i];
-        for (int i = 0; i < 5; ++i) family_rows[5 + i] = h.page_gsub[i];
+        for (int i = 0; i < kPageGClasses; ++i) family_rows[5 + i] = h.page_gsub[i];
     }
     if (d_op_rows)
         for (int i = 0; i < kSliceOps; ++i) d_op_rows[i] = h.page_d_ops[i];

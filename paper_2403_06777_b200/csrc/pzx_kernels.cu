@@ -1594,8 +1594,10 @@ __device__ __forceinline__ void add3(uint32_t& J0, uint32_t& J1, uint32_t& J2, u
 //   kGS : Y only;  J2 ^= Y & J1, J1 ^= Y                   (J += 2Y)
 //   kGE0: J2 ^= X & Y                                       (J += 4XY)
 //   kGE2: J2 ^= Y & (J1 ^ X), J1 ^= Y                       (J += 2Y + 4XY)
-//   kGG : g_row                                             (J += (k + 4X) Y)
-constexpr int kGS = 0, kGE0 = 1, kGE2 = 2, kGG = 3;
+//   kG1 : J2 ^= (J1 & J0 & Y) ^ (X & Y), J1 ^= J0 & Y,
+//         J0 ^= Y                                           (J += Y + 4XY, 5 LOP3)
+//   kGG : g_row                                             (J += (k + 4X) Y, 7 LOP3)
+constexpr int kGS = 0, kGE0 = 1, kGE2 = 2, kGG = 3, kG1 = 4;
 
 template <int V>
 struct GRow {
@@ -1631,6 +1633,10 @@ __device__ __forceinline__ void g_apply(const GRow<V>& r, uint32_t lanebit, uint
         } else if constexpr (V == kGE2) {
             J2 ^= Y & (J1 ^ X);
             J1 ^= Y;
+        } else if constexpr (V == kG1) {
+            J2 ^= (J1 & J0 & Y) ^ (X & Y);
+            J1 ^= J0 & Y;
+            J0 ^= Y;
         } else {
             g_row(J0, J1, J2, X, Y, r.b.x, r.b.y);
         }
@@ -1805,10 +1811,11 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                 }
                 const bool dead = nc != 0 && __all_sync(0xFFFFFFFFu, Z == 0xFFFFFFFFu);
                 if (dead) {
-                    q += ng + nl + nd + (h1.z & 0xFFu) + ((h1.z >> 8) & 0xFFu) + ((h1.z >> 16) & 0xFFu) + (h1.z >> 24);
+                    q += ng + nl + nd + (h1.z & 0xFFu) + ((h1.z >> 8) & 0xFFu) + ((h1.z >> 16) & 0xFFu) + (h1.z >> 24) +
+                         h1.w;
                 } else {
                     // G rows, by update class (page_term): S2 / S6 (single parity, J += 2q / 6q),
-                    // E0 (J2 ^= X & Y), E2 (J += 2Y + 4XY), GG (any k: g_row, 7 LOP3). Pairs of
+                    // E0 (J2 ^= X & Y), E2 (J += 2Y + 4XY), G1 / G3 (J += Y / 3Y + 4XY). Pairs of
                     // rows go to two counters (J, H) so consecutive rows do not wait on each
                     // other's carries; H is added into J once, after the G rows.
                     {
@@ -1824,9 +1831,14 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                         }
                         g_loop<kGE0>(ra, rm, ne0, lanebit, J0, J1, J2, H0, H1, H2);
                         g_loop<kGE2>(ra, rm, ne2, lanebit, J0, J1, J2, H0, H1, H2);
-                        g_loop<kGG>(ra, rm, ng, lanebit, J0, J1, J2, H0, H1, H2);
+                        g_loop<kG1>(ra, rm, ng, lanebit, J0, J1, J2, H0, H1, H2);
+                        if (h1.w) {  // J += 3Y + 4XY = ~(~J + Y + 4X'Y): the G1 update on ~J (X' stored)
+                            J0 = ~J0; J1 = ~J1; J2 = ~J2; H0 = ~H0; H1 = ~H1; H2 = ~H2;
+                            g_loop<kG1>(ra, rm, h1.w, lanebit, J0, J1, J2, H0, H1, H2);
+                            J0 = ~J0; J1 = ~J1; J2 = ~J2; H0 = ~H0; H1 = ~H1; H2 = ~H2;
+                        }
                         add3(J0, J1, J2, H0, H1, H2);
-                        q += ns2 + ns6 + ne0 + ne2 + ng;
+                        q += ns2 + ns6 + ne0 + ne2 + ng + h1.w;
                     }
                     // L rows (single-parity lambda / mu rows; the host sends them here only
                     // when the term has < 16 lambda-capable rows, so S fits its 4 register

@@ -331,10 +331,10 @@ class DeviceTable:
         return ops, kinds
 
     def page_stats(self):
-        """(family_rows [C, G, D, dropped, L, then G by class S2, S6, E0, E2, GG],
+        """(family_rows [C, G, D, dropped, L, then G by class S2, S6, E0, E2, G1, G3],
         dispatch rows per op [129]) of the page layout, or None when the table
         has none (pzx_table_page_stats)."""
-        fam = np.zeros(10, np.uint64)
+        fam = np.zeros(11, np.uint64)
         ops = np.zeros(129, np.uint64)
         st = N.lib().pzx_table_page_stats(self.handle, N.ptr(fam, C.c_uint64), N.ptr(ops, C.c_uint64))
         if st == 6:
@@ -596,11 +596,11 @@ class HostTable:
     page_stats = DeviceTable.page_stats
 
     def page_layout(self):
-        """(slots uint32 [n, 8], term_slot [m], jfold [m], family_rows [10]) of the
+        """(slots uint32 [n, 8], term_slot [m], jfold [m], family_rows [11]) of the
         page kernel's layout (pzx_table_page_layout), or None without one."""
         L = N.lib()
         n = C.c_uint64()
-        fam = np.zeros(10, np.uint64)
+        fam = np.zeros(11, np.uint64)
         st = L.pzx_table_page_layout(self.handle, None, C.byref(n), None, None, N.ptr(fam, C.c_uint64))
         if st == 6:
             return None

@@ -43,7 +43,7 @@ warp), then per row and warp:
       S2/S6 (single parity, J += 2q / 6q): 2 LDS + LOP3->P + SEL + 2 LOP3   6      4
       E0 (J2 ^= X & Y): 2 LDS + 2 x (LOP3->P + SEL) + 1 LOP3                7      5
       E2 (J += 2Y + 4XY): 2 LDS + 2 x (LOP3->P + SEL) + 3 LOP3              9      7
-      GG (any k): 3 LDS + 2 x (LOP3->P + SEL) + 7 LOP3                     14     11
+      G1/G3 (odd k): 2 LDS + 2 x (LOP3->P + SEL) + 5 LOP3                  11      9
     L row: 3 LDS + LOP3->P + 2 SEL + 7 LOP3 (phase) + 7 LOP3 (lambda)     20     17
     D row: 3 LDS + 2 x (LOP3->P + SEL) + the class's LOP3 chain       7 + body  4 + body
 Loop control, row prefetch, TMA waits, counter decode, TMEM traffic and the
@@ -94,16 +94,16 @@ def min_counts_page(family_rows, d_op_rows, term_kinds, n_assign: int) -> dict:
     """Minimum warp-instructions / warp-POPCs of one page-kernel launch."""
     body, _ = _op_table()
     fr = [float(x) for x in family_rows]
-    fr += [0.0] * (10 - len(fr))
-    c, g, d, _dropped, l_ = fr[:5]  # family_rows: C, G, D, dropped, L, G by class S2, S6, E0, E2, GG
+    fr += [0.0] * (11 - len(fr))
+    c, g, d, _dropped, l_ = fr[:5]  # family_rows: C, G, D, dropped, L, G by class S2, S6, E0, E2, G1, G3
     s_, e0, e2 = fr[5] + fr[6], fr[7], fr[8]
-    gg = g - s_ - e0 - e2          # (a layout without the class split: every G row is GG)
+    gg = g - s_ - e0 - e2          # G1 + G3 (a layout without the class split: every G row is odd-k)
     d_ops = np.asarray(d_op_rows, np.float64)
     rows = c + g + d + l_
     pre = rows * (1 + 2 * 5 + 1) / 32.0
-    row_inst = (pre + 5 * c + 6 * s_ + 7 * e0 + 9 * e2 + 14 * gg + 20 * l_ +
+    row_inst = (pre + 5 * c + 6 * s_ + 7 * e0 + 9 * e2 + 11 * gg + 20 * l_ +
                 float(np.sum(d_ops * (3 + 4 + body))))
-    row_alu = (rows * 6 / 32.0 + 3 * c + 4 * s_ + 5 * e0 + 7 * e2 + 11 * gg + 17 * l_ +
+    row_alu = (rows * 6 / 32.0 + 3 * c + 4 * s_ + 5 * e0 + 7 * e2 + 9 * gg + 17 * l_ +
                float(np.sum(d_ops * (4 + body))))
     kinds = np.asarray(term_kinds, np.float64)
     term_inst = float(np.sum(kinds * 32 * np.array(EPI_PER_ASSIGN)))

@@ -65,16 +65,16 @@ def test_frac_is_bounded_and_shard_invariant():
 
 
 def test_page_minimum_by_family_and_class():
-    # C, G (all in the class split), D, dropped, L | S2, S6, E0, E2, GG
-    fam = [10, 40, 2, 5, 4, 8, 2, 10, 10, 10]
+    # C, G (all in the class split), D, dropped, L | S2, S6, E0, E2, G1, G3
+    fam = [10, 40, 2, 5, 4, 8, 2, 10, 10, 6, 4]
     d_ops = np.zeros(129)
     d_ops[0] = 2  # class (0,0) two-parity: body 1
     c = RL.min_counts_page(fam, d_ops, np.array([1, 0, 0]), 1024)
     rows = 10 + 40 + 2 + 4
     pre = rows * 12 / 32
-    assert abs(c["warp_instructions"] - (pre + 5 * 10 + 6 * 10 + 7 * 10 + 9 * 10 + 14 * 10 + 20 * 4
+    assert abs(c["warp_instructions"] - (pre + 5 * 10 + 6 * 10 + 7 * 10 + 9 * 10 + 11 * 10 + 20 * 4
                                          + 2 * 8 + 32 * 3)) < 1e-9
-    assert abs(c["warp_alu"] - (rows * 6 / 32 + 3 * 10 + 4 * 10 + 5 * 10 + 7 * 10 + 11 * 10 + 17 * 4
+    assert abs(c["warp_alu"] - (rows * 6 / 32 + 3 * 10 + 4 * 10 + 5 * 10 + 7 * 10 + 9 * 10 + 17 * 4
                                 + 2 * 5)) < 1e-9
     # a layout without the class split counts every G row as GG
     old = RL.min_counts_page(fam[:5], d_ops, np.array([1, 0, 0]), 1024)

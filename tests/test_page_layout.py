@@ -35,18 +35,19 @@ def emulate_term(slots, hdr, a):
     cnt = int(slots[hdr, 4])
     nc, ng, nd = cnt & 0xFF, (cnt >> 8) & 0xFF, (cnt >> 16) & 0xFF
     nl = int(slots[hdr, 5])
-    ng += sum((int(slots[hdr, 6]) >> (8 * i)) & 0xFF for i in range(4))  # S2, S6, E0, E2 + GG
+    ng += sum((int(slots[hdr, 6]) >> (8 * i)) & 0xFF for i in range(4)) + int(slots[hdr, 7])  # + S2..E2, G3
     j = z = s1 = pa = pb = 0
     q = hdr + 1
     for _ in range(nc):
         w = slots[q]
         z |= vec(w[0], w[1], w[6], a)
         q += 1
-    cls = [0] * 4 + [ng]
+    cls = [0] * 4 + [ng, int(slots[hdr, 7])]
     for i in range(4):
         cls[i] = (int(slots[hdr, 6]) >> (8 * i)) & 0xFF
         cls[4] -= cls[i]
-    for c, n_c in enumerate(cls):          # S2, S6, E0, E2, GG: the kernel's per-class updates
+    cls[4] -= cls[5]
+    for c, n_c in enumerate(cls):          # S2, S6, E0, E2, G1, G3: the kernel's per-class updates
         for _ in range(n_c):
             w = slots[q]
             X = vec(w[0], w[1], w[6], a)
@@ -64,9 +65,12 @@ def emulate_term(slots, hdr, a):
             elif c == 3:
                 assert k == 2
                 j += 2 * Y + 4 * (X & Y)
+            elif c == 4:
+                assert k == 1
+                j += Y + 4 * (X & Y)        # X = p ^ K2: v2 = Y & X carries k's bit 2
             else:
-                assert k in (1, 3)
-                j += (k * Y + 4 * (X & Y))  # X = p ^ K2: v2 = Y & X carries k's bit 2
+                assert k == 3
+                j += -Y + 4 * (X & Y)       # X stored complemented: 3Y + 4(~X)Y = -Y + 4XY (mod 8)
             q += 1
     for _ in range(nl):
         w = slots[q]
@@ -109,11 +113,12 @@ def test_page_layout_reconstructs_reference_terms(case):
     assert lay is not None
     slots, tslot, jfold, fam = lay
     assert slots.shape[0] % PAGE == 0 and int(fam[:5].sum()) == h.n_rows and fam[5:].sum() == fam[1]
+    assert len(fam) == 11
     # no term straddles a page; the last term of every used page is flagged
     for t in range(h.n_terms):
         cnt = int(slots[tslot[t], 4])
         n = 1 + (cnt & 0xFF) + ((cnt >> 8) & 0xFF) + ((cnt >> 16) & 0xFF) + int(slots[tslot[t], 5])
-        n += sum((int(slots[tslot[t], 6]) >> (8 * i)) & 0xFF for i in range(4))
+        n += sum((int(slots[tslot[t], 6]) >> (8 * i)) & 0xFF for i in range(4)) + int(slots[tslot[t], 7])
         assert tslot[t] // PAGE == (tslot[t] + n - 1) // PAGE
         nxt = tslot[t + 1] if t + 1 < h.n_terms else None
         if nxt is not None and nxt // PAGE != tslot[t] // PAGE:
