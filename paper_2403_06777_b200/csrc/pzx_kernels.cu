@@ -105,6 +105,10 @@ constexpr int kTileRows = 256;
 #ifndef PZX_PI_TAB
 #define PZX_PI_TAB 1
 #endif
+// page kernel: the lane-parity pre-pass split over the CTA's four warps
+#ifndef PZX_CTA_PREPASS
+#define PZX_CTA_PREPASS 1
+#endif
 
 // ------------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1791,6 +1795,28 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
         for (uint32_t i = 0; i < np; ++i) {
             mbar_wait(&bars[i & 1], (i >> 1) & 1u);
             const uint4* pg = pages + (i & 1) * kPageSlots * 2;
+#if PZX_CTA_PREPASS
+            // pre-pass, split over the CTA: warp w reads the masks of slots [64 w, 64 w + 64)
+            // ONCE (their 8-byte reads at a 32-byte stride are 4-way bank-conflicted) and
+            // writes the lane-parity words of all four warps
+            {
+                const uint32_t cbase = wbase - warp * 1024u;  // the CTA's first assignment
+                uint2* M0 = Mw - warp * uint32_t(kPageSlots);
+#pragma unroll
+                for (uint32_t k = 0; k < 2; ++k) {
+                    const uint32_t q = warp * 64u + lane + 32u * k;
+                    const uint4 rec = pg[2 * q + 1];
+                    const uint32_t lx = lw_s[(rec.z >> 5) & 31u], ly = lw_s[(rec.w >> 5) & 31u];
+#pragma unroll
+                    for (uint32_t w = 0; w < 4; ++w) {
+                        const uint32_t b = cbase + w * 1024u;
+                        M0[w * kPageSlots + q] = make_uint2(lx ^ (0u - (uint32_t(__popc(rec.z & b)) & 1u)),
+                                                            ly ^ (0u - (uint32_t(__popc(rec.w & b)) & 1u)));
+                    }
+                }
+            }
+            __syncthreads();
+#else
             // pre-pass: this warp's lane-parity words of every slot of the page
 #pragma unroll 4
             for (uint32_t q = lane; q < uint32_t(kPageSlots); q += 32) {
@@ -1800,6 +1826,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                 Mw[q] = make_uint2(mx, my);
             }
             __syncwarp();
+#endif
             while (term < te) {
                 const uint4 h0 = pg[2 * s], h1 = pg[2 * s + 1];
                 const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu, nl = h1.y;
