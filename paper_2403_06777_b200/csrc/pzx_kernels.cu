@@ -915,6 +915,50 @@ __device__ __forceinline__ void transpose8_bytes(uint32_t (&P)[8]) {
     }
 }
 
+// Epilogue of a term with lambda / mu rows only (fast counters; every TMEM kernel):
+// acc += crot[j] * uz[s | 16 z]. Two byte-lane transposes of mostly-zero
+// planes put j at bits 4..6 (the crot byte offset) and s | 16 z at bits 3..7
+// (the uz byte offset): no LEA, and dead assignments read crot[j] -- entries
+// 0..7 fill the 32 banks exactly, so no bank conflict -- times uz[31] = 0
+// (slice_epilogue_tr KIND 1 sends them to one zero entry that conflicts with
+// the live j = 7 reads).
+template <int NT, bool LC>
+__device__ __forceinline__ void page_epilogue_lam(const SmemLut& L, uint32_t crot_s, SliceAcc<NT, true>& acc,
+                                                  uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
+                                                  const KindCounters<NT, LC>& K) {
+    uint32_t R[8] = {0u, 0u, 0u, 0u, J0, J1, J2, 0u};
+    transpose8_bytes(R);
+    uint32_t Q[8] = {0u, 0u, 0u, K.S[0] | Z, K.S[1] | Z, K.S[2] | Z, K.S[3] | Z, Z};
+    transpose8_bytes(Q);
+    const uint32_t uz_s = smem_u32(L.uz);
+    tmem_wait_st();
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t sel = 0x4440u | uint32_t(m);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t v[16];
+            tmem_ld16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+            double2 c[4];
+            double f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                c[r] = lds_d2(crot_s + __byte_perm(R[4 * h + r], 0u, sel));
+                f[r] = lds_d(uz_s + __byte_perm(Q[4 * h + r], 0u, sel));
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double2 o = v2d(v + 4 * r);
+                o.x = fma(c[r].x, f[r], o.x);
+                o.y = fma(c[r].y, f[r], o.y);
+                d2v(o, v + 4 * r);
+            }
+            tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
+        }
+    }
+}
+
 // Term epilogue fast path, TMEM accumulators, transposed decode.
 // The planes are grouped so that each transposed byte IS a table index:
 //   KIND 0 (kind-free term):  {J0 J1 J2 Z}         -> crot[j | z << 3]              acc += C w^j
@@ -934,6 +978,10 @@ __device__ __forceinline__ void slice_epilogue_tr(const SmemLut& L, const double
     uint32_t Q[8] = {J0 | Z, J1 | Z, J2 | Z, Z, 0u, 0u, 0u, 0u};
     if constexpr (KIND == 1) {
         Q[4] = K.S[0]; Q[5] = K.S[1]; Q[6] = K.S[2]; Q[7] = K.S[3];
+    }
+    if constexpr (KIND == 1) {
+        page_epilogue_lam<NT, LC>(L, smem_u32(crot), acc, J0, J1, J2, Z, K);
+        return;
     }
     transpose8_bytes(Q);
     uint32_t R[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -1676,50 +1724,6 @@ __device__ __forceinline__ void g_loop(uint32_t& ra, uint32_t& rm, uint32_t n, u
         g_load(r, ra, rm);
         g_apply(r, lanebit, J0, J1, J2);
         ra += 32; rm += 8;
-    }
-}
-
-// Page-kernel epilogue of a term with lambda / mu rows only (fast counters):
-// acc += crot[j] * uz[s | 16 z]. Two byte-lane transposes of mostly-zero
-// planes put j at bits 4..6 (the crot byte offset) and s | 16 z at bits 3..7
-// (the uz byte offset): no LEA, and dead assignments read crot[j] -- entries
-// 0..7 fill the 32 banks exactly, so no bank conflict -- times uz[31] = 0
-// (slice_epilogue_tr KIND 1 sends them to one zero entry that conflicts with
-// the live j = 7 reads).
-template <int NT, bool LC>
-__device__ __forceinline__ void page_epilogue_lam(const SmemLut& L, uint32_t crot_s, SliceAcc<NT, true>& acc,
-                                                  uint32_t J0, uint32_t J1, uint32_t J2, uint32_t Z,
-                                                  const KindCounters<NT, LC>& K) {
-    uint32_t R[8] = {0u, 0u, 0u, 0u, J0, J1, J2, 0u};
-    transpose8_bytes(R);
-    uint32_t Q[8] = {0u, 0u, 0u, K.S[0] | Z, K.S[1] | Z, K.S[2] | Z, K.S[3] | Z, Z};
-    transpose8_bytes(Q);
-    const uint32_t uz_s = smem_u32(L.uz);
-    tmem_wait_st();
-#pragma unroll 1
-    for (int m = 0; m < 4; ++m) {
-        const uint32_t sel = 0x4440u | uint32_t(m);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            uint32_t v[16];
-            tmem_ld16(acc.taddr + 16u * uint32_t(2 * m + h), v);
-            double2 c[4];
-            double f[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                c[r] = lds_d2(crot_s + __byte_perm(R[4 * h + r], 0u, sel));
-                f[r] = lds_d(uz_s + __byte_perm(Q[4 * h + r], 0u, sel));
-            }
-            tmem_wait_ld();
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                double2 o = v2d(v + 4 * r);
-                o.x = fma(c[r].x, f[r], o.x);
-                o.y = fma(c[r].y, f[r], o.y);
-                d2v(o, v + 4 * r);
-            }
-            tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
-        }
     }
 }
 
