@@ -288,10 +288,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs (tests/test_gpu_runtime.py): PZX_BENCH_DEVICE pins every rank to
+    # one GPU and PZX_BENCH_BACKEND=gloo runs the host-side collectives without
+    # NCCL, so the multi-rank path can be exercised on a one-GPU box (the ranks'
+    # kernels never wait on one another); the default is one GPU per rank + NCCL
+    dev = int(os.environ.get("PZX_BENCH_DEVICE", local))
+    backend = os.environ.get("PZX_BENCH_BACKEND", "nccl")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(dev)
     peaks, peaks_kind = load_peaks()
 

@@ -215,3 +215,36 @@ def test_term_split_gpu_partials_over_gloo(world):
     assert np.max(np.abs(summed - full)) <= 1e-12 * scale
     assert np.max(np.abs(det - full)) <= 1e-12 * scale
     assert np.array_equal(ex, full_ex)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("impl", ["ours", "reference"])
+def test_bench_two_ranks_one_json_line(impl):
+    """bench.py under torchrun with 2 ranks (the driver's N > 1 launch), both
+    ranks pinned to the box's one GPU with gloo host collectives: rank 0 alone
+    prints ONE JSON line; ours reports the whole job (n_gpus 2, both shards of
+    the C2r batch) with the host-buffer leg equal to the device-resident run;
+    the reference arm runs on rank 0 only and the other rank exits 0."""
+    import json
+    env = dict(os.environ, PZX_BENCH_BACKEND="gloo", PZX_BENCH_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", "c2r", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    if impl == "reference":
+        cmd += ["--impl", "reference", "--ref-per-thread", "1"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["n_gpus"] == 2
+    if impl == "ours":
+        assert d["e2e"]["matches_device_run"] is True and d["gpu_launches"] > 0
+        assert d["roofline"]["kernel"]["kernel"] == "page" and 0 < d["roofline"]["frac"] < 1
+    else:
+        assert d["impl"] == "reference"
