@@ -1541,20 +1541,23 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
 // Enumerated batches (all 2^P amplitudes, contiguous sweeps; n_params <= 32) on
 // the PAGE layout (pzx_host.cpp, page_term): pages of
 // kPageSlots 32-byte records, terms never straddling a page, each term a
-// header (its constant) + constraint (C), generic (G) and dispatch (D) rows.
-// A thread owns 32 assignments (bit-sliced as in k_eval_slice), a warp 1024
-// consecutive ones, base_w + 32 lane + g. Per page and warp, a pre-pass
-// resolves the parity of every row mask against the warp's high bits ONCE per
-// row (one POPC per row and warp, spread over the lanes) into a lane word
+// header (its constant) + constraint (C), generic (G, by update class), lambda
+// (L) and dispatch (D) rows. A thread owns 32 assignments (bit-sliced as in
+// k_eval_slice), a warp 1024 consecutive ones, base_w + 32 lane + g. Per page,
+// a pre-pass (split over the CTA's warps) resolves the parity of every row mask
+// against each warp's high bits ONCE per row and warp into a lane word
 //   M = LW(mask bits 5..9) ^ -parity(mask & base_w)     (bit l: lane l's parity)
 // so the row loops form X = parity ? ~W : W with a predicate test of M and a
 // SEL -- no per-thread POPC. Per row and warp:
 //   C: Z |= X                                            (6 instructions)
-//   G: J += (k + 4p)q~, branch-free, by update class     (~7-16, no jump)
-//   L: J += k p, S += p ^ inv (single-parity lambda rows) (~20, no jump)
+//   G: J += (k + 4p)q~, one loop per update class        (~5.5-12, no jump)
+//   L: J += k p, S += p ^ inv (single-parity lambda rows) (~22, no jump)
 //   D: the generated class body through the jump table   (the slice kernel's)
 // After a term's C rows a warp whose 1024 assignments are all zero skips the
-// rest of the term (constraint-first order, PAPER "Conclusions").
+// rest of the term (constraint-first order, PAPER "Conclusions"). Epilogues:
+// pi terms through the warp's T[j, a, b] table (page_epilogue_pi), lambda-only
+// terms through crot[j] * uz (page_epilogue_lam), the rest slice_epilogue_apply.
+// Knobs (A/B builds): -DPZX_PI_TAB=0, -DPZX_CTA_PREPASS=0.
 __host__ __device__ constexpr uint32_t page_lut_offset() { return 2 * kPageSlots * 32 + 16; }
 
 // Page-kernel epilogue of a term with pi / pi' rows (fast counters): the warp
