@@ -413,10 +413,9 @@ int page_term(HostTable& h, const C128& cpp) {
     // families in record order: 0 C, 1 G, 2 L, 3 D
     std::vector<PageRec> recs;
     recs.reserve(h.pend.size());
-    int n_lam = 0, n_l = 0;  // rows that can bump the lambda counter / L candidates
+    int n_lam = 0;  // rows that can bump the lambda counter
     for (const auto& pr : h.pend) {
         recs.push_back(classify_page_row(pr.psi, pr.phi, pr.op));
-        n_l += recs.back().fam == 5;
         n_lam += (kSliceKindFlags[pr.op] & int(kSliceLamFlag)) != 0;
     }
     // the L loop keeps the lambda counter in its 4 register planes: a term
@@ -438,7 +437,6 @@ int page_term(HostTable& h, const C128& cpp) {
         if (f == 3) h.page_d_ops[h.pend[i].op] += 1;
         fam[f].push_back(r);
     }
-    (void)n_l;
     h.pend.clear();
     // G rows by update cost (k = the record's K0 | K1 << 1; single rows have x-mask 0, X = K2):
     //   0 S2: single, J += 2q        1 S6: single, J += 6q        (J2 ^= q & J1 (~J1); J1 ^= q)
