@@ -186,7 +186,11 @@ pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5
                                int32_t* e_sqrt2, int32_t* n_lm);
 
 /* Synchronous evaluation from HOST buffers: assignments[n] -> amp[2n]
- * (re,im interleaved; may be NULL) and prob[n] (may be NULL). */
+ * (re,im interleaved; may be NULL) and prob[n] (may be NULL). A small call
+ * (n <= 65536, pinned host buffers, an enumerated or contiguous batch)
+ * repeated with the same arguments is captured into a CUDA graph on its
+ * second occurrence and replayed from the third (the word contents are read
+ * at every replay); PZX_NO_GRAPHS=1 disables this. */
 pzx_status pzx_evaluate(pzx_ctx* ctx, const pzx_table* t, const uint64_t* assignments,
                         uint64_t n, double* amp, double* prob, uint32_t flags);
 /* Enumerated batch first, first+1, ..., first+n-1 (generated on device). */

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -860,11 +861,24 @@ struct pzx_ctx {
     cudaMemPool_t pool = nullptr;
     // what the last evaluation launched (pzx_last_kernel; bench.py's roofline)
     int last_kernel = 0, last_groups = 0, last_chunks = 0;
+    // small host-buffer calls repeated with the same arguments replay one CUDA
+    // graph (H2D + kernels + D2H) instead of re-issuing every API call
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;  // this library's kernels per replay
+        int kernel = 0, groups = 0, chunks = 0;
+        void *d_asg = nullptr, *d_amp = nullptr, *d_prob = nullptr;  // scratch the graph was captured on
+        int seen = 0;
+    };
+    std::map<std::vector<uint64_t>, GraphEntry> graphs;
 };
+
+std::atomic<uint64_t> g_table_gen{1};
 
 struct pzx_table {
     pzx_ctx* ctx = nullptr;
     int device = 0;
+    uint64_t gen = g_table_gen.fetch_add(1);  // unique per table object (graph-cache keys)
     DevTable dev;
     HostTable host;
     void* d_rows = nullptr;
@@ -1410,6 +1424,8 @@ void pzx_destroy(pzx_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (void* p : {ctx->d_asg, ctx->d_amp, ctx->d_prob, ctx->d_partial, ctx->d_chunks, ctx->d_dbg, ctx->d_sort, ctx->d_xout})
         if (p) cudaFree(p);
+    for (auto& g : ctx->graphs)
+        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     cudaStreamDestroy(ctx->stream);
     // pending stream-ordered frees on callers' streams: the driver releases
     // the pool once they have completed
@@ -1801,9 +1817,18 @@ pzx_status pzx_table_term_info(const pzx_table* t, uint64_t term, int64_t coef[5
 
 static pzx_status eval_host_impl(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
                                  uint64_t n, double* amp, double* prob, uint32_t flags);
+static pzx_status eval_host_graph(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
+                                  uint64_t n, double* amp, double* prob, uint32_t flags, bool* handled);
 static pzx_status eval_host(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
                             uint64_t n, double* amp, double* prob, uint32_t flags) {
     NvtxRange nv("pzx.evaluate_host (H2D + kernels + D2H)");
+    if (!ctx || !t) return PZX_E_INVALID;
+    if (flags & kNoSyncFlag) return set_err(ctx, PZX_E_INVALID, "evaluate: unknown flag bit");
+    if (t->device >= 0 && t->device == ctx->device) {
+        bool handled = false;
+        const pzx_status st = eval_host_graph(ctx, t, asg, first, n, amp, prob, flags, &handled);
+        if (st || handled) return st;
+    }
     return eval_host_impl(ctx, t, asg, first, n, amp, prob, flags);
 }
 static pzx_status eval_host_impl(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
@@ -1838,9 +1863,95 @@ static pzx_status eval_host_impl(pzx_ctx* ctx, const pzx_table* t, const uint64_
         r.d_prob = static_cast<double*>(ctx->d_prob);
     }
     if (!amp && !prob) return PZX_OK;
-    if ((st = run_eval(ctx, t, r, flags))) return st;
-    if (amp && (st = cuda_err(ctx, cudaMemcpyAsync(amp, ctx->d_amp, n * 16, cudaMemcpyDeviceToHost, ctx->stream), "D2H amplitudes"))) return st;
-    if (prob && (st = cuda_err(ctx, cudaMemcpyAsync(prob, ctx->d_prob, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H probabilities"))) return st;
+    auto enqueue_rest = [&]() -> pzx_status {  // kernels + D2H (the H2D is already enqueued)
+        pzx_status s2;
+        if ((s2 = run_eval(ctx, t, r, flags))) return s2;
+        if (amp && (s2 = cuda_err(ctx, cudaMemcpyAsync(amp, ctx->d_amp, n * 16, cudaMemcpyDeviceToHost, ctx->stream), "D2H amplitudes"))) return s2;
+        if (prob && (s2 = cuda_err(ctx, cudaMemcpyAsync(prob, ctx->d_prob, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H probabilities"))) return s2;
+        return PZX_OK;
+    };
+    if ((st = enqueue_rest())) return st;
+    if (flags & kNoSyncFlag) return PZX_OK;  // (graph capture)
+    return cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "evaluate");
+}
+
+// Small, repeated host-buffer calls (a sampling loop, bench.py's e2e leg):
+// the second identical call (same table object, words / buffers, batch and
+// flags, pinned host memory, enumerated or contiguous-word batch) is captured
+// into a CUDA graph -- H2D, kernels (their stream-ordered scratch as graph
+// allocation nodes), D2H -- and later identical calls replay it: one
+// cudaGraphLaunch instead of every API call. Word CONTENTS may change between
+// calls (the H2D node reads them at replay); the kernel choice depends only on
+// the key. PZX_NO_GRAPHS=1 turns this off.
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PZX_NO_GRAPHS");
+        return !(e && std::string(e) == "1");
+    }();
+    return on;
+}
+
+bool host_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost;
+}
+
+static pzx_status eval_host_graph(pzx_ctx* ctx, const pzx_table* t, const uint64_t* asg, uint64_t first,
+                                  uint64_t n, double* amp, double* prob, uint32_t flags, bool* handled) {
+    *handled = false;
+    constexpr uint64_t kGraphMaxBatch = uint64_t(1) << 16;
+    if (!graphs_enabled() || n == 0 || n > kGraphMaxBatch || (!amp && !prob)) return PZX_OK;
+    if (!host_pinned(asg) || !host_pinned(amp) || !host_pinned(prob)) return PZX_OK;
+    bool contig = true;  // word lists: only contiguous ones (their kernel choice is fixed by asg[0])
+    if (asg)
+        for (uint64_t i = 1; contig && i < n; ++i) contig = asg[i] == asg[0] + i;
+    if (!contig) return PZX_OK;
+    const std::vector<uint64_t> key = {t->gen, uint64_t(reinterpret_cast<uintptr_t>(asg)), asg ? asg[0] : first, n,
+                                       uint64_t(reinterpret_cast<uintptr_t>(amp)),
+                                       uint64_t(reinterpret_cast<uintptr_t>(prob)), flags};
+    auto& g = ctx->graphs[key];
+    pzx_status st;
+    // the device scratch the graph uses (grown first, so a replay sees the same buffers)
+    if (asg && (st = cuda_err(ctx, grow(&ctx->d_asg, &ctx->asg_cap, n * 8), "alloc assignments"))) return st;
+    if (amp && (st = cuda_err(ctx, grow(&ctx->d_amp, &ctx->amp_cap, n * 16), "alloc amplitudes"))) return st;
+    if (prob && (st = cuda_err(ctx, grow(&ctx->d_prob, &ctx->prob_cap, n * 8), "alloc probabilities"))) return st;
+    if (g.exec && (g.d_asg != (asg ? ctx->d_asg : nullptr) || g.d_amp != (amp ? ctx->d_amp : nullptr) ||
+                   g.d_prob != (prob ? ctx->d_prob : nullptr))) {
+        cudaGraphExecDestroy(g.exec);  // a scratch buffer moved since the capture
+        g.exec = nullptr;
+    }
+    if (!g.exec) {
+        if (++g.seen < 2) return PZX_OK;  // capture from the second identical call on
+        if (ctx->graphs.size() > 64) return PZX_OK;
+        const uint64_t l0 = ctx->launches;
+        if ((st = cuda_err(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal), "graph capture")))
+            return PZX_OK;
+        pzx_status cst = eval_host_impl(ctx, t, asg, first, n, amp, prob, flags | kNoSyncFlag);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+        cudaGraphExec_t exec = nullptr;
+        if (cst == PZX_OK && ce == cudaSuccess && graph &&
+            cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+            g.exec = exec;
+            g.launches = ctx->launches - l0;
+            g.kernel = ctx->last_kernel; g.groups = ctx->last_groups; g.chunks = ctx->last_chunks;
+            g.d_asg = asg ? ctx->d_asg : nullptr;
+            g.d_amp = amp ? ctx->d_amp : nullptr;
+            g.d_prob = prob ? ctx->d_prob : nullptr;
+            ctx->launches = l0;  // counted when the graph runs
+        } else {
+            ctx->launches = l0;
+            cudaGetLastError();
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (!g.exec) return PZX_OK;  // not capturable: the plain path runs
+    }
+    if ((st = cuda_err(ctx, cudaGraphLaunch(g.exec, ctx->stream), "graph launch"))) return st;
+    ctx->launches += g.launches;
+    ctx->last_kernel = g.kernel; ctx->last_groups = g.groups; ctx->last_chunks = g.chunks;
+    *handled = true;
     return cuda_err(ctx, cudaStreamSynchronize(ctx->stream), "evaluate");
 }
 

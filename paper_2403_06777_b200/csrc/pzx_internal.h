@@ -87,6 +87,7 @@ struct DevTable {
 
 // page layout (enumerated page kernel): pages of kPageSlots 32-byte records
 constexpr int kPageSlots = 256;
+constexpr uint32_t kNoSyncFlag = 1u << 30;  // internal: enqueue without the final stream sync (graph capture)
 constexpr int kPageGClasses = 6;  // page-layout G rows by update class: S2, S6, E0, E2, G1, G3
 
 constexpr int kSortedGroups = 4;              // 4-bit groups: parameters 0..15 via tables (dense batches)

@@ -248,3 +248,47 @@ def test_bench_two_ranks_one_json_line(impl):
         assert d["roofline"]["kernel"]["kernel"] == "page" and 0 < d["roofline"]["frac"] < 1
     else:
         assert d["impl"] == "reference"
+
+
+def test_repeated_host_calls_replay_a_graph(ctx):
+    """Small host-buffer calls repeated with the same arguments (pinned
+    buffers) are captured into a CUDA graph on the second call and replayed
+    after: results bit-identical to the plain path, the launch count per call
+    unchanged, new word CONTENTS honoured (contiguous, other start; then
+    non-contiguous -> the plain sorted / POPC path)."""
+    import ctypes as C
+    import torch
+    from paper_2403_06777_b200 import _native as NV
+    L = NV.lib()
+    e = synth.generate(12, 400, 0, 30, 77)
+    t = ctx.compile_bit_table(e)
+    n = 1024
+    w = torch.arange(0, n, dtype=torch.int64).pin_memory()
+    amp = torch.empty(2 * n, dtype=torch.float64).pin_memory()
+    prob = torch.empty(n, dtype=torch.float64).pin_memory()
+
+    def call():
+        c0 = ctx.launch_count
+        st = L.pzx_evaluate(ctx.handle, t.handle, C.cast(w.data_ptr(), C.POINTER(C.c_uint64)), n,
+                            C.cast(amp.data_ptr(), NV.dblp), C.cast(prob.data_ptr(), NV.dblp), P.PROB_ABS2)
+        assert st == 0, L.pzx_last_error(ctx.handle).decode()
+        return amp.numpy().copy(), prob.numpy().copy(), ctx.launch_count - c0
+
+    words = np.arange(0, n, dtype=np.uint64)
+    want = ctx.evaluate_batch(t, words)
+    runs = [call() for _ in range(5)]                      # plain, capture, replays
+    for a, p, nl in runs:
+        assert np.array_equal(a.view(np.complex128), want) and nl == runs[0][2] and nl > 0
+        assert np.allclose(p, np.abs(want) ** 2, rtol=1e-14, atol=0) and np.array_equal(p, runs[0][1])
+    w.copy_(torch.arange(2048, 2048 + n, dtype=torch.int64))  # another contiguous range: new key
+    want2 = ctx.evaluate_batch(t, np.arange(2048, 2048 + n, dtype=np.uint64))
+    for _ in range(3):
+        a, _, _ = call()
+        assert np.array_equal(a.view(np.complex128), want2)
+    rnd = np.random.default_rng(5).integers(0, 1 << 12, n, dtype=np.uint64)
+    w.copy_(torch.from_numpy(rnd.view(np.int64)))           # not contiguous: plain path
+    want3 = ctx.evaluate_batch(t, rnd)
+    for _ in range(3):
+        a, _, _ = call()
+        assert np.array_equal(a.view(np.complex128), want3)
+    t.free()
