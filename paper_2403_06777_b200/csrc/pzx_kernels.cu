@@ -109,6 +109,10 @@ constexpr int kTileRows = 256;
 #ifndef PZX_CTA_PREPASS
 #define PZX_CTA_PREPASS 1
 #endif
+// lambda-term epilogue: TMEM loads one group ahead
+#ifndef PZX_EPI_TMEM_PIPE
+#define PZX_EPI_TMEM_PIPE 1
+#endif
 
 // ------------------------------------------------------------- PTX glue ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -932,6 +936,38 @@ __device__ __forceinline__ void page_epilogue_lam(const SmemLut& L, uint32_t cro
     transpose8_bytes(Q);
     const uint32_t uz_s = smem_u32(L.uz);
     tmem_wait_st();
+#if PZX_EPI_TMEM_PIPE
+    // TMEM loads one group of 4 assignments ahead: group k+1's tcgen05.ld is in
+    // flight while group k is looked up and accumulated (two register sets)
+    uint32_t va[16], vb[16];
+    tmem_ld16(acc.taddr, va);
+    auto group = [&](int k, uint32_t (&v)[16], uint32_t (&vn)[16]) {
+        const uint32_t sel = 0x4440u | uint32_t(k >> 1);
+        const int h = k & 1;
+        double2 c[4];
+        double f[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            c[r] = lds_d2(crot_s + __byte_perm(R[4 * h + r], 0u, sel));
+            f[r] = lds_d(uz_s + __byte_perm(Q[4 * h + r], 0u, sel));
+        }
+        tmem_wait_ld();
+        if (k < 7) tmem_ld16(acc.taddr + 16u * uint32_t(k + 1), vn);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 o = v2d(v + 4 * r);
+            o.x = fma(c[r].x, f[r], o.x);
+            o.y = fma(c[r].y, f[r], o.y);
+            d2v(o, v + 4 * r);
+        }
+        tmem_st16(acc.taddr + 16u * uint32_t(k), v);
+    };
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        group(k, va, vb);
+        group(k + 1, vb, va);
+    }
+#else
 #pragma unroll 1
     for (int m = 0; m < 4; ++m) {
         const uint32_t sel = 0x4440u | uint32_t(m);
@@ -957,6 +993,7 @@ __device__ __forceinline__ void page_epilogue_lam(const SmemLut& L, uint32_t cro
             tmem_st16(acc.taddr + 16u * uint32_t(2 * m + h), v);
         }
     }
+#endif
 }
 
 // Term epilogue fast path, TMEM accumulators, transposed decode.
