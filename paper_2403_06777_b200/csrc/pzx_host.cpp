@@ -1004,12 +1004,18 @@ void chunk_bounds(const HostTable& h, uint64_t tb, uint64_t te, int chunks, std:
 // 256 x 37 CTAs, i.e. ~2 -> ~16 waves of the 4 TMEM CTAs an SM holds: the
 // last-wave tail shrinks), while the warp-chunk kernel (C4) loses 35 % with
 // more chunks and keeps 8.
-int grid_waves(bool warp_chunks) {
+// target grid size in waves of resident CTAs (term chunks x assignment blocks);
+// the page kernel's CTAs vary more in duration (warp-level zero skips), so its
+// grid is finer: C2 37 -> 74 term chunks, 190.8 -> 188.3 ms (PZX_WAVES sweep,
+// profiles/README.md r02)
+int grid_waves(int kc) {
     static const int v = [] {
         const char* e = std::getenv("PZX_WAVES");
-        return e ? std::max(1, std::atoi(e)) : 64;
+        return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    return warp_chunks ? 8 : v;
+    if (kc == KC_SLICEWC) return 8;
+    if (v) return v;
+    return kc == KC_PAGE ? 128 : 64;
 }
 
 // chunk-partial scratch bound (bytes); tuning knob PZX_PARTIAL_MIB
@@ -1130,7 +1136,7 @@ pzx_status run_eval(pzx_ctx* ctx, const pzx_table* t, LaunchReq& r, uint32_t fla
     const int ablocks = grid_assign_blocks(t->dev, r, kc);
     const uint64_t nterms = r.term_end - r.term_begin;
     int chunks = 1;
-    const int kWaves = grid_waves(kc == KC_SLICEWC);
+    const int kWaves = grid_waves(kc);
     const int wave = ctx->n_sm * resident_ctas_per_sm(t->dev, kc, slice_threads(r), r.sorted_groups);
     const int target = kWaves * wave;
     if (ablocks < target && nterms > 1) {
