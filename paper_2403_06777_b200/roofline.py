@@ -115,6 +115,27 @@ def min_counts_page(family_rows, d_op_rows, term_kinds, n_assign: int) -> dict:
             "per_term_per_warp": term_inst / max(float(np.sum(kinds)), 1.0)}
 
 
+# Shared-memory wavefronts (1 / clk / SM) of the page kernel's own data movement:
+# a warp-wide 128-bit load with per-lane addresses costs >= 4 wavefronts (one per
+# quarter-warp), a uniform one 2, 64- / 32-bit loads 1-2 (tools/micro/lds128_bcast.cu).
+PAGE_WF_ROW = {"c": 3.0, "s": 2.0, "e": 3.0, "g": 3.0, "l": 5.0, "d": 5.0}  # record + lane word per row-warp
+PAGE_WF_ASSIGN = (4.0, 5.5, 5.5)  # per (term, assignment-warp): crot | crot + uz | T + uz
+
+
+def smem_floor_page(family_rows, term_kinds, n_assign: int) -> float:
+    """Minimum shared-memory wavefronts of one page-kernel launch: the row
+    loops' record / lane-word loads and the epilogue's per-lane table lookups
+    at their conflict-free cost (no pre-pass, no bank conflicts)."""
+    fr = [float(x) for x in family_rows] + [0.0] * 11
+    c, g, d, _dropped, l_ = fr[:5]
+    s_ = fr[5] + fr[6]
+    W = PAGE_WF_ROW
+    rows = W["c"] * c + W["s"] * s_ + W["g"] * (g - s_) + W["l"] * l_ + W["d"] * d
+    kinds = np.asarray(term_kinds, np.float64)
+    terms = float(np.sum(kinds * 32 * np.array(PAGE_WF_ASSIGN)))
+    return n_assign / 1024.0 * (rows + terms)
+
+
 def roofline(op_rows, term_kinds, n_assign: int, seconds: float, f_mhz: float, kernel: str = "slice",
              sorted_groups: int = 4, page_stats=None) -> dict:
     """The bench's `roofline` object: the binding resource of the algorithm's
@@ -143,4 +164,13 @@ def roofline(op_rows, term_kinds, n_assign: int, seconds: float, f_mhz: float, k
                 "min_time_issue_s": t_issue, "min_time_alu_s": t_alu, "min_time_popc_s": t_xu,
                 "min_per_row_per_warp": c["per_row_per_warp"], "min_per_term_per_warp": c["per_term_per_warp"],
                 "kernel_model": kernel if kernel != "sorted" else f"sorted (G={sorted_groups})"})
+    if kernel == "page" and page_stats is not None:
+        # informational: the page kernel against the floor of its own shared-memory
+        # traffic (the pipe ncu shows closest to saturation); frac stays the
+        # conservative instruction minimum above
+        wf = smem_floor_page(page_stats[0], term_kinds, n_assign)
+        t_smem = wf / (N_SM * hz)
+        out["smem_floor"] = {"wavefronts": wf, "time_s": t_smem, "frac": t_smem / seconds,
+                             "note": "conflict-free shared-memory wavefronts of the row loads and epilogue "
+                                     "lookups at 1 / clk / SM; not the reported frac"}
     return out

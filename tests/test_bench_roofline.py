@@ -88,3 +88,15 @@ def test_headline_table_is_alu_bound_and_classes_cover_g():
     ops, kinds = h.slice_stats()
     r = RL.roofline(ops, kinds, 1 << 20, 0.2, 1965.0, "page", page_stats=(fam, d_ops))
     assert r["bound"] == "alu pipe" and 0 < r["frac"] < 1
+
+
+def test_page_smem_floor_is_informational_and_pinned():
+    fam = [10, 40, 2, 5, 4, 8, 2, 10, 10, 6, 4]   # C, G, D, dropped, L | S2, S6, E0, E2, G1, G3
+    kinds = np.array([1, 2, 3])
+    wf = RL.smem_floor_page(fam, kinds, 1024)
+    want = 3 * 10 + 2 * 10 + 3 * 30 + 5 * 4 + 5 * 2 + 32 * (4 * 1 + 5.5 * 2 + 5.5 * 3)
+    assert abs(wf - want) < 1e-9
+    d_ops = np.zeros(129)
+    r = RL.roofline(np.zeros(129), kinds, 1024, 1e-3, 1965.0, "page", page_stats=(fam, d_ops))
+    assert "smem_floor" in r and r["smem_floor"]["frac"] > 0
+    assert r["frac"] == r["achieved"] / r["peak"]            # the reported frac is unchanged
