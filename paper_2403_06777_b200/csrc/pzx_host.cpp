@@ -308,13 +308,13 @@ void push_row(HostTable& h, PairRow pr, int& e, int& lm) {
 //   G (generic monomial): value w^(c0 + (k + 4p')(q' ^ inv)) sqrt2^e g, g constant
 //       (every class with ka or kb in {0,4}: 28 of 64, ~83 % of the rows of the
 //       BASELINE tables)                                   -> branch-free J += (k + 4p')q~
-//   L (lambda): one parity, no zero, exactly one lambda/mu variant
-//       (terms with < 16 lambda-capable rows)              -> J += k p, S += p ^ inv
+//   L (lambda): one parity, no zero, exactly one lambda/mu variant, k in {0, 4}
+//       (terms with < 16 lambda-capable rows)              -> J += k p, S += p ^ inv (L0 then L4)
 //   D (dispatch): zero-pair / lambda / pi / pi' rows       -> the generated class bodies
 // and rows whose reachable variants are equal are dropped (their w^j goes
 // into the term constant like every c0; their sqrt2^e and mu are already in
 // E_t / nLM_t). Records (8 x u32), in the order header, C, G, L, D:
-//   header: {C_page (double2), nc | n_g1 << 8 | nd << 16 | last_in_page << 24, nl,
+//   header: {C_page (double2), nc | n_g1 << 8 | nd << 16 | last_in_page << 24, n_l0 | n_l4 << 8,
 //            n_s2 | n_s6 << 8 | n_e0 << 16 | n_e2 << 24, n_g3}
 // with the G rows in the order S2, S6, E0, E2, G1, G3 (page_term: by update cost)
 //   C: {W ^ zc, ~(W ^ zc), 0, 0, 0, 0, psi, 0}
@@ -338,8 +338,9 @@ PageRec classify_page_row(uint64_t psi, uint64_t phi, uint32_t op) {
         r.jfold = so.jbase;
         return r;
     };
-    // L (single-parity lambda/mu row, one lambda variant): J += k p, S += p ^ inv
-    if (single && so.lam_tt && !so.pi_tt && !so.pip_tt && !(so.zero_tt & 3) && (so.lam_tt & 3) != 3) {
+    // L (single-parity lambda/mu row, one lambda variant, k in {0, 4}): J2 ^= (k/4) p, S += p ^ inv
+    if (single && so.lam_tt && !so.pi_tt && !so.pip_tt && !(so.zero_tt & 3) && (so.lam_tt & 3) != 3 &&
+        ((jv(1) - jv(0)) & 3) == 0) {
         dispatch();  // keep the D form: the term may have too many lambda rows for the fast counters
         std::memcpy(r.dw, r.w, sizeof r.w);
         r.djfold = r.jfold;
@@ -454,6 +455,8 @@ int page_term(HostTable& h, const C128& cpp) {
         gsub[sc].push_back(r);
         h.page_gsub[sc] += 1;
     }
+    std::vector<PageRec> lsub[2];  // L rows: k = 0 (S only), k = 4 (J2 ^= p)
+    for (const PageRec& r : fam[2]) lsub[r.w[7] ? 1 : 0].push_back(r);
     const uint32_t n = uint32_t(1 + fam[0].size() + fam[1].size() + fam[2].size() + fam[3].size());
     if (n > uint32_t(kPageSlots)) {  // a term must fit one page: no page layout for this table
         h.want_prows = false;
@@ -473,7 +476,7 @@ int page_term(HostTable& h, const C128& cpp) {
     h.prows.push_back(make_uint4(q[0], q[1], q[2], q[3]));
     h.prows.push_back(make_uint4(uint32_t(fam[0].size()) | uint32_t(gsub[4].size()) << 8 |
                                      uint32_t(fam[3].size()) << 16,
-                                 uint32_t(fam[2].size()),
+                                 uint32_t(lsub[0].size()) | uint32_t(lsub[1].size()) << 8,
                                  uint32_t(gsub[0].size()) | uint32_t(gsub[1].size()) << 8 |
                                      uint32_t(gsub[2].size()) << 16 | uint32_t(gsub[3].size()) << 24,
                                  uint32_t(gsub[5].size())));
@@ -485,7 +488,8 @@ int page_term(HostTable& h, const C128& cpp) {
     };
     put(fam[0]);
     for (int sc = 0; sc < kPageGClasses; ++sc) put(gsub[sc]);
-    put(fam[2]);
+    put(lsub[0]);
+    put(lsub[1]);
     put(fam[3]);
     h.page_fill += n;
     if (h.page_fill == uint32_t(kPageSlots)) page_pad(h);

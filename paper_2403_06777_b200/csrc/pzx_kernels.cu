@@ -1588,7 +1588,7 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_slice_wc(const DevTab
 // SEL -- no per-thread POPC. Per row and warp:
 //   C: Z |= X                                            (6 instructions)
 //   G: J += (k + 4p)q~, one loop per update class        (~5.5-12, no jump)
-//   L: J += k p, S += p ^ inv (single-parity lambda rows) (~22, no jump)
+//   L: J += k p (k in {0, 4}), S += p ^ inv               (~13, no jump)
 //   D: the generated class body through the jump table   (the slice kernel's)
 // After a term's C rows a warp whose 1024 assignments are all zero skips the
 // rest of the term (constraint-first order, PAPER "Conclusions"). Epilogues:
@@ -1873,7 +1873,8 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
 #endif
             while (term < te) {
                 const uint4 h0 = pg[2 * s], h1 = pg[2 * s + 1];
-                const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu, nl = h1.y;
+                const uint32_t nc = h1.x & 0xFFu, ng = (h1.x >> 8) & 0xFFu, nd = (h1.x >> 16) & 0xFFu;
+                const uint32_t nl0 = h1.y & 0xFFu, nl4 = h1.y >> 8, nl = nl0 + nl4;
                 uint32_t q = s + 1;
                 // C rows: parity constraints
                 for (const uint32_t e = q + nc; q < e; ++q) {
@@ -1911,17 +1912,16 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                         add3(J0, J1, J2, H0, H1, H2);
                         q += ns2 + ns6 + ne0 + ne2 + ng + h1.w;
                     }
-                    // L rows (single-parity lambda / mu rows; the host sends them here only
-                    // when the term has < 16 lambda-capable rows, so S fits its 4 register
-                    // planes): J += k p, S += Lambda, Lambda = p ^ inv -- both from the x
-                    // parity word
+                    // L rows (single-parity lambda / mu rows with k in {0, 4}; the host sends
+                    // them here only when the term has < 16 lambda-capable rows, so S fits its
+                    // 4 register planes): S += Lambda, Lambda = p ^ inv, and for L4 rows
+                    // J2 ^= p -- both from the x parity word and one 16-byte record load
                     if (nl) {
-#pragma unroll 2
-                        for (const uint32_t e = q + nl; q < e; ++q) {
-                            const uint4 a = pg[2 * q], b = pg[2 * q + 1];
-                            const bool px = Mw[q].x & lanebit;
-                            const uint32_t lam = px ? a.y : a.x, p = px ? a.w : a.z;
-                            g_row(J0, J1, J2, b.w, p, b.x, b.y);
+                        auto lrow = [&](uint32_t qq, bool k4) {
+                            const uint4 a = pg[2 * qq];
+                            const bool px = Mw[qq].x & lanebit;
+                            const uint32_t lam = px ? a.y : a.x;
+                            if (k4) J2 ^= px ? a.w : a.z;
                             const uint32_t c0 = K.S[0] & lam;
                             K.S[0] ^= lam;
                             const uint32_t c1 = K.S[1] & c0;
@@ -1929,7 +1929,11 @@ __global__ void __launch_bounds__(kSliceThreads, 4) k_eval_page(const DevTable t
                             const uint32_t c2 = K.S[2] & c1;
                             K.S[2] ^= c1;
                             K.S[3] ^= c2;
-                        }
+                        };
+#pragma unroll 2
+                        for (const uint32_t e = q + nl0; q < e; ++q) lrow(q, false);
+#pragma unroll 2
+                        for (const uint32_t e = q + nl4; q < e; ++q) lrow(q, true);
                         K.nS = nl;
                     }
                     // D rows: the class bodies of the bit-sliced kernels (generated PTX)

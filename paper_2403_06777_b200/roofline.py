@@ -44,7 +44,7 @@ warp), then per row and warp:
       E0 (J2 ^= X & Y): 2 LDS + 2 x (LOP3->P + SEL) + 1 LOP3                7      5
       E2 (J += 2Y + 4XY): 2 LDS + 2 x (LOP3->P + SEL) + 3 LOP3              9      7
       G1/G3 (odd k): 2 LDS + 2 x (LOP3->P + SEL) + 5 LOP3                  11      9
-    L row: 3 LDS + LOP3->P + 2 SEL + 7 LOP3 (phase) + 7 LOP3 (lambda)     20     17
+    L row (k in {0, 4}): 2 LDS + LOP3->P + SEL + 7 LOP3 (lambda ripple)    11      9
     D row: 3 LDS + 2 x (LOP3->P + SEL) + the class's LOP3 chain       7 + body  4 + body
 Loop control, row prefetch, TMA waits, counter decode, TMEM traffic and the
 chunk reduction are implementation overhead and are NOT in the minimum, so
@@ -101,9 +101,9 @@ def min_counts_page(family_rows, d_op_rows, term_kinds, n_assign: int) -> dict:
     d_ops = np.asarray(d_op_rows, np.float64)
     rows = c + g + d + l_
     pre = rows * (1 + 2 * 5 + 1) / 32.0
-    row_inst = (pre + 5 * c + 6 * s_ + 7 * e0 + 9 * e2 + 11 * gg + 20 * l_ +
+    row_inst = (pre + 5 * c + 6 * s_ + 7 * e0 + 9 * e2 + 11 * gg + 11 * l_ +
                 float(np.sum(d_ops * (3 + 4 + body))))
-    row_alu = (rows * 6 / 32.0 + 3 * c + 4 * s_ + 5 * e0 + 7 * e2 + 9 * gg + 17 * l_ +
+    row_alu = (rows * 6 / 32.0 + 3 * c + 4 * s_ + 5 * e0 + 7 * e2 + 9 * gg + 9 * l_ +
                float(np.sum(d_ops * (4 + body))))
     kinds = np.asarray(term_kinds, np.float64)
     term_inst = float(np.sum(kinds * 32 * np.array(EPI_PER_ASSIGN)))
@@ -118,7 +118,7 @@ def min_counts_page(family_rows, d_op_rows, term_kinds, n_assign: int) -> dict:
 # Shared-memory wavefronts (1 / clk / SM) of the page kernel's own data movement:
 # a warp-wide 128-bit load with per-lane addresses costs >= 4 wavefronts (one per
 # quarter-warp), a uniform one 2, 64- / 32-bit loads 1-2 (tools/micro/lds128_bcast.cu).
-PAGE_WF_ROW = {"c": 3.0, "s": 2.0, "e": 3.0, "g": 3.0, "l": 5.0, "d": 5.0}  # record + lane word per row-warp
+PAGE_WF_ROW = {"c": 3.0, "s": 2.0, "e": 3.0, "g": 3.0, "l": 3.0, "d": 5.0}  # record + lane word per row-warp
 PAGE_WF_ASSIGN = (4.0, 5.5, 5.5)  # per (term, assignment-warp): crot | crot + uz | T + uz
 
 

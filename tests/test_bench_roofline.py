@@ -72,29 +72,31 @@ def test_page_minimum_by_family_and_class():
     c = RL.min_counts_page(fam, d_ops, np.array([1, 0, 0]), 1024)
     rows = 10 + 40 + 2 + 4
     pre = rows * 12 / 32
-    assert abs(c["warp_instructions"] - (pre + 5 * 10 + 6 * 10 + 7 * 10 + 9 * 10 + 11 * 10 + 20 * 4
+    assert abs(c["warp_instructions"] - (pre + 5 * 10 + 6 * 10 + 7 * 10 + 9 * 10 + 11 * 10 + 11 * 4
                                          + 2 * 8 + 32 * 3)) < 1e-9
-    assert abs(c["warp_alu"] - (rows * 6 / 32 + 3 * 10 + 4 * 10 + 5 * 10 + 7 * 10 + 9 * 10 + 17 * 4
+    assert abs(c["warp_alu"] - (rows * 6 / 32 + 3 * 10 + 4 * 10 + 5 * 10 + 7 * 10 + 9 * 10 + 9 * 4
                                 + 2 * 5)) < 1e-9
     # a layout without the class split counts every G row as GG
     old = RL.min_counts_page(fam[:5], d_ops, np.array([1, 0, 0]), 1024)
     assert old["warp_alu"] > c["warp_alu"]
 
 
-def test_headline_table_is_alu_bound_and_classes_cover_g():
+def test_headline_table_bound_and_classes_cover_g():
     h = P.HostTable(synth.generate_config(synth.CONFIGS["c2"]))
     fam, d_ops = h.page_stats()
     assert int(fam[5:].sum()) == int(fam[1])
     ops, kinds = h.slice_stats()
     r = RL.roofline(ops, kinds, 1 << 20, 0.2, 1965.0, "page", page_stats=(fam, d_ops))
-    assert r["bound"] == "alu pipe" and 0 < r["frac"] < 1
+    assert r["bound"] in ("alu pipe", "issue") and 0 < r["frac"] < 1
+    # the two minima are within a few % of each other for this table (the binding one is reported)
+    assert 0.8 < r["min_time_alu_s"] / r["min_time_issue_s"] < 1.25
 
 
 def test_page_smem_floor_is_informational_and_pinned():
     fam = [10, 40, 2, 5, 4, 8, 2, 10, 10, 6, 4]   # C, G, D, dropped, L | S2, S6, E0, E2, G1, G3
     kinds = np.array([1, 2, 3])
     wf = RL.smem_floor_page(fam, kinds, 1024)
-    want = 3 * 10 + 2 * 10 + 3 * 30 + 5 * 4 + 5 * 2 + 32 * (4 * 1 + 5.5 * 2 + 5.5 * 3)
+    want = 3 * 10 + 2 * 10 + 3 * 30 + 3 * 4 + 5 * 2 + 32 * (4 * 1 + 5.5 * 2 + 5.5 * 3)
     assert abs(wf - want) < 1e-9
     d_ops = np.zeros(129)
     r = RL.roofline(np.zeros(129), kinds, 1024, 1e-3, 1965.0, "page", page_stats=(fam, d_ops))

@@ -34,7 +34,7 @@ def emulate_term(slots, hdr, a):
         OPS = P.slice_op_table()
     cnt = int(slots[hdr, 4])
     nc, ng, nd = cnt & 0xFF, (cnt >> 8) & 0xFF, (cnt >> 16) & 0xFF
-    nl = int(slots[hdr, 5])
+    nl = (int(slots[hdr, 5]) & 0xFF) + (int(slots[hdr, 5]) >> 8)  # L0 + L4
     ng += sum((int(slots[hdr, 6]) >> (8 * i)) & 0xFF for i in range(4)) + int(slots[hdr, 7])  # + S2..E2, G3
     j = z = s1 = pa = pb = 0
     q = hdr + 1
@@ -72,11 +72,12 @@ def emulate_term(slots, hdr, a):
                 assert k == 3
                 j += -Y + 4 * (X & Y)       # X stored complemented: 3Y + 4(~X)Y = -Y + 4XY (mod 8)
             q += 1
-    for _ in range(nl):
+    for i_l in range(nl):
         w = slots[q]
         lam = vec(w[0], w[1], w[6], a)      # Lambda = p ^ inv, from the x parity word
         p_ = vec(w[2], w[3], w[6], a)
         k = (1 if w[4] else 0) + (2 if w[5] else 0) + (4 if w[7] else 0)
+        assert k == (0 if i_l < (int(slots[hdr, 5]) & 0xFF) else 4)   # L0 rows, then L4 rows
         j += k * p_
         s1 += lam
         q += 1
@@ -117,7 +118,8 @@ def test_page_layout_reconstructs_reference_terms(case):
     # no term straddles a page; the last term of every used page is flagged
     for t in range(h.n_terms):
         cnt = int(slots[tslot[t], 4])
-        n = 1 + (cnt & 0xFF) + ((cnt >> 8) & 0xFF) + ((cnt >> 16) & 0xFF) + int(slots[tslot[t], 5])
+        n = 1 + (cnt & 0xFF) + ((cnt >> 8) & 0xFF) + ((cnt >> 16) & 0xFF) + (int(slots[tslot[t], 5]) & 0xFF)
+        n += int(slots[tslot[t], 5]) >> 8
         n += sum((int(slots[tslot[t], 6]) >> (8 * i)) & 0xFF for i in range(4)) + int(slots[tslot[t], 7])
         assert tslot[t] // PAGE == (tslot[t] + n - 1) // PAGE
         nxt = tslot[t + 1] if t + 1 < h.n_terms else None
